@@ -1,0 +1,839 @@
+/*
+ * nb_oracle.c -- TEST INFRASTRUCTURE ONLY: the parity oracle for the B200 path.
+ *
+ * A plain, slow, single-threaded CPU implementation of what the hot path
+ * computes, written from the paper and the readings of SURVEY.md §8(c)
+ * (listed in DESIGN.md §3).  Only tests/, __graft_entry__.smoke() and
+ * bench.py's CPU-baseline legs may load it; the product path
+ * (paper_2503_02134_b200/) never does.  No code is shared with the CUDA path.
+ *
+ * Paper passages followed (PAPER.md line numbers):
+ *   - Nekbone CG loop, Table 2 (:158-168): solveM, glsc3 (beta), add2s1, ax,
+ *     glsc3 (pap), add2s2 x2, glsc3 (rtr).
+ *   - ax -> local_grad3 / local_grad3_t / mxm / add2, call graph (:147).
+ *   - gather-scatter "ensure continuity" on an unassembled per-element
+ *     matrix (:404), GS precision as the stagnation mechanism (:339-341, :429-431).
+ *   - Jacobi J^-1 = 1/diag(A), one-time cast (:444).
+ *   - mixed policy: fp32 loop, fp64 dots + gather-scatter + init (:53, :537).
+ *
+ * Compiled -O2 -ffp-contract=off -fno-fast-math: no FMA contraction, C float
+ * and double exactly as each policy states.
+ *
+ * Parity pins live in tests/test_oracle_*.py (closed forms, dense assembly,
+ * patch test, spectral convergence, dense solve, stagnation).
+ */
+#include "nb_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+struct or_mesh {
+    int nelx, nely, nelz, p, n;
+    int64_t E, NL, NX, NY, NZ, NG;
+    int64_t n_unmasked, n_shared_global, n_shared_copies;
+    double z[16], w[16], D[256];   /* GLL nodes, weights, D[i*n+j] */
+    float Df[256];                 /* one-time float cast of D */
+    double *xyz;                   /* 3*NL, factor-major */
+    double *jac;                   /* NL */
+    double *g;                     /* 6*NL factor-major g1..g6 (C-6 ordering) */
+    float *gf;                     /* one-time float cast */
+    double *B;                     /* NL */
+    int64_t *gid;                  /* NL */
+    uint8_t *mask;                 /* NL */
+    double *c;                     /* NL, 1/multiplicity */
+    float *cf;
+    int32_t nseg;
+    int32_t *off, *idx;            /* GS CSR */
+    double *dinv;                  /* NL fp64 */
+    float *dinvf;                  /* one-time float cast */
+};
+
+/* ------------------------------------------------------------------ */
+/* C-1: GLL basis                     */
+/* ------------------------------------------------------------------ */
+
+/* Legendre P_p(x) and P_{p-1}(x) by the three-term recurrence. */
+static void legendre(int p, double x, double *Pp, double *Ppm1)
+{
+    double P0 = 1.0, P1 = x;
+    if (p == 0) { *Pp = 1.0; *Ppm1 = 0.0; return; }
+    for (int k = 2; k <= p; k++) {
+        double P2 = ((2.0 * k - 1.0) * x * P1 - (k - 1.0) * P0) / k;
+        P0 = P1;
+        P1 = P2;
+    }
+    *Pp = P1;
+    *Ppm1 = P0;
+}
+
+int or_gll(int p, double *nodes, double *weights, double *D)
+{
+    if (p < 1 || p > 15) return 1;
+    const int n = p + 1;
+    const double pi = 3.14159265358979323846;
+    /* Newton on f(x) = (1-x^2) P_p'(x) = p (P_{p-1} - x P_p), f'(x) = -p(p+1) P_p(x)
+       (Legendre ODE), from x_i = -cos(pi i / p); stop at |dx| < 1e-16 (100 its max). */
+    for (int i = 0; i < n; i++) {
+        double x = -cos(pi * i / p);
+        if (i == 0) x = -1.0;
+        if (i == p) x = 1.0;
+        int it = 0;
+        for (; it < 100; it++) {
+            double Pp, Pm;
+            legendre(p, x, &Pp, &Pm);
+            double dx = (Pm - x * Pp) / ((p + 1.0) * Pp);
+            x += dx;
+            if (fabs(dx) < 1e-16) break;
+        }
+        if (it == 100) {
+            /* rounding can leave |dx| oscillating at ~1 ulp; accept if f(x) is at roundoff */
+            double Pp, Pm;
+            legendre(p, x, &Pp, &Pm);
+            if (fabs(Pm - x * Pp) > 1e-13) return 2;
+        }
+        nodes[i] = x;
+    }
+    /* weights w_i = 2 / (p(p+1) P_p(x_i)^2) */
+    double Pn[16];
+    for (int i = 0; i < n; i++) {
+        double Pp, Pm;
+        legendre(p, nodes[i], &Pp, &Pm);
+        Pn[i] = Pp;
+        weights[i] = 2.0 / (p * (p + 1.0) * Pp * Pp);
+    }
+    /* D_ij = P_p(x_i) / (P_p(x_j) (x_i - x_j)), i != j; D_ii = -sum_{j!=i} D_ij (C-1 reading) */
+    for (int i = 0; i < n; i++) {
+        double s = 0.0;
+        for (int j = 0; j < n; j++) {
+            if (j == i) continue;
+            D[i * n + j] = Pn[i] / (Pn[j] * (nodes[i] - nodes[j]));
+            s += D[i * n + j];
+        }
+        D[i * n + i] = -s;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* C-5: counter-based SplitMix64                                        */
+/* ------------------------------------------------------------------ */
+
+uint64_t or_splitmix64(uint64_t seed, uint64_t stream, uint64_t i)
+{
+    uint64_t z = (seed ^ (stream * 0xD1B54A32D192ED03ull)) + (i + 1ull) * 0x9E3779B97F4A7C15ull;
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+
+double or_prng_u(uint64_t seed, uint64_t stream, uint64_t i)
+{
+    uint64_t z = or_splitmix64(seed, stream, i);
+    return (double)(z >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
+}
+
+/* ------------------------------------------------------------------ */
+/* helpers                                                              */
+/* ------------------------------------------------------------------ */
+
+/* local index l -> element e and (i,j,k) ; C-4: l = e n^3 + i + n j + n^2 k */
+static void split_local(const or_mesh *m, int64_t l, int64_t *e, int *i, int *j, int *k)
+{
+    int64_t n3 = (int64_t)m->n * m->n * m->n;
+    *e = l / n3;
+    int64_t r = l % n3;
+    *i = (int)(r % m->n);
+    *j = (int)((r / m->n) % m->n);
+    *k = (int)(r / ((int64_t)m->n * m->n));
+}
+
+static void element_xyz(const or_mesh *m, int64_t e, int *ex, int *ey, int *ez)
+{
+    *ex = (int)(e % m->nelx);
+    *ey = (int)((e / m->nelx) % m->nely);
+    *ez = (int)(e / ((int64_t)m->nelx * m->nely));
+}
+
+/* C-3: deformed vertex position */
+static void vertex_pos(int ix, int iy, int iz, int nelx, int nely, int nelz, double amp,
+                       const double phi[3], double out[3])
+{
+    const double pi = 3.14159265358979323846;
+    double X = (double)ix / nelx, Y = (double)iy / nely, Z = (double)iz / nelz;
+    out[0] = X;
+    out[1] = Y;
+    out[2] = Z;
+    if (amp == 0.0) return;
+    if (ix == 0 || ix == nelx || iy == 0 || iy == nely || iz == 0 || iz == nelz) return;
+    double bubble = sin(pi * X) * sin(pi * Y) * sin(pi * Z);
+    const int kv[3][3] = {{1, 2, 1}, {2, 1, 1}, {1, 1, 2}};
+    const double h[3] = {1.0 / nelx, 1.0 / nely, 1.0 / nelz};
+    for (int a = 0; a < 3; a++) {
+        double kdot = kv[a][0] * X + kv[a][1] * Y + kv[a][2] * Z;
+        out[a] += amp * h[a] * bubble * cos(2.0 * pi * kdot + phi[a]);
+    }
+}
+
+/* ------------------------------------------------------------------ */
+/* mesh setup (C-2 .. C-9)                                              */
+/* ------------------------------------------------------------------ */
+
+void or_mesh_free(or_mesh *m)
+{
+    if (!m) return;
+    free(m->xyz); free(m->jac); free(m->g); free(m->gf); free(m->B); free(m->gid);
+    free(m->mask); free(m->c); free(m->cf); free(m->off); free(m->idx); free(m->dinv); free(m->dinvf);
+    free(m);
+}
+
+or_mesh *or_mesh_new(int nelx, int nely, int nelz, int p, double deform_amp, uint64_t seed)
+{
+    if (nelx < 1 || nely < 1 || nelz < 1 || p < 1 || p > 15) return NULL;
+    or_mesh *m = (or_mesh *)calloc(1, sizeof(or_mesh));
+    m->nelx = nelx; m->nely = nely; m->nelz = nelz; m->p = p; m->n = p + 1;
+    const int n = m->n;
+    const int64_t n3 = (int64_t)n * n * n;
+    m->E = (int64_t)nelx * nely * nelz;
+    m->NL = m->E * n3;
+    m->NX = (int64_t)nelx * p + 1; m->NY = (int64_t)nely * p + 1; m->NZ = (int64_t)nelz * p + 1;
+    m->NG = m->NX * m->NY * m->NZ;
+    if (m->NL >= 2147483647LL) { free(m); return NULL; }
+    if (or_gll(p, m->z, m->w, m->D)) { free(m); return NULL; }
+    for (int a = 0; a < n * n; a++) m->Df[a] = (float)m->D[a];
+
+    const int64_t NL = m->NL;
+    m->xyz = (double *)malloc(3 * NL * sizeof(double));
+    m->jac = (double *)malloc(NL * sizeof(double));
+    m->g = (double *)malloc(6 * NL * sizeof(double));
+    m->gf = (float *)malloc(6 * NL * sizeof(float));
+    m->B = (double *)malloc(NL * sizeof(double));
+    m->gid = (int64_t *)malloc(NL * sizeof(int64_t));
+    m->mask = (uint8_t *)malloc(NL);
+    m->c = (double *)malloc(NL * sizeof(double));
+    m->cf = (float *)malloc(NL * sizeof(float));
+    m->dinv = (double *)malloc(NL * sizeof(double));
+    m->dinvf = (float *)malloc(NL * sizeof(float));
+
+    /* C-3 phases */
+    double phi[3];
+    const double pi = 3.14159265358979323846;
+    for (int a = 0; a < 3; a++) phi[a] = pi * (1.0 + or_prng_u(seed, 3, (uint64_t)a));
+
+    /* C-2/C-3: GLL node coordinates by trilinear interpolation of the 8 moved vertices */
+    int ok = 1;
+    for (int64_t e = 0; e < m->E; e++) {
+        int ex, ey, ez;
+        element_xyz(m, e, &ex, &ey, &ez);
+        double V[2][2][2][3];
+        for (int cz = 0; cz < 2; cz++)
+            for (int cy = 0; cy < 2; cy++)
+                for (int cx = 0; cx < 2; cx++)
+                    vertex_pos(ex + cx, ey + cy, ez + cz, nelx, nely, nelz, deform_amp, phi, V[cz][cy][cx]);
+        double *X = m->xyz, *Y = m->xyz + NL, *Z = m->xyz + 2 * NL;
+        for (int k = 0; k < n; k++)
+            for (int j = 0; j < n; j++)
+                for (int i = 0; i < n; i++) {
+                    double Nx[2] = {(1.0 - m->z[i]) / 2.0, (1.0 + m->z[i]) / 2.0};
+                    double Ny[2] = {(1.0 - m->z[j]) / 2.0, (1.0 + m->z[j]) / 2.0};
+                    double Nz[2] = {(1.0 - m->z[k]) / 2.0, (1.0 + m->z[k]) / 2.0};
+                    double pos[3] = {0.0, 0.0, 0.0};
+                    for (int cz = 0; cz < 2; cz++)
+                        for (int cy = 0; cy < 2; cy++)
+                            for (int cx = 0; cx < 2; cx++)
+                                for (int a = 0; a < 3; a++)
+                                    pos[a] += Nx[cx] * Ny[cy] * Nz[cz] * V[cz][cy][cx][a];
+                    int64_t l = e * n3 + i + n * j + (int64_t)n * n * k;
+                    X[l] = pos[0]; Y[l] = pos[1]; Z[l] = pos[2];
+                }
+        /* C-6: Jacobian via D, G = W J R R^T, B = W J */
+        for (int k = 0; k < n; k++)
+            for (int j = 0; j < n; j++)
+                for (int i = 0; i < n; i++) {
+                    int64_t l = e * n3 + i + n * j + (int64_t)n * n * k;
+                    double M[3][3]; /* M[a][b] = d x_a / d r_b */
+                    const double *F[3] = {X, Y, Z};
+                    for (int a = 0; a < 3; a++) {
+                        double dr = 0.0, ds = 0.0, dt = 0.0;
+                        for (int q = 0; q < n; q++) {
+                            dr += m->D[i * n + q] * F[a][e * n3 + q + n * j + (int64_t)n * n * k];
+                            ds += m->D[j * n + q] * F[a][e * n3 + i + n * q + (int64_t)n * n * k];
+                            dt += m->D[k * n + q] * F[a][e * n3 + i + n * j + (int64_t)n * n * q];
+                        }
+                        M[a][0] = dr; M[a][1] = ds; M[a][2] = dt;
+                    }
+                    double det = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1])
+                               - M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0])
+                               + M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+                    if (!(det > 0.0)) ok = 0;
+                    double R[3][3]; /* R[a][b] = d r_a / d x_b = inverse of M */
+                    R[0][0] = (M[1][1] * M[2][2] - M[1][2] * M[2][1]) / det;
+                    R[0][1] = (M[0][2] * M[2][1] - M[0][1] * M[2][2]) / det;
+                    R[0][2] = (M[0][1] * M[1][2] - M[0][2] * M[1][1]) / det;
+                    R[1][0] = (M[1][2] * M[2][0] - M[1][0] * M[2][2]) / det;
+                    R[1][1] = (M[0][0] * M[2][2] - M[0][2] * M[2][0]) / det;
+                    R[1][2] = (M[0][2] * M[1][0] - M[0][0] * M[1][2]) / det;
+                    R[2][0] = (M[1][0] * M[2][1] - M[1][1] * M[2][0]) / det;
+                    R[2][1] = (M[0][1] * M[2][0] - M[0][0] * M[2][1]) / det;
+                    R[2][2] = (M[0][0] * M[1][1] - M[0][1] * M[1][0]) / det;
+                    double W = m->w[i] * m->w[j] * m->w[k];
+                    double G[3][3];
+                    for (int a = 0; a < 3; a++)
+                        for (int b = 0; b < 3; b++) {
+                            double s = 0.0;
+                            for (int q = 0; q < 3; q++) s += R[a][q] * R[b][q];
+                            G[a][b] = W * det * s;
+                        }
+                    m->jac[l] = det;
+                    m->g[0 * NL + l] = G[0][0];
+                    m->g[1 * NL + l] = G[0][1];
+                    m->g[2 * NL + l] = G[0][2];
+                    m->g[3 * NL + l] = G[1][1];
+                    m->g[4 * NL + l] = G[1][2];
+                    m->g[5 * NL + l] = G[2][2];
+                    m->B[l] = W * det;
+                }
+    }
+    for (int64_t a = 0; a < 6 * NL; a++) m->gf[a] = (float)m->g[a];
+
+    /* C-4: global ids and mask */
+    for (int64_t l = 0; l < NL; l++) {
+        int64_t e; int i, j, k, ex, ey, ez;
+        split_local(m, l, &e, &i, &j, &k);
+        element_xyz(m, e, &ex, &ey, &ez);
+        int64_t I = (int64_t)ex * p + i, J = (int64_t)ey * p + j, K = (int64_t)ez * p + k;
+        m->gid[l] = I + m->NX * (J + m->NY * K);
+        int bnd = (I == 0 || I == m->NX - 1 || J == 0 || J == m->NY - 1 || K == 0 || K == m->NZ - 1);
+        m->mask[l] = bnd ? 0 : 1;
+    }
+    /* multiplicity by brute-force counting of copies per global id */
+    int32_t *cnt = (int32_t *)calloc(m->NG, sizeof(int32_t));
+    for (int64_t l = 0; l < NL; l++) cnt[m->gid[l]]++;
+    for (int64_t l = 0; l < NL; l++) {
+        m->c[l] = 1.0 / cnt[m->gid[l]];
+        m->cf[l] = (float)m->c[l];
+    }
+    /* GS segments: shared global nodes (count >= 2) ascending gid, copies ascending l */
+    int32_t *seg = (int32_t *)malloc(m->NG * sizeof(int32_t));
+    int64_t nseg = 0, ncopies = 0, nunm = 0;
+    for (int64_t gg = 0; gg < m->NG; gg++) {
+        if (cnt[gg] >= 2) { seg[gg] = (int32_t)nseg++; ncopies += cnt[gg]; }
+        else seg[gg] = -1;
+    }
+    m->nseg = (int32_t)nseg;
+    m->off = (int32_t *)malloc((nseg + 1) * sizeof(int32_t));
+    m->idx = (int32_t *)malloc((ncopies > 0 ? ncopies : 1) * sizeof(int32_t));
+    m->off[0] = 0;
+    for (int64_t gg = 0; gg < m->NG; gg++)
+        if (seg[gg] >= 0) m->off[seg[gg] + 1] = m->off[seg[gg]] + cnt[gg];
+    int32_t *fill = (int32_t *)calloc(nseg > 0 ? nseg : 1, sizeof(int32_t));
+    for (int64_t l = 0; l < NL; l++) {
+        int32_t s = seg[m->gid[l]];
+        if (s >= 0) m->idx[m->off[s] + fill[s]++] = (int32_t)l;
+    }
+    free(fill);
+    free(seg);
+    /* unmasked unique nodes */
+    {
+        uint8_t *seen = (uint8_t *)calloc(m->NG, 1);
+        for (int64_t l = 0; l < NL; l++)
+            if (m->mask[l] && !seen[m->gid[l]]) { seen[m->gid[l]] = 1; nunm++; }
+        free(seen);
+    }
+    free(cnt);
+    m->n_unmasked = nunm;
+    m->n_shared_global = nseg;
+    m->n_shared_copies = ncopies;
+
+    /* C-9: Jacobi diagonal, closed form, then consistent fp64 dssum, dinv = 1/diag (0 on mask) */
+    double *diag = (double *)malloc(NL * sizeof(double));
+    for (int64_t e = 0; e < m->E; e++)
+        for (int k = 0; k < n; k++)
+            for (int j = 0; j < n; j++)
+                for (int i = 0; i < n; i++) {
+                    int64_t base = e * n3;
+                    int64_t l = base + i + n * j + (int64_t)n * n * k;
+                    double s = 0.0;
+                    for (int q = 0; q < n; q++) {
+                        double d = m->D[q * n + i];
+                        s += d * d * m->g[0 * NL + base + q + n * j + (int64_t)n * n * k];
+                    }
+                    for (int q = 0; q < n; q++) {
+                        double d = m->D[q * n + j];
+                        s += d * d * m->g[3 * NL + base + i + n * q + (int64_t)n * n * k];
+                    }
+                    for (int q = 0; q < n; q++) {
+                        double d = m->D[q * n + k];
+                        s += d * d * m->g[5 * NL + base + i + n * j + (int64_t)n * n * q];
+                    }
+                    s += 2.0 * m->D[i * n + i] * m->D[j * n + j] * m->g[1 * NL + l];
+                    s += 2.0 * m->D[i * n + i] * m->D[k * n + k] * m->g[2 * NL + l];
+                    s += 2.0 * m->D[j * n + j] * m->D[k * n + k] * m->g[4 * NL + l];
+                    diag[l] = s;
+                }
+    or_dssum_d(m, OR_GS_CONSISTENT, diag);
+    for (int64_t l = 0; l < NL; l++) {
+        if (m->mask[l]) {
+            if (!(diag[l] > 0.0)) ok = 0;
+            m->dinv[l] = 1.0 / diag[l];
+        } else {
+            m->dinv[l] = 0.0;
+        }
+        m->dinvf[l] = (float)m->dinv[l];
+    }
+    free(diag);
+    if (!ok) { or_mesh_free(m); return NULL; }
+    return m;
+}
+
+void or_mesh_info(const or_mesh *m, int64_t *info)
+{
+    info[0] = m->E;
+    info[1] = m->NL;
+    info[2] = m->NG;
+    info[3] = m->n_unmasked;
+    info[4] = m->n_shared_global;
+    info[5] = m->n_shared_copies;
+    info[6] = m->p;
+    info[7] = 1;
+}
+
+void or_export_maps(const or_mesh *m, int64_t *gid, uint8_t *mask, int32_t *gs_off, int32_t *gs_idx)
+{
+    if (gid) memcpy(gid, m->gid, m->NL * sizeof(int64_t));
+    if (mask) memcpy(mask, m->mask, m->NL);
+    if (gs_off) memcpy(gs_off, m->off, (m->nseg + 1) * sizeof(int32_t));
+    if (gs_idx) memcpy(gs_idx, m->idx, m->n_shared_copies * sizeof(int32_t));
+}
+
+void or_export_geom(const or_mesh *m, double *g6, double *B, double *dinv, double *c, double *xyz, double *jac)
+{
+    if (g6) memcpy(g6, m->g, 6 * m->NL * sizeof(double));
+    if (B) memcpy(B, m->B, m->NL * sizeof(double));
+    if (dinv) memcpy(dinv, m->dinv, m->NL * sizeof(double));
+    if (c) memcpy(c, m->c, m->NL * sizeof(double));
+    if (xyz) memcpy(xyz, m->xyz, 3 * m->NL * sizeof(double));
+    if (jac) memcpy(jac, m->jac, m->NL * sizeof(double));
+}
+
+/* ------------------------------------------------------------------ */
+/* C-7: local operator ("ax_e": local_grad3, geometric scaling, local_grad3_t) */
+/* ------------------------------------------------------------------ */
+
+void or_local_grad3(int p, const double *D, const double *u, double *ur, double *us, double *ut)
+{
+    const int n = p + 1;
+    for (int k = 0; k < n; k++)
+        for (int j = 0; j < n; j++)
+            for (int i = 0; i < n; i++) {
+                double a = 0.0, b = 0.0, c = 0.0;
+                for (int l = 0; l < n; l++) {
+                    a += D[i * n + l] * u[l + n * j + n * n * k];
+                    b += D[j * n + l] * u[i + n * l + n * n * k];
+                    c += D[k * n + l] * u[i + n * j + n * n * l];
+                }
+                int q = i + n * j + n * n * k;
+                ur[q] = a; us[q] = b; ut[q] = c;
+            }
+}
+
+void or_ax_local_d(const or_mesh *m, const double *u, double *w)
+{
+    const int n = m->n;
+    const int64_t n3 = (int64_t)n * n * n, NL = m->NL;
+    double *ur = (double *)malloc(n3 * sizeof(double)), *us = (double *)malloc(n3 * sizeof(double));
+    double *ut = (double *)malloc(n3 * sizeof(double));
+    const double *D = m->D;
+    for (int64_t e = 0; e < m->E; e++) {
+        const double *ue = u + e * n3;
+        or_local_grad3(m->p, D, ue, ur, us, ut);
+        for (int64_t q = 0; q < n3; q++) {
+            int64_t l = e * n3 + q;
+            double g1 = m->g[l], g2 = m->g[NL + l], g3 = m->g[2 * NL + l];
+            double g4 = m->g[3 * NL + l], g5 = m->g[4 * NL + l], g6 = m->g[5 * NL + l];
+            double a = ur[q], b = us[q], c = ut[q];
+            ur[q] = (g1 * a + g2 * b) + g3 * c;
+            us[q] = (g2 * a + g4 * b) + g5 * c;
+            ut[q] = (g3 * a + g5 * b) + g6 * c;
+        }
+        for (int k = 0; k < n; k++)
+            for (int j = 0; j < n; j++)
+                for (int i = 0; i < n; i++) {
+                    double a = 0.0, b = 0.0, c = 0.0;
+                    for (int l = 0; l < n; l++) {
+                        a += D[l * n + i] * ur[l + n * j + n * n * k];
+                        b += D[l * n + j] * us[i + n * l + n * n * k];
+                        c += D[l * n + k] * ut[i + n * j + n * n * l];
+                    }
+                    w[e * n3 + i + n * j + n * n * k] = (a + b) + c;
+                }
+    }
+    free(ur); free(us); free(ut);
+}
+
+void or_ax_local_f(const or_mesh *m, const float *u, float *w)
+{
+    const int n = m->n;
+    const int64_t n3 = (int64_t)n * n * n, NL = m->NL;
+    float *ur = (float *)malloc(n3 * sizeof(float)), *us = (float *)malloc(n3 * sizeof(float));
+    float *ut = (float *)malloc(n3 * sizeof(float));
+    const float *D = m->Df;
+    for (int64_t e = 0; e < m->E; e++) {
+        const float *ue = u + e * n3;
+        for (int k = 0; k < n; k++)
+            for (int j = 0; j < n; j++)
+                for (int i = 0; i < n; i++) {
+                    float a = 0.0f, b = 0.0f, c = 0.0f;
+                    for (int l = 0; l < n; l++) {
+                        a += D[i * n + l] * ue[l + n * j + n * n * k];
+                        b += D[j * n + l] * ue[i + n * l + n * n * k];
+                        c += D[k * n + l] * ue[i + n * j + n * n * l];
+                    }
+                    int q = i + n * j + n * n * k;
+                    ur[q] = a; us[q] = b; ut[q] = c;
+                }
+        for (int64_t q = 0; q < n3; q++) {
+            int64_t l = e * n3 + q;
+            float g1 = m->gf[l], g2 = m->gf[NL + l], g3 = m->gf[2 * NL + l];
+            float g4 = m->gf[3 * NL + l], g5 = m->gf[4 * NL + l], g6 = m->gf[5 * NL + l];
+            float a = ur[q], b = us[q], c = ut[q];
+            ur[q] = (g1 * a + g2 * b) + g3 * c;
+            us[q] = (g2 * a + g4 * b) + g5 * c;
+            ut[q] = (g3 * a + g5 * b) + g6 * c;
+        }
+        for (int k = 0; k < n; k++)
+            for (int j = 0; j < n; j++)
+                for (int i = 0; i < n; i++) {
+                    float a = 0.0f, b = 0.0f, c = 0.0f;
+                    for (int l = 0; l < n; l++) {
+                        a += D[l * n + i] * ur[l + n * j + n * n * k];
+                        b += D[l * n + j] * us[i + n * l + n * n * k];
+                        c += D[l * n + k] * ut[i + n * j + n * n * l];
+                    }
+                    w[e * n3 + i + n * j + n * n * k] = (a + b) + c;
+                }
+    }
+    free(ur); free(us); free(ut);
+}
+
+/* ------------------------------------------------------------------ */
+/* C-8: gather-scatter QQ^T over the CSR segments                      */
+/* ------------------------------------------------------------------ */
+
+void or_dssum_d(const or_mesh *m, int order, double *u)
+{
+    double vals[8];
+    for (int32_t s = 0; s < m->nseg; s++) {
+        int32_t a = m->off[s], cnt = m->off[s + 1] - a;
+        for (int q = 0; q < cnt; q++) vals[q] = u[m->idx[a + q]];
+        if (order == OR_GS_CONSISTENT) {
+            double t = 0.0;
+            for (int q = 0; q < cnt; q++) t += vals[q];
+            for (int q = 0; q < cnt; q++) u[m->idx[a + q]] = t;
+        } else {
+            for (int q = 0; q < cnt; q++) {
+                double t = vals[q];
+                for (int r = 0; r < cnt; r++)
+                    if (r != q) t += vals[r];
+                u[m->idx[a + q]] = t;
+            }
+        }
+    }
+}
+
+void or_dssum_f(const or_mesh *m, int order, float *u)
+{
+    float vals[8];
+    for (int32_t s = 0; s < m->nseg; s++) {
+        int32_t a = m->off[s], cnt = m->off[s + 1] - a;
+        for (int q = 0; q < cnt; q++) vals[q] = u[m->idx[a + q]];
+        if (order == OR_GS_CONSISTENT) {
+            float t = 0.0f;
+            for (int q = 0; q < cnt; q++) t += vals[q];
+            for (int q = 0; q < cnt; q++) u[m->idx[a + q]] = t;
+        } else {
+            for (int q = 0; q < cnt; q++) {
+                float t = vals[q];
+                for (int r = 0; r < cnt; r++)
+                    if (r != q) t += vals[r];
+                u[m->idx[a + q]] = t;
+            }
+        }
+    }
+}
+
+void or_dssum_fd(const or_mesh *m, int order, float *u)
+{
+    float vals[8];
+    for (int32_t s = 0; s < m->nseg; s++) {
+        int32_t a = m->off[s], cnt = m->off[s + 1] - a;
+        for (int q = 0; q < cnt; q++) vals[q] = u[m->idx[a + q]];
+        if (order == OR_GS_CONSISTENT) {
+            double t = 0.0;
+            for (int q = 0; q < cnt; q++) t += (double)vals[q];
+            for (int q = 0; q < cnt; q++) u[m->idx[a + q]] = (float)t;
+        } else {
+            for (int q = 0; q < cnt; q++) {
+                double t = (double)vals[q];
+                for (int r = 0; r < cnt; r++)
+                    if (r != q) t += (double)vals[r];
+                u[m->idx[a + q]] = (float)t;
+            }
+        }
+    }
+}
+
+void or_ax_d(const or_mesh *m, int order, const double *u, double *w)
+{
+    or_ax_local_d(m, u, w);
+    or_dssum_d(m, order, w);
+    for (int64_t l = 0; l < m->NL; l++)
+        if (!m->mask[l]) w[l] = 0.0;
+}
+
+void or_ax_f(const or_mesh *m, int policy, int order, const float *u, float *w)
+{
+    or_ax_local_f(m, u, w);
+    if (policy == OR_MIXED) or_dssum_fd(m, order, w);
+    else or_dssum_f(m, order, w);
+    for (int64_t l = 0; l < m->NL; l++)
+        if (!m->mask[l]) w[l] = 0.0f;
+}
+
+/* ------------------------------------------------------------------ */
+/* glsc3 (Table 2 lines 3, 6, 9)                                        */
+/* ------------------------------------------------------------------ */
+
+double or_glsc3_d(const double *a, const double *c, const double *b, int64_t n)
+{
+    double s = 0.0;
+    for (int64_t i = 0; i < n; i++) s += (a[i] * c[i]) * b[i];
+    return s;
+}
+
+double or_glsc3_mixed(const float *a, const double *c, const float *b, int64_t n)
+{
+    double s = 0.0;
+    for (int64_t i = 0; i < n; i++) s += ((double)a[i] * c[i]) * (double)b[i];
+    return s;
+}
+
+static float tree_f(const float *a, const float *c, const float *b, int64_t lo, int64_t hi)
+{
+    if (hi - lo <= 32) {
+        float s = 0.0f;
+        for (int64_t i = lo; i < hi; i++) s += (a[i] * c[i]) * b[i];
+        return s;
+    }
+    int64_t mid = lo + (hi - lo) / 2;
+    float left = tree_f(a, c, b, lo, mid);
+    float right = tree_f(a, c, b, mid, hi);
+    return left + right;
+}
+
+float or_glsc3_f_tree(const float *a, const float *c, const float *b, int64_t n)
+{
+    if (n <= 0) return 0.0f;
+    return tree_f(a, c, b, 0, n);
+}
+
+float or_glsc3_f_seq(const float *a, const float *c, const float *b, int64_t n)
+{
+    float s = 0.0f;
+    for (int64_t i = 0; i < n; i++) s += (a[i] * c[i]) * b[i];
+    return s;
+}
+
+/* ------------------------------------------------------------------ */
+/* C-10 / C-11: PCG and the stagnation rule                             */
+/* ------------------------------------------------------------------ */
+
+/* C-11: status of a run that did not converge by max_iter. */
+static int classify(const double *res, int k, int W)
+{
+    /* running minimum m_j = min_{i<=j} res_i */
+    double mk = res[0];
+    for (int i = 1; i <= k; i++) if (res[i] < mk) mk = res[i];
+    if (res[k] > 100.0 * mk) return OR_STAGNATED;
+    if (W > 0 && k >= W) {
+        double mkw = res[0];
+        for (int i = 1; i <= k - W; i++) if (res[i] < mkw) mkw = res[i];
+        if (mk > 0.1 * mkw) return OR_STAGNATED;
+    }
+    return OR_MAXITER;
+}
+
+static void finish_report(or_report *rep, const double *res, int k, int status, double rtr0, double rtr)
+{
+    rep->iterations = k;
+    rep->status = status;
+    rep->rtr0 = rtr0;
+    rep->rtr_final = rtr;
+    rep->rel_res_final = res[k];
+    double mn = res[0];
+    for (int i = 1; i <= k; i++) if (res[i] < mn) mn = res[i];
+    rep->rel_res_min = mn;
+}
+
+static double true_residual(const or_mesh *m, const double *b64, const double *x)
+{
+    const int64_t NL = m->NL;
+    double *w = (double *)malloc(NL * sizeof(double));
+    double *r = (double *)malloc(NL * sizeof(double));
+    or_ax_d(m, OR_GS_CONSISTENT, x, w);
+    for (int64_t l = 0; l < NL; l++) r[l] = b64[l] - w[l];
+    double rr = or_glsc3_d(r, m->c, r, NL), bb = or_glsc3_d(b64, m->c, b64, NL);
+    free(w); free(r);
+    return bb > 0.0 ? sqrt(rr / bb) : 0.0;
+}
+
+static int cg_fp64(const or_mesh *m, int max_iter, double rtol, int order, int W, const double *b64,
+                   double *x, double *res, or_report *rep)
+{
+    const int64_t NL = m->NL;
+    double *r = (double *)malloc(NL * sizeof(double)), *p = (double *)malloc(NL * sizeof(double));
+    double *z = (double *)malloc(NL * sizeof(double)), *w = (double *)malloc(NL * sizeof(double));
+    for (int64_t l = 0; l < NL; l++) { x[l] = 0.0; r[l] = b64[l]; p[l] = 0.0; }
+    double rtr0 = or_glsc3_d(r, m->c, r, NL), rtr = rtr0, rho = 0.0, rho_old = 1.0;
+    res[0] = 1.0;
+    int k = 0, status = OR_MAXITER;
+    if (rtr0 == 0.0) { status = OR_CONVERGED; res[0] = 0.0; }
+    else {
+        for (k = 1; k <= max_iter; k++) {
+            for (int64_t l = 0; l < NL; l++) z[l] = r[l] * m->dinv[l];                /* solveM */
+            rho = or_glsc3_d(r, m->c, z, NL);                                        /* glsc3 */
+            double beta = (k == 1) ? 0.0 : rho / rho_old;
+            rho_old = rho;
+            for (int64_t l = 0; l < NL; l++) p[l] = z[l] + beta * p[l];              /* add2s1 */
+            or_ax_d(m, order, p, w);                                                 /* ax */
+            double pap = or_glsc3_d(w, m->c, p, NL);                                 /* glsc3 */
+            if (!(pap > 0.0) || !isfinite(pap) || !isfinite(rho)) { status = OR_BREAKDOWN; res[k] = res[k - 1]; break; }
+            double alpha = rho / pap;
+            for (int64_t l = 0; l < NL; l++) x[l] = x[l] + alpha * p[l];             /* add2s2 */
+            for (int64_t l = 0; l < NL; l++) r[l] = r[l] - alpha * w[l];             /* add2s2 */
+            rtr = or_glsc3_d(r, m->c, r, NL);                                        /* glsc3 */
+            res[k] = sqrt(rtr / rtr0);
+            if (!isfinite(rtr)) { status = OR_BREAKDOWN; break; }
+            if (res[k] <= rtol || rtr == 0.0) { status = OR_CONVERGED; break; }
+        }
+        if (k > max_iter) { k = max_iter; status = rtol > 0.0 ? classify(res, k, W) : OR_MAXITER; }
+    }
+    finish_report(rep, res, k, status, rtr0, rtr);
+    free(r); free(p); free(z); free(w);
+    return 0;
+}
+
+/* fp32 and mixed policies (C-10 table). */
+static int cg_f32(const or_mesh *m, int policy, int max_iter, double rtol, int order, int W, int seqdot,
+                  int x64, const double *b64, double *x_out, double *res, or_report *rep)
+{
+    const int64_t NL = m->NL;
+    const int mixed = (policy == OR_MIXED);
+    float *x = (float *)malloc(NL * sizeof(float)), *r = (float *)malloc(NL * sizeof(float));
+    float *p = (float *)malloc(NL * sizeof(float)), *z = (float *)malloc(NL * sizeof(float));
+    float *w = (float *)malloc(NL * sizeof(float));
+    double *xd = (x64 && mixed) ? (double *)malloc(NL * sizeof(double)) : NULL;
+    for (int64_t l = 0; l < NL; l++) { x[l] = 0.0f; r[l] = (float)b64[l]; p[l] = 0.0f; }
+    if (xd) for (int64_t l = 0; l < NL; l++) xd[l] = 0.0;
+
+    /* scalar recurrences: double under mixed, float under fp32 */
+#define DOT(a, b) (mixed ? or_glsc3_mixed((a), m->c, (b), NL) \
+                         : (double)(seqdot ? or_glsc3_f_seq((a), m->cf, (b), NL) : or_glsc3_f_tree((a), m->cf, (b), NL)))
+    double rtr0 = DOT(r, r), rtr = rtr0;
+    double rho = 0.0, rho_old = 1.0;
+    float rho_f = 0.0f, rho_old_f = 1.0f;
+    res[0] = 1.0;
+    int k = 0, status = OR_MAXITER;
+    if (rtr0 == 0.0) { status = OR_CONVERGED; res[0] = 0.0; }
+    else {
+        for (k = 1; k <= max_iter; k++) {
+            /* solveM: mixed z = (float)((double)r * dinv64); fp32 z = r * dinv32 */
+            if (mixed) for (int64_t l = 0; l < NL; l++) z[l] = (float)((double)r[l] * m->dinv[l]);
+            else for (int64_t l = 0; l < NL; l++) z[l] = r[l] * m->dinvf[l];
+            float beta_f;
+            if (mixed) {
+                rho = DOT(r, z);
+                double beta = (k == 1) ? 0.0 : rho / rho_old;
+                rho_old = rho;
+                beta_f = (float)beta;
+            } else {
+                rho_f = (float)DOT(r, z);
+                beta_f = (k == 1) ? 0.0f : rho_f / rho_old_f;
+                rho_old_f = rho_f;
+                rho = rho_f;
+            }
+            for (int64_t l = 0; l < NL; l++) p[l] = z[l] + beta_f * p[l];           /* add2s1 */
+            or_ax_f(m, policy, order, p, w);                                         /* ax */
+            float alpha_f;
+            double pap;
+            if (mixed) {
+                pap = DOT(w, p);
+                if (!(pap > 0.0) || !isfinite(pap) || !isfinite(rho)) { status = OR_BREAKDOWN; res[k] = res[k - 1]; break; }
+                alpha_f = (float)(rho / pap);
+                if (xd) {
+                    double alpha = rho / pap;
+                    for (int64_t l = 0; l < NL; l++) xd[l] = xd[l] + alpha * (double)p[l];
+                }
+            } else {
+                float pap_f = (float)DOT(w, p);
+                pap = pap_f;
+                if (!(pap_f > 0.0f) || !isfinite(pap_f) || !isfinite(rho_f)) { status = OR_BREAKDOWN; res[k] = res[k - 1]; break; }
+                alpha_f = rho_f / pap_f;
+            }
+            for (int64_t l = 0; l < NL; l++) x[l] = x[l] + alpha_f * p[l];           /* add2s2 */
+            for (int64_t l = 0; l < NL; l++) r[l] = r[l] - alpha_f * w[l];           /* add2s2 */
+            rtr = DOT(r, r);                                                         /* glsc3 */
+            res[k] = sqrt(rtr / rtr0);
+            if (!isfinite(rtr)) { status = OR_BREAKDOWN; break; }
+            if (res[k] <= rtol || rtr == 0.0) { status = OR_CONVERGED; break; }
+        }
+        if (k > max_iter) { k = max_iter; status = rtol > 0.0 ? classify(res, k, W) : OR_MAXITER; }
+    }
+#undef DOT
+    finish_report(rep, res, k, status, rtr0, rtr);
+    for (int64_t l = 0; l < NL; l++) x_out[l] = xd ? xd[l] : (double)x[l];
+    free(x); free(r); free(p); free(z); free(w); free(xd);
+    return 0;
+}
+
+int or_cg(const or_mesh *m, int policy, int max_iter, double rtol, int gs_order, int stag_window,
+          int seqdot, int x64, const double *b64, double *x_out, double *hist, or_report *rep)
+{
+    if (!m || !b64 || !x_out || !rep || max_iter < 0 || rtol < 0.0) return 1;
+    if (policy < OR_FP64 || policy > OR_MIXED) return 1;
+    double *res = (double *)calloc((size_t)max_iter + 1, sizeof(double));
+    int rc;
+    if (policy == OR_FP64) rc = cg_fp64(m, max_iter, rtol, gs_order, stag_window, b64, x_out, res, rep);
+    else rc = cg_f32(m, policy, max_iter, rtol, gs_order, stag_window, seqdot, x64, b64, x_out, res, rep);
+    if (hist) for (int i = 0; i <= rep->iterations; i++) hist[i] = res[i];
+    rep->true_res = true_residual(m, b64, x_out);
+    free(res);
+    return rc;
+}
+
+/* ------------------------------------------------------------------ */
+/* C-5: right-hand sides                                                */
+/* ------------------------------------------------------------------ */
+
+void or_rhs(const or_mesh *m, int kind, double noise_amp, uint64_t seed, double *b)
+{
+    const int64_t NL = m->NL;
+    if (kind == OR_RHS_UNIFORM) {
+        for (int64_t l = 0; l < NL; l++)
+            b[l] = m->mask[l] ? or_prng_u(seed, 1, (uint64_t)m->gid[l]) : 0.0;
+        return;
+    }
+    const double pi = 3.14159265358979323846;
+    const double *X = m->xyz, *Y = m->xyz + NL, *Z = m->xyz + 2 * NL;
+    for (int64_t l = 0; l < NL; l++) {
+        double f = 3.0 * pi * pi * sin(pi * X[l]) * sin(pi * Y[l]) * sin(pi * Z[l])
+                 + noise_amp * or_prng_u(seed, 2, (uint64_t)m->gid[l]);
+        b[l] = m->B[l] * f;
+    }
+    or_dssum_d(m, OR_GS_CONSISTENT, b);
+    for (int64_t l = 0; l < NL; l++)
+        if (!m->mask[l]) b[l] = 0.0;
+}
