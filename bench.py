@@ -1,0 +1,327 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 SEM Jacobi-PCG hot path (arxiv 2503.02134) -- driver contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--policy mixed]
+
+Workload (BASELINE.json configs[1], the metric's configuration): 16x16x16 undeformed
+hex elements on [0,1]^3, p = 7 (2,097,152 local DOF), Dirichlet faces, uniform[-1,1]
+RHS from seed 0, Jacobi-PCG to rtol 1e-8, mixed policy (fp32 vectors/Ax, fp64 GS,
+dots and Jacobi).  One step = one complete nb_cg solve (all SURVEY.md §8(a) per-iteration
+rows a5..a12; setup a1..a4 is done once before timing, like Nekbone's solve time).
+value = local DOF x iterations / solve time, summed over ranks / max-over-ranks time.
+
+Multi-GPU: the single-GPU solve is replicated (independent problems per rank, no
+data-path collective) -> "scaling": "weak"; DESIGN.md §7 explains why.
+--impl reference times the oracle (plain C, one core) on bounded samples of the same
+workload (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = {"workload": "configs[1]: box 16x16x16 undeformed, p=7, uniform RHS seed 0, Jacobi-PCG rtol 1e-8",
+            "nel": [16, 16, 16], "p": 7, "deform": 0.0, "rtol": 1e-8, "rhs": "uniform seed 0"}
+METRIC = "DOF·iter/s and time-to-1e-8 residual (fp64 vs mixed); Ax/dssum HBM GB/s"
+UNIT = "DOF·iter/s"
+POLICIES = {"fp64": 0, "fp32": 1, "mixed": 2}
+# bytes per local DOF moved by each kernel, by policy (vectors, g, dinv at
+# their policy precision; c and the mask are analytic, not read)
+K1_BYTES = {0: 8 + 8 + 8 + 48 + 8 + 8, 1: 4 + 4 + 4 + 24 + 4 + 4, 2: 4 + 8 + 4 + 24 + 4 + 4}
+K3_BYTES = {0: 8 * 5 + 8 * 2, 1: 4 * 5 + 4 * 2, 2: 4 * 4 + 8 + 4 * 2}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (clocks + throttle reasons)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 5]
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[2 + i] and "Not" not in r[2 + i]})
+        loaded = [s for s in sm if mx and s > 0.3 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def dist_init(n_gpus):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return rank, world, local
+
+
+def barrier_sync(world):
+    import torch
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------- CPU oracle legs
+def oracle_sample(iters: int, policy: str = "mixed"):
+    """Time the oracle (as it stands, one core) on `iters` CG iterations of configs[1]."""
+    import oracle
+    nel, p = WORKLOAD["nel"], WORKLOAD["p"]
+    t0 = time.perf_counter()
+    m = oracle.Mesh(*nel, p, deform=0.0, seed=0)
+    b = m.rhs(oracle.RHS_UNIFORM, seed=0)
+    t_setup = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _, _, rep = m.cg(b, {"fp64": oracle.FP64, "fp32": oracle.FP32, "mixed": oracle.MIXED}[policy],
+                     max_iter=iters, rtol=0.0)
+    dt = time.perf_counter() - t0
+    return m.n_local * rep.iterations / dt, dt, t_setup, rep.iterations, m.n_local
+
+
+def run_reference(args):
+    rank, world, _ = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0
+    if rank != 0:
+        return 0
+    iters = args.ref_iters
+    for _ in range(args.warmup):
+        oracle_sample(max(1, iters // 4), args.policy)
+    vals, times = [], []
+    for _ in range(args.steps):
+        v, dt, _, it, nl = oracle_sample(iters, args.policy)
+        vals.append(v)
+        times.append(dt)
+    total = sum(times)
+    value = nl * iters * args.steps / total
+    sample = (f"{iters} CG iterations ({args.policy}, rtol=0) of configs[1] per step, mesh setup excluded; "
+              f"oracle plain C -O2 single-threaded")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64 (mixed)",
+            "data": "synthetic", "config": dict(WORKLOAD, policy=args.policy),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import paper_2503_02134_b200 as nb
+
+    rank, world, local = dist_init(args.gpus)
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+    pol = POLICIES[args.policy]
+    nel, p = WORKLOAD["nel"], WORKLOAD["p"]
+    mesh = nb.Mesh(*nel, p, deform=0.0, seed=0, device=dev)
+    NL = mesh.n_local
+    b = mesh.rhs(pol, nb.NB_RHS_UNIFORM, seed=0)
+    x = mesh.empty(pol)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+    max_iter = 4000
+
+    def solve(time_kernels=False):
+        rep, _ = nb.nb_cg(mesh.h, b, x, pol, max_iter, WORKLOAD["rtol"], time_kernels=time_kernels, history=False)
+        return rep
+
+    for _ in range(max(3, args.warmup)):
+        solve()
+    st = torch.cuda.current_stream()
+    clocks = Clocks(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    iters, launches = [], 0
+    barrier_sync(world)
+    clocks.start()
+    for s in range(args.steps):
+        flush.zero_()                          # L2 flush between steps (outside the events)
+        ev[s][0].record(st)
+        rep = solve()
+        ev[s][1].record(st)
+        iters.append(rep.iterations)
+        launches += rep.kernel_launches
+    barrier_sync(world)
+    ck = clocks.stop()
+    step_ms = [a.elapsed_time(b2) for a, b2 in ev]
+    t_local = sum(step_ms) / 1e3
+    t_max = max_over_ranks(t_local, world)
+    dof_iter = sum_over_ranks(float(NL * sum(iters)), world)
+    value = dof_iter / t_max
+
+    # per-kernel durations: the same solves with CUDA events around every launch
+    kt = [solve(time_kernels=True) for _ in range(max(1, min(args.steps, 3)))]
+    it_k = sum(r.iterations for r in kt)
+    ax_ms = sum(r.k_ax_ms for r in kt) / it_k
+    gs_ms = sum(r.k_gs_ms for r in kt) / it_k
+    up_ms = sum(r.k_upd_ms for r in kt) / it_k
+    peak, peak_src = load_peaks()
+    k1_bytes = K1_BYTES[pol] * NL
+    achieved = k1_bytes / (ax_ms * 1e-3) / 1e9
+    info = mesh.info
+    vs = 4 if pol else 8
+    gs_bytes = info.n_shared_copies * (2 * vs + 4) + (info.n_shared_global + 1) * 4 + info.n_shared_global * vs
+    k3_bytes = K3_BYTES[pol] * NL
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(f"k_ax_{args.policy}_configs1")
+    except Exception:
+        pass
+
+    # e2e: the public host-buffer call, pinned host b/x, copies inside the timed region
+    bh = b.cpu().pin_memory()
+    xh = torch.empty_like(bh).pin_memory()
+    e2e_t, e2e_it = 0.0, 0
+    for s in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep, _ = nb.nb_cg_host(mesh.h, bh, xh, pol, max_iter, WORKLOAD["rtol"])
+        e2e_t += time.perf_counter() - t0
+        e2e_it += rep.iterations
+    e2e_t = max_over_ranks(e2e_t, world)
+    e2e_val = sum_over_ranks(float(NL * e2e_it), world) / e2e_t
+
+    # time-to-1e-8 for every policy (reported next to the headline; not the timed region)
+    ttr = {}
+    if rank == 0 and not args.quick:
+        for name, pp in POLICIES.items():
+            bb = mesh.rhs(pp, nb.NB_RHS_UNIFORM, seed=0)
+            xx = mesh.empty(pp)
+            reps = []
+            for _ in range(3):
+                flush.zero_()
+                r, _ = nb.nb_cg(mesh.h, bb, xx, pp, max_iter, WORKLOAD["rtol"], history=False)
+                reps.append(r)
+            rk, _ = nb.nb_cg(mesh.h, bb, xx, pp, max_iter, WORKLOAD["rtol"], time_kernels=True, history=False)
+            n_it = rk.iterations
+            ttr[name] = {"iterations": reps[-1].iterations, "status": reps[-1].status,
+                         "time_ms": statistics.median(r.solve_ms for r in reps),
+                         "dof_iter_per_s": NL * reps[-1].iterations / (statistics.median(r.solve_ms for r in reps) * 1e-3),
+                         "ax_us": 1e3 * rk.k_ax_ms / n_it, "dssum_us": 1e3 * rk.k_gs_ms / n_it,
+                         "update_us": 1e3 * rk.k_upd_ms / n_it,
+                         "ax_alg_GBps": K1_BYTES[pp] * NL / (rk.k_ax_ms * 1e-3 / n_it) / 1e9,
+                         "update_alg_GBps": K3_BYTES[pp] * NL / (rk.k_upd_ms * 1e-3 / n_it) / 1e9}
+        ttr["speedup_fp64_over_mixed_time"] = ttr["fp64"]["time_ms"] / ttr["mixed"]["time_ms"]
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, dt, _, it, _ = oracle_sample(args.cpu_iters, args.policy)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{it} CG iterations ({args.policy}, rtol=0) of configs[1], setup excluded, "
+                         f"{dt:.1f} s on one host core"}
+
+    if rank == 0:
+        ms_per_step = 1e3 * t_max / args.steps
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": {0: "f64", 1: "f32", 2: "f32+f64 (mixed)"}[pol],
+                "data": "synthetic",
+                "config": dict(WORKLOAD, policy=args.policy, iterations=iters[0], n_local=NL,
+                               l2="256 MiB write between steps (outside the step events)",
+                               parallelism="replicas" if world > 1 else "single GPU"),
+                "time_to_rtol_ms": 1e3 * t_max / args.steps,
+                "roofline": {"bound": "hbm", "kernel": "k_ax (K1: Jacobi + add2s1 + local Ax + mask + interior pap)",
+                             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                             "traffic": traffic, "peak_source": peak_src,
+                             "alg_bytes_per_launch": k1_bytes, "avg_launch_us": 1e3 * ax_ms,
+                             "share_of_iteration": ax_ms / (ax_ms + gs_ms + up_ms),
+                             "dssum": {"avg_launch_us": 1e3 * gs_ms, "alg_bytes_per_launch": gs_bytes,
+                                       "achieved_GBps": gs_bytes / (gs_ms * 1e-3) / 1e9},
+                             "update": {"avg_launch_us": 1e3 * up_ms, "alg_bytes_per_launch": k3_bytes,
+                                        "achieved_GBps": k3_bytes / (up_ms * 1e-3) / 1e9,
+                                        "frac": k3_bytes / (up_ms * 1e-3) / 1e9 / peak}},
+                "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": NL * vs, "d2h_bytes_per_step": NL * vs},
+                "gpu_launches": launches, "clocks": ck, "cpu_baseline": cpu, "policies": ttr}
+        print(json.dumps(line), flush=True)
+    mesh.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--policy", default="mixed", choices=list(POLICIES))
+    ap.add_argument("--cpu-iters", type=int, default=60)
+    ap.add_argument("--ref-iters", type=int, default=20)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip the per-policy time-to-rtol table")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,155 @@
+/*
+ * nb.h -- C ABI of the B200 (sm_100a) Nekbone-style mixed-precision SEM Jacobi-PCG.
+ *
+ * The only public header.  C99; no C++ or torch types cross it.  Every entry
+ * point returns an nb_status code and never aborts or throws; on a non-OK
+ * return nb_last_error() gives a thread-local message.
+ *
+ * What is computed (arxiv 2503.02134, PAPER.md):
+ *   - the Nekbone CG loop of Table 2 (:158-168): solveM (Jacobi, :444), glsc3,
+ *     add2s1, ax, glsc3, add2s2 x2, glsc3;
+ *   - ax = per-element local_grad3 / geometric scaling / local_grad3_t (:147),
+ *     followed by gather-scatter "to ensure continuity" of the unassembled
+ *     per-element representation (:404) and the Dirichlet mask;
+ *   - under three precision policies: fp64, fp32, and the paper's mixed
+ *     strategy "single precision PCG loop with the global communication via
+ *     the Gather-Scatter library performed in double" plus double dot products
+ *     and preconditioner (:53, :429-431, :537; BASELINE.json north_star).
+ * Readings where the paper is silent (mesh, deformation, numbering, RHS,
+ * stopping rule) are SURVEY.md §8(c) C-1..C-17 and are listed in DESIGN.md §3.
+ *
+ * Conventions shared by every call:
+ *   - Local ("L-vector") layout: n = p+1, index
+ *     l = e*n^3 + i + n*j + n^2*k, element e = ex + nelx*(ey + nely*ez).
+ *     A vector has n_local contiguous entries (double for NB_FP64, float for
+ *     NB_FP32 / NB_MIXED).
+ *   - Device pointers must be 16-byte aligned and point into memory of the
+ *     handle's device.  The caller owns every vector it passes; the library
+ *     never frees or retains them past the call.
+ *   - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     nb_rhs / nb_ax / nb_dssum are asynchronous on it; nb_cg returns after
+ *     the solve has finished (its report is host data).
+ *   - A handle is not re-entrant: one call in flight per handle.
+ */
+#ifndef NB_H
+#define NB_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nb_handle nb_handle;
+
+/* Precision policy: selects both element type and arithmetic.
+ *   NB_FP64 : double data, double arithmetic everywhere.
+ *   NB_FP32 : float data, float arithmetic, float gather-scatter accumulation,
+ *             float dot products and scalars, float Jacobi copy.
+ *   NB_MIXED: float data and float Ax arithmetic; gather-scatter accumulated in
+ *             double and rounded once to float; Jacobi z = (float)((double)r * dinv64);
+ *             glsc3 products and accumulation and the CG scalars in double. */
+typedef enum { NB_FP64 = 0, NB_FP32 = 1, NB_MIXED = 2 } nb_policy;
+
+/* Gather-scatter summation order:
+ *   NB_GS_CONSISTENT: one sum per shared global node, copies ascending, written to all copies.
+ *   NB_GS_PER_COPY  : copy l receives w_l + sum_{m != l, ascending} w_m, emulating the
+ *                     pairwise exchange mode whose fp32 stagnation the paper reports
+ *                     (Table 3). */
+typedef enum { NB_GS_CONSISTENT = 0, NB_GS_PER_COPY = 1 } nb_gs_order;
+
+/* Right-hand sides, generated in fp64 and cast once:
+ *   NB_RHS_UNIFORM     : b_l = mask_l * U(seed, 1, gid_l), U the counter SplitMix64 in [-1,1).
+ *   NB_RHS_MANUFACTURED: b = mask . QQ^T (B . f), f = 3 pi^2 sin(pi x) sin(pi y) sin(pi z)
+ *                        + noise_amp * U(seed, 2, gid). */
+typedef enum { NB_RHS_UNIFORM = 0, NB_RHS_MANUFACTURED = 1 } nb_rhs_kind;
+
+typedef enum {
+    NB_OK = 0,
+    NB_EINVAL = 1,      /* bad sizes/arguments, NULL or misaligned pointers, p outside [1,15] */
+    NB_ENOMEM = 2,      /* device or host allocation failed */
+    NB_ECUDA = 3,       /* CUDA runtime error; message in nb_last_error() */
+    NB_EGEOM = 4,       /* non-positive Jacobian or Jacobi diagonal at setup */
+    NB_EBREAKDOWN = 5,  /* pap <= 0 with rtr > 0, or a non-finite scalar */
+    NB_ESTATE = 6       /* handle destroyed / used from the wrong device */
+} nb_status;
+
+/* nb_cg_report.status (stagnation is NB_OK with status NB_STAGNATED) */
+enum { NB_CONVERGED = 0, NB_MAXITER = 1, NB_STAGNATED = 2, NB_BROKEDOWN = 3 };
+
+/* nb_ax flags */
+enum { NB_AX_LOCAL = 1u };   /* w = A_L u only: no gather-scatter, no mask */
+
+typedef struct {
+    int64_t E, n_local, n_global, n_unmasked, n_shared_global, n_shared_copies;
+    int32_t p, nelx, nely, nelz;
+} nb_info;
+
+typedef struct {
+    nb_policy policy;
+    int32_t max_iter;          /* >= 0 */
+    double rtol;               /* stop when sqrt(rtr/rtr0) <= rtol; 0 = run exactly max_iter */
+    nb_gs_order gs_order;
+    int32_t stag_window;       /* C-11 window W (default 200 when <= 0) */
+    int32_t time_kernels;      /* 1: record per-kernel CUDA-event durations into the report */
+    double *rel_res_history;   /* host, length max_iter+1, nullable: [0] = 1, [k] = sqrt(rtr_k/rtr0) */
+} nb_cg_opts;
+
+typedef struct {
+    int32_t iterations;        /* completed CG iterations */
+    int32_t status;            /* NB_CONVERGED / NB_MAXITER / NB_STAGNATED / NB_BROKEDOWN */
+    double rtr0, rtr_final, rel_res_final, rel_res_min;
+    double solve_ms;           /* device time of the solve (CUDA events on the caller stream) */
+    int64_t kernel_launches;   /* kernels of this library launched by the solve */
+    double k_ax_ms, k_gs_ms, k_upd_ms;  /* when time_kernels: summed durations of the three
+                                           per-iteration kernels (Ax, dssum, update) */
+} nb_cg_report;
+
+/* Build the box mesh [0,1]^3 of nelx*nely*nelz hexes of order p on `device`
+ * (SURVEY.md C-1..C-9): GLL nodes/weights/D, deformed trilinear geometry
+ * (deform_amp = vertex amplitude as a fraction of element size, 0 = undeformed;
+ * phases seeded by `seed`), g1..g6 and B, numbering, mask, GS segments and the
+ * Jacobi diagonal.  All device data is allocated here and owned by the handle.
+ * Errors: NB_EINVAL (p not in [1,15], nel < 1, n_local >= 2^31), NB_ENOMEM, NB_ECUDA, NB_EGEOM. */
+int nb_setup(int32_t nelx, int32_t nely, int32_t nelz, int32_t p, double deform_amp, uint64_t seed,
+             int32_t device, nb_handle **out);
+int nb_destroy(nb_handle *h);                 /* NULL is a no-op; frees all device memory */
+int nb_query(const nb_handle *h, nb_info *out);
+
+/* Fill device vector b (policy precision of `prec`) with a right-hand side. Async. */
+int nb_rhs(nb_handle *h, nb_rhs_kind kind, double noise_amp, uint64_t seed, nb_policy prec,
+           void *b, void *stream);
+
+/* w = mask . QQ^T A_L u  (or w = A_L u with NB_AX_LOCAL).  u, w: device, distinct,
+ * precision of `prec` (NB_MIXED: float data, float Ax, double GS accumulation).  Async.
+ * PAPER.md:163 ("call ax(w,p,g,ur,us,ut,wk,n)"), :147. */
+int nb_ax(nb_handle *h, nb_policy prec, const void *u, void *w, uint32_t flags, void *stream);
+
+/* In place u = QQ^T u over the shared-node segments (no mask).  Async.  PAPER.md:309, :404. */
+int nb_dssum(nb_handle *h, nb_policy prec, nb_gs_order order, void *u, void *stream);
+
+/* Jacobi-PCG (Table 2 order) from x0 = 0.  b, x: device vectors in the
+ * policy precision; b must be continuous and masked (e.g. from nb_rhs).  Blocks until done.
+ * Returns NB_OK for converged / max_iter / stagnated runs, NB_EBREAKDOWN on breakdown
+ * (report filled in either case). */
+int nb_cg(nb_handle *h, const nb_cg_opts *o, const void *b, void *x, nb_cg_report *rep, void *stream);
+
+/* Same solve with HOST buffers (pinned or pageable): copies b in and x out on `stream`. */
+int nb_cg_host(nb_handle *h, const nb_cg_opts *o, const void *b_host, void *x_host,
+               nb_cg_report *rep, void *stream);
+
+/* Host copies of the integer maps (caller-allocated host arrays, each nullable):
+ * gid[n_local], mask[n_local], gs_off[n_shared_global+1], gs_idx[n_shared_copies]. */
+int nb_export_maps(const nb_handle *h, int64_t *gid, uint8_t *mask, int32_t *gs_off, int32_t *gs_idx);
+/* Host copies of the fp64 setup data (nullable): g6[6*n_local] factor-major (g1..g6 each
+ * n_local long, C-6 ordering g1=Grr,g2=Grs,g3=Grt,g4=Gss,g5=Gst,g6=Gtt), B, dinv[n_local]. */
+int nb_export_geom(const nb_handle *h, double *g6, double *B, double *dinv);
+/* GLL nodes[p+1], weights[p+1], D[(p+1)^2] (row-major, D[i*(p+1)+j] = l_j'(x_i)). */
+int nb_export_basis(const nb_handle *h, double *nodes, double *weights, double *D);
+
+const char *nb_last_error(void);
+const char *nb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

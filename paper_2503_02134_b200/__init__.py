@@ -1,0 +1,292 @@
+"""B200 (sm_100a) mixed-precision SEM Jacobi-PCG -- thin Python binding over include/nb.h.
+
+Every step of the hot path runs in the CUDA kernels of ``csrc/`` behind the C ABI
+in ``libnb.so``; this module only marshals arguments (torch tensors -> device
+pointers, the current torch stream -> cudaStream_t).  There is no CPU fallback:
+if the library cannot be loaded, importing the binding functions raises.
+
+Names follow include/nb.h (``nb_setup``, ``nb_ax``, ``nb_dssum``, ``nb_cg`` ...).
+The method is arxiv 2503.02134's Nekbone CG loop (Table 2)
+under the fp64 / fp32 / mixed policies.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._build import LIB, build as _build_lib
+
+NB_FP64, NB_FP32, NB_MIXED = 0, 1, 2
+NB_GS_CONSISTENT, NB_GS_PER_COPY = 0, 1
+NB_RHS_UNIFORM, NB_RHS_MANUFACTURED = 0, 1
+NB_AX_LOCAL = 1
+NB_CONVERGED, NB_MAXITER, NB_STAGNATED, NB_BROKEDOWN = 0, 1, 2, 3
+NB_OK, NB_EINVAL, NB_ENOMEM, NB_ECUDA, NB_EGEOM, NB_EBREAKDOWN, NB_ESTATE = range(7)
+POLICY_NAMES = {NB_FP64: "fp64", NB_FP32: "fp32", NB_MIXED: "mixed"}
+
+EXPORTED = ["nb_setup", "nb_destroy", "nb_query", "nb_rhs", "nb_ax", "nb_dssum", "nb_cg", "nb_cg_host",
+            "nb_export_maps", "nb_export_geom", "nb_export_basis", "nb_last_error", "nb_version"]
+
+
+class NbError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"nb error {code}: {msg}")
+        self.code = code
+
+
+class nb_info(C.Structure):
+    _fields_ = [("E", C.c_int64), ("n_local", C.c_int64), ("n_global", C.c_int64), ("n_unmasked", C.c_int64),
+                ("n_shared_global", C.c_int64), ("n_shared_copies", C.c_int64), ("p", C.c_int32),
+                ("nelx", C.c_int32), ("nely", C.c_int32), ("nelz", C.c_int32)]
+
+
+class nb_cg_opts(C.Structure):
+    _fields_ = [("policy", C.c_int), ("max_iter", C.c_int32), ("rtol", C.c_double), ("gs_order", C.c_int),
+                ("stag_window", C.c_int32), ("time_kernels", C.c_int32), ("rel_res_history", C.c_void_p)]
+
+
+class nb_cg_report(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("status", C.c_int32), ("rtr0", C.c_double), ("rtr_final", C.c_double),
+                ("rel_res_final", C.c_double), ("rel_res_min", C.c_double), ("solve_ms", C.c_double),
+                ("kernel_launches", C.c_int64), ("k_ax_ms", C.c_double), ("k_gs_ms", C.c_double),
+                ("k_upd_ms", C.c_double)]
+
+
+_lib = None
+
+
+def lib(auto_build: bool = True):
+    """Load libnb.so (building it in-tree with nvcc if it is missing or stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if auto_build:
+        _build_lib()
+    if not os.path.exists(LIB):
+        raise ImportError(f"{LIB} missing: the CUDA library must be built (python -m paper_2503_02134_b200._build)")
+    L = C.CDLL(LIB)
+    P, I, U64, D = C.c_void_p, C.c_int, C.c_uint64, C.c_double
+    L.nb_setup.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, D, U64, C.c_int32, C.POINTER(P)]
+    L.nb_destroy.argtypes = [P]
+    L.nb_query.argtypes = [P, C.POINTER(nb_info)]
+    L.nb_rhs.argtypes = [P, I, D, U64, I, P, P]
+    L.nb_ax.argtypes = [P, I, P, P, C.c_uint32, P]
+    L.nb_dssum.argtypes = [P, I, I, P, P]
+    L.nb_cg.argtypes = [P, C.POINTER(nb_cg_opts), P, P, C.POINTER(nb_cg_report), P]
+    L.nb_cg_host.argtypes = [P, C.POINTER(nb_cg_opts), P, P, C.POINTER(nb_cg_report), P]
+    L.nb_export_maps.argtypes = [P, P, P, P, P]
+    L.nb_export_geom.argtypes = [P, P, P, P]
+    L.nb_export_basis.argtypes = [P, P, P, P]
+    L.nb_last_error.restype = C.c_char_p
+    L.nb_version.restype = C.c_char_p
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != NB_OK:
+        raise NbError(rc, lib().nb_last_error().decode())
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _dptr(t, dtype=None):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("expected a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"expected dtype {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+def policy_dtype(policy: int):
+    import torch
+    return torch.float64 if policy == NB_FP64 else torch.float32
+
+
+def policy_np_dtype(policy: int):
+    return np.float64 if policy == NB_FP64 else np.float32
+
+
+# --------------------------------------------------------------------------- C-ABI mirrors
+def nb_setup(nelx: int, nely: int, nelz: int, p: int, deform_amp: float = 0.0, seed: int = 0, device: int = 0):
+    h = C.c_void_p()
+    _check(lib().nb_setup(nelx, nely, nelz, p, deform_amp, seed, device, C.byref(h)))
+    return h
+
+
+def nb_destroy(h):
+    _check(lib().nb_destroy(h))
+
+
+def nb_query(h) -> nb_info:
+    info = nb_info()
+    _check(lib().nb_query(h, C.byref(info)))
+    return info
+
+
+def nb_rhs(h, kind: int, noise_amp: float, seed: int, prec: int, b, stream=None):
+    _check(lib().nb_rhs(h, kind, noise_amp, seed, prec, _dptr(b, policy_dtype(prec)), _stream(stream)))
+
+
+def nb_ax(h, prec: int, u, w, flags: int = 0, stream=None):
+    dt = policy_dtype(prec)
+    _check(lib().nb_ax(h, prec, _dptr(u, dt), _dptr(w, dt), flags, _stream(stream)))
+
+
+def nb_dssum(h, prec: int, order: int, u, stream=None):
+    _check(lib().nb_dssum(h, prec, order, _dptr(u, policy_dtype(prec)), _stream(stream)))
+
+
+def _opts(policy, max_iter, rtol, gs_order, stag_window, time_kernels, hist):
+    o = nb_cg_opts()
+    o.policy, o.max_iter, o.rtol, o.gs_order = policy, max_iter, rtol, gs_order
+    o.stag_window, o.time_kernels = stag_window, int(time_kernels)
+    o.rel_res_history = hist.ctypes.data if hist is not None else None
+    return o
+
+
+def nb_cg(h, b, x, policy: int = NB_MIXED, max_iter: int = 1000, rtol: float = 1e-8,
+          gs_order: int = NB_GS_CONSISTENT, stag_window: int = 200, time_kernels: bool = False,
+          history: bool = True, stream=None, allow_breakdown: bool = True):
+    """Jacobi-PCG from x0 = 0; returns (report, rel_res_history)."""
+    dt = policy_dtype(policy)
+    hist = np.zeros(max_iter + 1) if history else None
+    o = _opts(policy, max_iter, rtol, gs_order, stag_window, time_kernels, hist)
+    rep = nb_cg_report()
+    rc = lib().nb_cg(h, C.byref(o), _dptr(b, dt), _dptr(x, dt), C.byref(rep), _stream(stream))
+    if rc != NB_OK and not (allow_breakdown and rc == NB_EBREAKDOWN):
+        _check(rc)
+    return rep, (hist[: rep.iterations + 1] if hist is not None else None)
+
+
+def nb_cg_host(h, b_host, x_host, policy: int = NB_MIXED, max_iter: int = 1000, rtol: float = 1e-8,
+               gs_order: int = NB_GS_CONSISTENT, stag_window: int = 200, history: bool = False, stream=None):
+    """Same solve with host buffers (numpy arrays or pinned CPU tensors); copies inside the call."""
+    def hp(a):
+        if isinstance(a, np.ndarray):
+            assert a.flags["C_CONTIGUOUS"] and a.dtype == policy_np_dtype(policy)
+            return C.c_void_p(a.ctypes.data)
+        assert a.device.type == "cpu" and a.is_contiguous() and a.dtype == policy_dtype(policy)
+        return C.c_void_p(a.data_ptr())
+    hist = np.zeros(max_iter + 1) if history else None
+    o = _opts(policy, max_iter, rtol, gs_order, stag_window, False, hist)
+    rep = nb_cg_report()
+    rc = lib().nb_cg_host(h, C.byref(o), hp(b_host), hp(x_host), C.byref(rep), _stream(stream))
+    if rc not in (NB_OK, NB_EBREAKDOWN):
+        _check(rc)
+    return rep, (hist[: rep.iterations + 1] if hist is not None else None)
+
+
+def nb_export_maps(h):
+    info = nb_query(h)
+    gid = np.zeros(info.n_local, dtype=np.int64)
+    mask = np.zeros(info.n_local, dtype=np.uint8)
+    off = np.zeros(info.n_shared_global + 1, dtype=np.int32)
+    idx = np.zeros(max(info.n_shared_copies, 1), dtype=np.int32)
+    _check(lib().nb_export_maps(h, gid.ctypes.data, mask.ctypes.data, off.ctypes.data, idx.ctypes.data))
+    return gid, mask, off, idx[: info.n_shared_copies]
+
+
+def nb_export_geom(h):
+    info = nb_query(h)
+    g6 = np.zeros((6, info.n_local))
+    B = np.zeros(info.n_local)
+    dinv = np.zeros(info.n_local)
+    _check(lib().nb_export_geom(h, g6.ctypes.data, B.ctypes.data, dinv.ctypes.data))
+    return g6, B, dinv
+
+
+def nb_export_basis(h):
+    n = nb_query(h).p + 1
+    z, w, D = np.zeros(n), np.zeros(n), np.zeros((n, n))
+    _check(lib().nb_export_basis(h, z.ctypes.data, w.ctypes.data, D.ctypes.data))
+    return z, w, D
+
+
+def nb_last_error() -> str:
+    return lib().nb_last_error().decode()
+
+
+def nb_version() -> str:
+    return lib().nb_version().decode()
+
+
+# --------------------------------------------------------------------------- convenience
+@dataclass
+class CgResult:
+    iterations: int
+    status: int
+    rtr0: float
+    rel_res_final: float
+    rel_res_min: float
+    solve_ms: float
+    kernel_launches: int
+    k_ax_ms: float
+    k_gs_ms: float
+    k_upd_ms: float
+    history: np.ndarray | None
+
+
+class Mesh:
+    """Owning wrapper of an nb_handle (frees device memory on close/deletion)."""
+
+    def __init__(self, nelx, nely, nelz, p, deform=0.0, seed=0, device=0):
+        self.h = nb_setup(nelx, nely, nelz, p, deform, seed, device)
+        info = nb_query(self.h)
+        self.info = info
+        self.n_local = info.n_local
+        self.p, self.n = info.p, info.p + 1
+        self.E = info.E
+        self.device = device
+        self.dims = (nelx, nely, nelz)
+
+    def close(self):
+        if getattr(self, "h", None):
+            nb_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def empty(self, policy):
+        import torch
+        return torch.empty(self.n_local, dtype=policy_dtype(policy), device=f"cuda:{self.device}")
+
+    def rhs(self, policy=NB_MIXED, kind=NB_RHS_UNIFORM, noise=1e-3, seed=0):
+        b = self.empty(policy)
+        nb_rhs(self.h, kind, noise, seed, policy, b)
+        return b
+
+    def ax(self, u, policy, local=False):
+        w = self.empty(policy)
+        nb_ax(self.h, policy, u, w, NB_AX_LOCAL if local else 0)
+        return w
+
+    def dssum(self, u, policy, order=NB_GS_CONSISTENT):
+        v = u.clone()
+        nb_dssum(self.h, policy, order, v)
+        return v
+
+    def cg(self, b, policy=NB_MIXED, max_iter=1000, rtol=1e-8, gs_order=NB_GS_CONSISTENT, stag_window=200,
+           time_kernels=False):
+        x = self.empty(policy)
+        rep, hist = nb_cg(self.h, b, x, policy, max_iter, rtol, gs_order, stag_window, time_kernels)
+        r = CgResult(rep.iterations, rep.status, rep.rtr0, rep.rel_res_final, rep.rel_res_min, rep.solve_ms,
+                     rep.kernel_launches, rep.k_ax_ms, rep.k_gs_ms, rep.k_upd_ms, hist)
+        return x, r

@@ -1,0 +1,552 @@
+// nb_api.cu -- the C ABI (include/nb.h): argument checking, setup orchestration,
+// GLL basis on the host, CG driver (device-resident scalars, CUDA graph with a
+// conditional WHILE node so the whole iteration loop runs without host round trips).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "nb.h"
+#include "nb_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg)
+{
+    g_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char *where)
+{
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return NB_ECUDA;
+}
+#define NB_CU(call, where)                                     \
+    do {                                                       \
+        cudaError_t _e = (call);                               \
+        if (_e != cudaSuccess) return cuda_fail(_e, where);    \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// GLL basis, computed independently of the oracle: Newton on
+// q(x) = L_{N+1}(x) - L_{N-1}(x) (roots: +-1 and the zeros of L_N'),
+// q'(x) = (2N+1) L_N(x); derivative matrix from barycentric weights, diagonal
+// by the negative-sum rule.
+// ---------------------------------------------------------------------------
+void legendre3(int N, double x, double &LNm1, double &LN, double &LNp1)
+{
+    double a = 1.0, b = x;   // L_0, L_1
+    if (N == 0) { LNm1 = 0.0; LN = 1.0; LNp1 = x; return; }
+    for (int k = 1; k < N; k++) {
+        double c = ((2.0 * k + 1.0) * x * b - k * a) / (k + 1.0);
+        a = b;
+        b = c;
+    }
+    LNm1 = a;
+    LN = b;
+    LNp1 = ((2.0 * N + 1.0) * x * b - N * a) / (N + 1.0);
+}
+
+bool gll_basis(int N, double *x, double *w, double *D)
+{
+    const double pi = 3.14159265358979323846;
+    const int n = N + 1;
+    x[0] = -1.0;
+    x[N] = 1.0;
+    for (int j = 1; j <= (N - 1) / 2; j++) {
+        double t = -std::cos(pi * j / N);
+        bool ok = false;
+        for (int it = 0; it < 200; it++) {
+            double a, b, c;
+            legendre3(N, t, a, b, c);
+            const double dt = -(c - a) / ((2.0 * N + 1.0) * b);
+            t += dt;
+            if (std::fabs(dt) <= 1e-16) { ok = true; break; }
+        }
+        if (!ok) {
+            double a, b, c;
+            legendre3(N, t, a, b, c);
+            if (std::fabs(c - a) > 1e-13) return false;
+        }
+        x[j] = t;
+        x[N - j] = -t;
+    }
+    if (N % 2 == 0) x[N / 2] = 0.0;
+    for (int j = 0; j < n; j++) {
+        double a, b, c;
+        legendre3(N, x[j], a, b, c);
+        w[j] = 2.0 / (N * (N + 1.0) * b * b);
+    }
+    double lam[16];
+    for (int j = 0; j < n; j++) {
+        double prod = 1.0;
+        for (int k = 0; k < n; k++)
+            if (k != j) prod *= (x[j] - x[k]);
+        lam[j] = 1.0 / prod;
+    }
+    for (int i = 0; i < n; i++) {
+        double s = 0.0;
+        for (int j = 0; j < n; j++) {
+            if (j == i) continue;
+            const double v = (lam[j] / lam[i]) / (x[i] - x[j]);
+            D[i * n + j] = v;
+            s += v;
+        }
+        D[i * n + i] = -s;
+    }
+    return true;
+}
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+int check_dev_ptr(const nb_handle *h, const void *p, const char *name)
+{
+    if (!p) return fail(NB_EINVAL, std::string(name) + " is NULL");
+    if (!aligned16(p)) return fail(NB_EINVAL, std::string(name) + " is not 16-byte aligned");
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(NB_EINVAL, std::string(name) + " is not a CUDA pointer");
+    }
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+        return fail(NB_EINVAL, std::string(name) + " is not device memory");
+    if (at.device != h->device) return fail(NB_EINVAL, std::string(name) + " lives on another device");
+    return NB_OK;
+}
+
+size_t vsize(int prec) { return prec == NB_FP64 ? sizeof(double) : sizeof(float); }
+
+int ensure_f32(nb_handle *h)
+{
+    if (!h->g32) {
+        NB_CU(cudaMalloc(&h->g32, sizeof(float) * 6 * h->NL), "cudaMalloc g32");
+        NB_CU(nb::launch_cast(h->g64, h->g32, 6 * h->NL, 0), "cast g");
+    }
+    if (!h->dinv32) {
+        NB_CU(cudaMalloc(&h->dinv32, sizeof(float) * h->NL), "cudaMalloc dinv32");
+        NB_CU(nb::launch_cast(h->dinv64, h->dinv32, h->NL, 0), "cast dinv");
+    }
+    NB_CU(cudaStreamSynchronize(0), "cast sync");
+    return NB_OK;
+}
+
+int ensure_ws(nb_handle *h, int prec, int32_t max_iter)
+{
+    nb::Workspace &ws = h->ws[prec];
+    if (!ws.ready) {
+        const size_t vs = vsize(prec) * h->NL;
+        NB_CU(cudaMalloc(&ws.r, vs), "cudaMalloc r");
+        NB_CU(cudaMalloc(&ws.p, vs), "cudaMalloc p");
+        NB_CU(cudaMalloc(&ws.w, vs), "cudaMalloc w");
+        NB_CU(cudaMalloc(&ws.x, vs), "cudaMalloc x");
+        const int nax = nb::grid_ax(h, prec), ngs = nb::grid_gs(h), nup = nb::grid_upd(h, prec);
+        int slots = nax + ngs;
+        if (2 * nup > slots) slots = 2 * nup;
+        NB_CU(cudaMalloc(&ws.part, sizeof(double) * slots), "cudaMalloc part");
+        NB_CU(cudaMalloc(&ws.scal, sizeof(nb::Scal)), "cudaMalloc scal");
+        NB_CU(cudaMallocHost(&ws.scal_host, sizeof(nb::Scal)), "cudaMallocHost scal");
+        NB_CU(cudaMemset(ws.scal, 0, sizeof(nb::Scal)), "memset scal");
+        ws.ready = true;
+    }
+    if (ws.hist_cap < max_iter + 1) {
+        if (ws.hist) cudaFree(ws.hist);
+        ws.hist = nullptr;
+        ws.hist_cap = 0;
+        const int cap = max_iter + 1 < 1024 ? 1024 : max_iter + 1;
+        NB_CU(cudaMalloc(&ws.hist, sizeof(double) * cap), "cudaMalloc hist");
+        ws.hist_cap = cap;
+    }
+    return NB_OK;
+}
+
+void free_ws(nb::Workspace &ws)
+{
+    if (ws.exec) cudaGraphExecDestroy(ws.exec);
+    if (ws.graph) cudaGraphDestroy(ws.graph);
+    cudaFree(ws.r); cudaFree(ws.p); cudaFree(ws.w); cudaFree(ws.x);
+    cudaFree(ws.part); cudaFree(ws.scal); cudaFree(ws.hist);
+    if (ws.scal_host) cudaFreeHost(ws.scal_host);
+    ws = nb::Workspace();
+}
+
+// Conditional-WHILE graph: body = K1 (ax) -> K2 (dssum) -> K3 (update); K3's last block
+// clears the condition when the solve is done.
+int build_graph(nb_handle *h, int prec, int order)
+{
+    nb::Workspace &ws = h->ws[prec];
+    if (ws.exec && ws.graph_order == order) return NB_OK;
+    if (ws.exec) { cudaGraphExecDestroy(ws.exec); ws.exec = nullptr; }
+    if (ws.graph) { cudaGraphDestroy(ws.graph); ws.graph = nullptr; }
+    (void)nb::grid_ax(h, prec);   // initialise occupancy/attributes outside capture
+    cudaGraph_t graph;
+    NB_CU(cudaGraphCreate(&graph, 0), "cudaGraphCreate");
+    cudaGraphConditionalHandle cond;
+    NB_CU(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault), "cond handle");
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    NB_CU(cudaGraphAddNode(&node, graph, nullptr, 0, &cp), "add conditional node");
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    NB_CU(cudaStreamBeginCaptureToGraph(h->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed),
+          "begin capture");
+    cudaError_t e1 = nb::launch_cg_ax(h, prec, ws, h->cap_stream);
+    cudaError_t e2 = nb::launch_cg_gs(h, prec, order, ws, h->cap_stream, cond, true);
+    cudaError_t e3 = nb::launch_cg_upd(h, prec, ws, h->cap_stream, cond, true);
+    cudaGraph_t captured;
+    cudaError_t ec = cudaStreamEndCapture(h->cap_stream, &captured);
+    if (e1 != cudaSuccess) return cuda_fail(e1, "capture ax");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "capture gs");
+    if (e3 != cudaSuccess) return cuda_fail(e3, "capture upd");
+    if (ec != cudaSuccess) return cuda_fail(ec, "end capture");
+    cudaGraphExec_t exec;
+    NB_CU(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+    ws.graph = graph;
+    ws.exec = exec;
+    ws.graph_order = order;
+    return NB_OK;
+}
+
+// C-11 stagnation rule on the host history (only for runs that did not converge)
+int classify(const std::vector<double> &res, int k, int W)
+{
+    double mk = res[0];
+    for (int i = 1; i <= k; i++) mk = res[i] < mk ? res[i] : mk;
+    if (res[k] > 100.0 * mk) return NB_STAGNATED;
+    if (W > 0 && k >= W) {
+        double mkw = res[0];
+        for (int i = 1; i <= k - W; i++) mkw = res[i] < mkw ? res[i] : mkw;
+        if (mk > 0.1 * mkw) return NB_STAGNATED;
+    }
+    return NB_MAXITER;
+}
+
+}  // namespace
+
+namespace nb {
+void deform_phases(uint64_t seed, double ph[3])
+{
+    for (int a = 0; a < 3; a++) {
+        uint64_t z = (seed ^ (3ull * 0xD1B54A32D192ED03ull)) + ((uint64_t)a + 1ull) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        ph[a] = 3.14159265358979323846 * (1.0 + ((double)(z >> 11) * 0x1.0p-52 - 1.0));
+    }
+}
+}  // namespace nb
+
+extern "C" {
+
+const char *nb_last_error(void) { return g_err.c_str(); }
+const char *nb_version(void) { return "nb-b200 0.1 (sm_100a)"; }
+
+int nb_setup(int32_t nelx, int32_t nely, int32_t nelz, int32_t p, double deform_amp, uint64_t seed, int32_t device,
+             nb_handle **out)
+{
+    if (!out) return fail(NB_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (p < 1 || p > 15) return fail(NB_EINVAL, "p must be in [1,15]");
+    if (nelx < 1 || nely < 1 || nelz < 1) return fail(NB_EINVAL, "element counts must be >= 1");
+    if (!(deform_amp >= 0.0) || deform_amp > 0.25) return fail(NB_EINVAL, "deform_amp must be in [0, 0.25]");
+    const int n = p + 1;
+    const int64_t E = (int64_t)nelx * nely * nelz;
+    const int64_t NL = E * n * n * n;
+    if (NL >= 2147483647LL) return fail(NB_EINVAL, "n_local must be < 2^31 (int32 GS indices)");
+    int ndev = 0;
+    NB_CU(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) return fail(NB_EINVAL, "bad device ordinal");
+    NB_CU(cudaSetDevice(device), "cudaSetDevice");
+
+    nb_handle *h = new (std::nothrow) nb_handle();
+    if (!h) return fail(NB_ENOMEM, "host allocation failed");
+    h->device = device;
+    h->nelx = nelx; h->nely = nely; h->nelz = nelz; h->p = p; h->n = n;
+    h->E = E; h->NL = NL;
+    h->NX = (int64_t)nelx * p + 1; h->NY = (int64_t)nely * p + 1; h->NZ = (int64_t)nelz * p + 1;
+    h->NG = h->NX * h->NY * h->NZ;
+    h->n_unmasked = ((int64_t)nelx * p - 1) * ((int64_t)nely * p - 1) * ((int64_t)nelz * p - 1);
+    h->deform = deform_amp;
+    h->seed = seed;
+    if (!gll_basis(p, h->nodes, h->weights, h->D)) { delete h; return fail(NB_EINVAL, "GLL Newton failed"); }
+    cudaDeviceProp prop;
+    int rc = NB_OK;
+    auto bail = [&](int code) { nb_destroy(h); return code; };
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "props"));
+    h->sm_count = prop.multiProcessorCount;
+    if (h->NG >= 2147483647LL) return bail(fail(NB_EINVAL, "global node count must be < 2^31"));
+
+    cudaError_t e;
+    if ((e = cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking)) != cudaSuccess) return bail(cuda_fail(e, "stream"));
+    if ((e = nb::upload_basis(n, h->D)) != cudaSuccess) return bail(cuda_fail(e, "upload D"));
+    if ((e = cudaMalloc(&h->g64, sizeof(double) * 6 * NL)) != cudaSuccess) return bail(fail(NB_ENOMEM, "cudaMalloc g64"));
+    if ((e = cudaMalloc(&h->B, sizeof(double) * NL)) != cudaSuccess) return bail(fail(NB_ENOMEM, "cudaMalloc B"));
+    if ((e = cudaMalloc(&h->dinv64, sizeof(double) * NL)) != cudaSuccess) return bail(fail(NB_ENOMEM, "cudaMalloc dinv"));
+    if ((e = cudaMalloc(&h->flag, sizeof(int32_t))) != cudaSuccess) return bail(fail(NB_ENOMEM, "cudaMalloc flag"));
+    cudaStream_t st = h->cap_stream;
+    if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int32_t), st)) != cudaSuccess) return bail(cuda_fail(e, "memset"));
+    double ph[3];
+    nb::deform_phases(seed, ph);
+    if ((e = nb::launch_geometry(h, ph, st)) != cudaSuccess) return bail(cuda_fail(e, "geometry"));
+    if ((e = nb::build_gs(h, st)) != cudaSuccess) return bail(cuda_fail(e, "gs segments"));
+    double *diag = nullptr;
+    if ((e = cudaMalloc(&diag, sizeof(double) * NL)) != cudaSuccess) return bail(fail(NB_ENOMEM, "cudaMalloc diag"));
+    e = nb::launch_jacobi(h, diag, st);
+    int32_t flag = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&flag, h->flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(diag);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "jacobi"));
+    if (flag & 1) return bail(fail(NB_EGEOM, "non-positive Jacobian"));
+    if (flag & 2) return bail(fail(NB_EGEOM, "non-positive Jacobi diagonal"));
+    (void)rc;
+    *out = h;
+    return NB_OK;
+}
+
+int nb_destroy(nb_handle *h)
+{
+    if (!h) return NB_OK;
+    cudaSetDevice(h->device);
+    for (auto &ws : h->ws) free_ws(ws);
+    cudaFree(h->g64); cudaFree(h->g32); cudaFree(h->B); cudaFree(h->dinv64); cudaFree(h->dinv32);
+    cudaFree(h->gs_off); cudaFree(h->gs_idx); cudaFree(h->flag);
+    if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+    delete h;
+    return NB_OK;
+}
+
+int nb_query(const nb_handle *h, nb_info *o)
+{
+    if (!h || !o) return fail(NB_EINVAL, "NULL argument");
+    o->E = h->E; o->n_local = h->NL; o->n_global = h->NG; o->n_unmasked = h->n_unmasked;
+    o->n_shared_global = h->nseg; o->n_shared_copies = h->ncopies;
+    o->p = h->p; o->nelx = h->nelx; o->nely = h->nely; o->nelz = h->nelz;
+    return NB_OK;
+}
+
+int nb_rhs(nb_handle *h, nb_rhs_kind kind, double noise_amp, uint64_t seed, nb_policy prec, void *b, void *stream)
+{
+    if (!h) return fail(NB_EINVAL, "NULL handle");
+    if (prec < NB_FP64 || prec > NB_MIXED) return fail(NB_EINVAL, "bad policy");
+    if (kind != NB_RHS_UNIFORM && kind != NB_RHS_MANUFACTURED) return fail(NB_EINVAL, "bad rhs kind");
+    NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
+    int rc = check_dev_ptr(h, b, "b");
+    if (rc) return rc;
+    NB_CU(nb::launch_rhs(h, kind, noise_amp, seed, prec, b, (cudaStream_t)stream), "rhs");
+    return NB_OK;
+}
+
+int nb_ax(nb_handle *h, nb_policy prec, const void *u, void *w, uint32_t flags, void *stream)
+{
+    if (!h) return fail(NB_EINVAL, "NULL handle");
+    if (prec < NB_FP64 || prec > NB_MIXED) return fail(NB_EINVAL, "bad policy");
+    if (flags & ~NB_AX_LOCAL) return fail(NB_EINVAL, "unknown flags");
+    NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
+    int rc = check_dev_ptr(h, u, "u");
+    if (!rc) rc = check_dev_ptr(h, w, "w");
+    if (rc) return rc;
+    if (u == w) return fail(NB_EINVAL, "u and w must be distinct");
+    if (prec != NB_FP64 && (rc = ensure_f32(h))) return rc;
+    NB_CU(nb::launch_ax(h, prec, u, w, (flags & NB_AX_LOCAL) != 0, (cudaStream_t)stream), "ax");
+    return NB_OK;
+}
+
+int nb_dssum(nb_handle *h, nb_policy prec, nb_gs_order order, void *u, void *stream)
+{
+    if (!h) return fail(NB_EINVAL, "NULL handle");
+    if (prec < NB_FP64 || prec > NB_MIXED) return fail(NB_EINVAL, "bad policy");
+    if (order != NB_GS_CONSISTENT && order != NB_GS_PER_COPY) return fail(NB_EINVAL, "bad gs order");
+    NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
+    int rc = check_dev_ptr(h, u, "u");
+    if (rc) return rc;
+    NB_CU(nb::launch_dssum(h, prec, order, u, (cudaStream_t)stream), "dssum");
+    return NB_OK;
+}
+
+static int cg_impl(nb_handle *h, const nb_cg_opts *o, const void *b, bool b_host, void *x, bool x_host,
+                   nb_cg_report *rep, cudaStream_t st)
+{
+    const int prec = o->policy;
+    int rc;
+    if (prec != NB_FP64 && (rc = ensure_f32(h))) return rc;
+    if ((rc = ensure_ws(h, prec, o->max_iter))) return rc;
+    nb::Workspace &ws = h->ws[prec];
+    const size_t vbytes = vsize(prec) * h->NL;
+    if (!o->time_kernels && (rc = build_graph(h, prec, o->gs_order))) return rc;
+
+    cudaEvent_t t0, t1;
+    NB_CU(cudaEventCreate(&t0), "event");
+    NB_CU(cudaEventCreate(&t1), "event");
+    // device scalars
+    nb::Scal s0;
+    memset(&s0, 0, sizeof(s0));
+    s0.rtol = o->rtol;
+    s0.max_iter = o->max_iter;
+    *ws.scal_host = s0;
+    NB_CU(cudaEventRecord(t0, st), "event record");
+    NB_CU(cudaMemcpyAsync(ws.r, b, vbytes, b_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st), "copy b");
+    NB_CU(cudaMemcpyAsync(ws.scal, ws.scal_host, sizeof(nb::Scal), cudaMemcpyHostToDevice, st), "copy scal");
+    NB_CU(nb::launch_cg_init(h, prec, ws, nullptr, st), "cg init");
+    int64_t launches = 1;
+    double kms[3] = {0.0, 0.0, 0.0};
+    if (!o->time_kernels) {
+        NB_CU(cudaGraphLaunch(ws.exec, st), "graph launch");
+    } else {
+        // per-kernel CUDA-event timing: direct launches, check the done flag every 16 iterations
+        std::vector<cudaEvent_t> ev;
+        const int chunk = 16;
+        ev.resize(4 * chunk);
+        for (auto &e : ev) NB_CU(cudaEventCreate(&e), "event");
+        int k = 0;
+        bool done = false;
+        while (!done && k < o->max_iter) {
+            const int m = (o->max_iter - k) < chunk ? (o->max_iter - k) : chunk;
+            for (int c = 0; c < m; c++) {
+                cudaGraphConditionalHandle none = 0;
+                NB_CU(cudaEventRecord(ev[4 * c], st), "ev");
+                NB_CU(nb::launch_cg_ax(h, prec, ws, st), "ax");
+                NB_CU(cudaEventRecord(ev[4 * c + 1], st), "ev");
+                NB_CU(nb::launch_cg_gs(h, prec, o->gs_order, ws, st, none, false), "gs");
+                NB_CU(cudaEventRecord(ev[4 * c + 2], st), "ev");
+                NB_CU(nb::launch_cg_upd(h, prec, ws, st, none, false), "upd");
+                NB_CU(cudaEventRecord(ev[4 * c + 3], st), "ev");
+            }
+            NB_CU(cudaMemcpyAsync(ws.scal_host, ws.scal, sizeof(nb::Scal), cudaMemcpyDeviceToHost, st), "scal");
+            NB_CU(cudaStreamSynchronize(st), "sync");
+            const int before = k;
+            const int it_now = ws.scal_host->iter;
+            for (int c = 0; c < m; c++) {
+                if (before + c >= it_now && ws.scal_host->done) break;   // no-op launches after the end
+                float a, b2, c3;
+                cudaEventElapsedTime(&a, ev[4 * c], ev[4 * c + 1]);
+                cudaEventElapsedTime(&b2, ev[4 * c + 1], ev[4 * c + 2]);
+                cudaEventElapsedTime(&c3, ev[4 * c + 2], ev[4 * c + 3]);
+                kms[0] += a; kms[1] += b2; kms[2] += c3;
+            }
+            k += m;
+            launches += 3 * m;
+            done = ws.scal_host->done != 0;
+        }
+        for (auto &e : ev) cudaEventDestroy(e);
+    }
+    NB_CU(cudaMemcpyAsync(ws.scal_host, ws.scal, sizeof(nb::Scal), cudaMemcpyDeviceToHost, st), "copy scal back");
+    NB_CU(cudaMemcpyAsync(x, ws.x, vbytes, x_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st), "copy x");
+    NB_CU(cudaEventRecord(t1, st), "event record");
+    NB_CU(cudaStreamSynchronize(st), "solve sync");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    const nb::Scal s = *ws.scal_host;
+    const int k = s.iter;
+    std::vector<double> res(k + 1, 0.0);
+    NB_CU(cudaMemcpy(res.data(), ws.hist, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost), "copy hist");
+    if (!o->time_kernels) launches += 3 * (int64_t)(k + (s.status == NB_BROKEDOWN ? 1 : 0)) + (k < o->max_iter ? 0 : 0);
+    int status = s.status;
+    if (status == NB_MAXITER && o->rtol > 0.0) status = classify(res, k, o->stag_window > 0 ? o->stag_window : 200);
+    if (o->rel_res_history) memcpy(o->rel_res_history, res.data(), sizeof(double) * (k + 1));
+    if (rep) {
+        rep->iterations = k;
+        rep->status = status;
+        rep->rtr0 = s.rtr0;
+        rep->rtr_final = s.rtr;
+        rep->rel_res_final = res[k];
+        double mn = res[0];
+        for (int i = 1; i <= k; i++) mn = res[i] < mn ? res[i] : mn;
+        rep->rel_res_min = mn;
+        rep->solve_ms = ms;
+        rep->kernel_launches = launches;
+        rep->k_ax_ms = kms[0];
+        rep->k_gs_ms = kms[1];
+        rep->k_upd_ms = kms[2];
+    }
+    if (status == NB_BROKEDOWN) return fail(NB_EBREAKDOWN, "CG breakdown (pap <= 0 or non-finite scalar)");
+    return NB_OK;
+}
+
+static int cg_args(nb_handle *h, const nb_cg_opts *o)
+{
+    if (!h || !o) return fail(NB_EINVAL, "NULL argument");
+    if (o->policy < NB_FP64 || o->policy > NB_MIXED) return fail(NB_EINVAL, "bad policy");
+    if (o->gs_order != NB_GS_CONSISTENT && o->gs_order != NB_GS_PER_COPY) return fail(NB_EINVAL, "bad gs order");
+    if (o->max_iter < 0 || !(o->rtol >= 0.0)) return fail(NB_EINVAL, "bad max_iter/rtol");
+    NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
+    return NB_OK;
+}
+
+int nb_cg(nb_handle *h, const nb_cg_opts *o, const void *b, void *x, nb_cg_report *rep, void *stream)
+{
+    int rc = cg_args(h, o);
+    if (rc) return rc;
+    if ((rc = check_dev_ptr(h, b, "b")) || (rc = check_dev_ptr(h, x, "x"))) return rc;
+    return cg_impl(h, o, b, false, x, false, rep, (cudaStream_t)stream);
+}
+
+int nb_cg_host(nb_handle *h, const nb_cg_opts *o, const void *b_host, void *x_host, nb_cg_report *rep, void *stream)
+{
+    int rc = cg_args(h, o);
+    if (rc) return rc;
+    if (!b_host || !x_host) return fail(NB_EINVAL, "NULL host buffer");
+    return cg_impl(h, o, b_host, true, x_host, true, rep, (cudaStream_t)stream);
+}
+
+int nb_export_maps(const nb_handle *h, int64_t *gid, uint8_t *mask, int32_t *gs_off, int32_t *gs_idx)
+{
+    if (!h) return fail(NB_EINVAL, "NULL handle");
+    NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
+    if (gid || mask) {
+        int64_t *dg = nullptr;
+        uint8_t *dm = nullptr;
+        if (gid) NB_CU(cudaMalloc(&dg, sizeof(int64_t) * h->NL), "cudaMalloc");
+        if (mask) NB_CU(cudaMalloc(&dm, h->NL), "cudaMalloc");
+        NB_CU(nb::launch_maps(h, dg, dm, 0), "maps");
+        if (gid) NB_CU(cudaMemcpy(gid, dg, sizeof(int64_t) * h->NL, cudaMemcpyDeviceToHost), "copy gid");
+        if (mask) NB_CU(cudaMemcpy(mask, dm, h->NL, cudaMemcpyDeviceToHost), "copy mask");
+        cudaFree(dg);
+        cudaFree(dm);
+    }
+    if (gs_off) NB_CU(cudaMemcpy(gs_off, h->gs_off, sizeof(int32_t) * (h->nseg + 1), cudaMemcpyDeviceToHost), "copy off");
+    if (gs_idx && h->ncopies)
+        NB_CU(cudaMemcpy(gs_idx, h->gs_idx, sizeof(int32_t) * h->ncopies, cudaMemcpyDeviceToHost), "copy idx");
+    return NB_OK;
+}
+
+int nb_export_geom(const nb_handle *h, double *g6, double *B, double *dinv)
+{
+    if (!h) return fail(NB_EINVAL, "NULL handle");
+    NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
+    if (g6) {
+        // device layout [e][c][n^3] -> factor-major [c][NL]
+        const int64_t n3 = (int64_t)h->n * h->n * h->n;
+        std::vector<double> tmp(6 * h->NL);
+        NB_CU(cudaMemcpy(tmp.data(), h->g64, sizeof(double) * 6 * h->NL, cudaMemcpyDeviceToHost), "copy g");
+        for (int64_t e = 0; e < h->E; e++)
+            for (int c = 0; c < 6; c++)
+                memcpy(g6 + c * h->NL + e * n3, tmp.data() + (e * 6 + c) * n3, sizeof(double) * n3);
+    }
+    if (B) NB_CU(cudaMemcpy(B, h->B, sizeof(double) * h->NL, cudaMemcpyDeviceToHost), "copy B");
+    if (dinv) NB_CU(cudaMemcpy(dinv, h->dinv64, sizeof(double) * h->NL, cudaMemcpyDeviceToHost), "copy dinv");
+    return NB_OK;
+}
+
+int nb_export_basis(const nb_handle *h, double *nodes, double *weights, double *D)
+{
+    if (!h) return fail(NB_EINVAL, "NULL handle");
+    const int n = h->n;
+    if (nodes) memcpy(nodes, h->nodes, sizeof(double) * n);
+    if (weights) memcpy(weights, h->weights, sizeof(double) * n);
+    if (D) memcpy(D, h->D, sizeof(double) * n * n);
+    return NB_OK;
+}
+
+}  // extern "C"
