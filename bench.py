@@ -33,10 +33,15 @@ WORKLOAD = {"workload": "configs[1]: box 16x16x16 undeformed, p=7, uniform RHS s
 METRIC = "DOF·iter/s and time-to-1e-8 residual (fp64 vs mixed); Ax/dssum HBM GB/s"
 UNIT = "DOF·iter/s"
 POLICIES = {"fp64": 0, "fp32": 1, "mixed": 2}
-# bytes per local DOF moved by each kernel, by policy (vectors, g, dinv at
-# their policy precision; c and the mask are analytic, not read)
-K1_BYTES = {0: 8 + 8 + 8 + 48 + 8 + 8, 1: 4 + 4 + 4 + 24 + 4 + 4, 2: 4 + 8 + 4 + 24 + 4 + 4}
-K3_BYTES = {0: 8 * 5 + 8 * 2, 1: 4 * 5 + 4 * 2, 2: 4 * 4 + 8 + 4 * 2}
+# Algorithmic bytes per local DOF moved by each kernel, by policy: every
+# vector, g and dinv entry once at its policy precision; c and the mask are analytic.
+#   K1 (k_ax, CG):  z, p_old, x, 6 g  ->  p, x, w
+#   K2 (k_upd):     w, r, dinv        ->  r, z      (gather re-reads are not algorithmic)
+SV = {0: 8, 1: 4, 2: 4}          # vector entry
+SJ = {0: 8, 1: 4, 2: 8}          # dinv entry
+K1_BYTES = {p: 3 * SV[p] + 6 * SV[p] + 3 * SV[p] for p in SV}
+K2_BYTES = {p: 2 * SV[p] + SJ[p] + 2 * SV[p] for p in SV}
+AX_BYTES = {p: 2 * SV[p] + 6 * SV[p] for p in SV}     # standalone local Ax: u + 6 g -> w
 
 
 def load_peaks():
@@ -170,6 +175,19 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------- GPU arm
+def time_launches(fn, n, stream):
+    """Average device time (ms) of fn() over n back-to-back launches, CUDA events on `stream`."""
+    import torch
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fn()
+    a.record(stream)
+    for _ in range(n):
+        fn()
+    b.record(stream)
+    b.synchronize()
+    return a.elapsed_time(b) / n
+
+
 def run_ours(args):
     import torch
     import paper_2503_02134_b200 as nb
@@ -181,10 +199,12 @@ def run_ours(args):
     nel, p = WORKLOAD["nel"], WORKLOAD["p"]
     mesh = nb.Mesh(*nel, p, deform=0.0, seed=0, device=dev)
     NL = mesh.n_local
+    info = mesh.info
     b = mesh.rhs(pol, nb.NB_RHS_UNIFORM, seed=0)
     x = mesh.empty(pol)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
     max_iter = 4000
+    st = torch.cuda.current_stream()
 
     def solve(time_kernels=False):
         rep, _ = nb.nb_cg(mesh.h, b, x, pol, max_iter, WORKLOAD["rtol"], time_kernels=time_kernels, history=False)
@@ -192,10 +212,9 @@ def run_ours(args):
 
     for _ in range(max(3, args.warmup)):
         solve()
-    st = torch.cuda.current_stream()
     clocks = Clocks(dev)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    iters, launches = [], 0
+    iters, launches, statuses = [], 0, set()
     barrier_sync(world)
     clocks.start()
     for s in range(args.steps):
@@ -204,6 +223,7 @@ def run_ours(args):
         rep = solve()
         ev[s][1].record(st)
         iters.append(rep.iterations)
+        statuses.add(rep.status)
         launches += rep.kernel_launches
     barrier_sync(world)
     ck = clocks.stop()
@@ -213,19 +233,21 @@ def run_ours(args):
     dof_iter = sum_over_ranks(float(NL * sum(iters)), world)
     value = dof_iter / t_max
 
-    # per-kernel durations: the same solves with CUDA events around every launch
+    # per-kernel durations: the same solve with CUDA events around every launch (same stream)
     kt = [solve(time_kernels=True) for _ in range(max(1, min(args.steps, 3)))]
     it_k = sum(r.iterations for r in kt)
-    ax_ms = sum(r.k_ax_ms for r in kt) / it_k
-    gs_ms = sum(r.k_gs_ms for r in kt) / it_k
-    up_ms = sum(r.k_upd_ms for r in kt) / it_k
+    k1_ms = sum(r.k_ax_ms for r in kt) / it_k
+    k2_ms = sum(r.k_upd_ms for r in kt) / it_k
     peak, peak_src = load_peaks()
+    vs = SV[pol]
     k1_bytes = K1_BYTES[pol] * NL
-    achieved = k1_bytes / (ax_ms * 1e-3) / 1e9
-    info = mesh.info
-    vs = 4 if pol else 8
-    gs_bytes = info.n_shared_copies * (2 * vs + 4) + (info.n_shared_global + 1) * 4 + info.n_shared_global * vs
-    k3_bytes = K3_BYTES[pol] * NL
+    k2_bytes = K2_BYTES[pol] * NL
+    # standalone operator pieces (the metric's "Ax/dssum HBM GB/s"): local Ax and the CSR dssum
+    u = mesh.rhs(pol, nb.NB_RHS_UNIFORM, seed=5)
+    wv = mesh.empty(pol)
+    ax_ms = time_launches(lambda: nb.nb_ax(mesh.h, pol, u, wv, nb.NB_AX_LOCAL), 50, st)
+    gs_ms = time_launches(lambda: nb.nb_dssum(mesh.h, pol, nb.NB_GS_CONSISTENT, wv), 50, st)
+    gs_bytes = info.n_shared_copies * (2 * vs + 4) + (info.n_shared_global + 1) * 4
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -260,13 +282,12 @@ def run_ours(args):
                 reps.append(r)
             rk, _ = nb.nb_cg(mesh.h, bb, xx, pp, max_iter, WORKLOAD["rtol"], time_kernels=True, history=False)
             n_it = rk.iterations
-            ttr[name] = {"iterations": reps[-1].iterations, "status": reps[-1].status,
-                         "time_ms": statistics.median(r.solve_ms for r in reps),
-                         "dof_iter_per_s": NL * reps[-1].iterations / (statistics.median(r.solve_ms for r in reps) * 1e-3),
-                         "ax_us": 1e3 * rk.k_ax_ms / n_it, "dssum_us": 1e3 * rk.k_gs_ms / n_it,
-                         "update_us": 1e3 * rk.k_upd_ms / n_it,
-                         "ax_alg_GBps": K1_BYTES[pp] * NL / (rk.k_ax_ms * 1e-3 / n_it) / 1e9,
-                         "update_alg_GBps": K3_BYTES[pp] * NL / (rk.k_upd_ms * 1e-3 / n_it) / 1e9}
+            tmed = statistics.median(r.solve_ms for r in reps)
+            ttr[name] = {"iterations": reps[-1].iterations, "status": reps[-1].status, "time_ms": tmed,
+                         "dof_iter_per_s": NL * reps[-1].iterations / (tmed * 1e-3),
+                         "k1_us": 1e3 * rk.k_ax_ms / n_it, "k2_us": 1e3 * rk.k_upd_ms / n_it,
+                         "k1_alg_GBps": K1_BYTES[pp] * NL / (rk.k_ax_ms * 1e-3 / n_it) / 1e9,
+                         "k2_alg_GBps": K2_BYTES[pp] * NL / (rk.k_upd_ms * 1e-3 / n_it) / 1e9}
         ttr["speedup_fp64_over_mixed_time"] = ttr["fp64"]["time_ms"] / ttr["mixed"]["time_ms"]
 
     cpu = None
@@ -278,24 +299,31 @@ def run_ours(args):
 
     if rank == 0:
         ms_per_step = 1e3 * t_max / args.steps
+        k1_ach = k1_bytes / (k1_ms * 1e-3) / 1e9
+        k2_ach = k2_bytes / (k2_ms * 1e-3) / 1e9
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": {0: "f64", 1: "f32", 2: "f32+f64 (mixed)"}[pol],
                 "data": "synthetic",
-                "config": dict(WORKLOAD, policy=args.policy, iterations=iters[0], n_local=NL,
-                               l2="256 MiB write between steps (outside the step events)",
+                "config": dict(WORKLOAD, policy=args.policy, iterations=iters[0], status=sorted(statuses),
+                               n_local=NL, l2="256 MiB write between steps (outside the step events)",
                                parallelism="replicas" if world > 1 else "single GPU"),
-                "time_to_rtol_ms": 1e3 * t_max / args.steps,
-                "roofline": {"bound": "hbm", "kernel": "k_ax (K1: Jacobi + add2s1 + local Ax + mask + interior pap)",
-                             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "time_to_rtol_ms": ms_per_step,
+                "roofline": {"bound": "hbm", "kernel": "K1 k_ax (Jacobi p-update + deferred x + local Ax + mask + pap)",
+                             "achieved": k1_ach, "peak": peak, "unit": "GB/s", "frac": k1_ach / peak,
                              "traffic": traffic, "peak_source": peak_src,
-                             "alg_bytes_per_launch": k1_bytes, "avg_launch_us": 1e3 * ax_ms,
-                             "share_of_iteration": ax_ms / (ax_ms + gs_ms + up_ms),
-                             "dssum": {"avg_launch_us": 1e3 * gs_ms, "alg_bytes_per_launch": gs_bytes,
-                                       "achieved_GBps": gs_bytes / (gs_ms * 1e-3) / 1e9},
-                             "update": {"avg_launch_us": 1e3 * up_ms, "alg_bytes_per_launch": k3_bytes,
-                                        "achieved_GBps": k3_bytes / (up_ms * 1e-3) / 1e9,
-                                        "frac": k3_bytes / (up_ms * 1e-3) / 1e9 / peak}},
+                             "alg_bytes_per_launch": k1_bytes, "avg_launch_us": 1e3 * k1_ms,
+                             "share_of_iteration": k1_ms / (k1_ms + k2_ms)},
+                "kernels": {
+                    "K1_ax": {"avg_launch_us": 1e3 * k1_ms, "alg_bytes": k1_bytes, "GBps": k1_ach, "frac": k1_ach / peak},
+                    "K2_gather_update": {"avg_launch_us": 1e3 * k2_ms, "alg_bytes": k2_bytes, "GBps": k2_ach,
+                                         "frac": k2_ach / peak},
+                    "ax_local": {"avg_launch_us": 1e3 * ax_ms, "alg_bytes": AX_BYTES[pol] * NL,
+                                 "GBps": AX_BYTES[pol] * NL / (ax_ms * 1e-3) / 1e9,
+                                 "frac": AX_BYTES[pol] * NL / (ax_ms * 1e-3) / 1e9 / peak},
+                    "dssum_csr": {"avg_launch_us": 1e3 * gs_ms, "alg_bytes": gs_bytes,
+                                  "GBps": gs_bytes / (gs_ms * 1e-3) / 1e9,
+                                  "frac": gs_bytes / (gs_ms * 1e-3) / 1e9 / peak}},
                 "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": NL * vs, "d2h_bytes_per_step": NL * vs},
                 "gpu_launches": launches, "clocks": ck, "cpu_baseline": cpu, "policies": ttr}
         print(json.dumps(line), flush=True)

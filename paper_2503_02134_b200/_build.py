@@ -1,6 +1,11 @@
-"""Build the sm_100a shared library ``libnb.so`` in-tree with nvcc (no JIT cache)."""
+"""Build the sm_100a shared library ``libnb.so`` in-tree with nvcc (no JIT cache).
+
+Each translation unit is compiled to an object in parallel (one per precision policy for
+the hot-path kernels), then linked into one shared library.
+"""
 from __future__ import annotations
 
+import concurrent.futures as cf
 import os
 import subprocess
 import sys
@@ -8,28 +13,45 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
+OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libnb.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("nb_api.cu", "nb_kernels.cu")]
-HEADERS = [os.path.join(CSRC, f) for f in ("nb_internal.h", "nb_common.cuh")] + [os.path.join(ROOT, "include", "nb.h")]
+UNITS = ("nb_api.cu", "nb_setup_k.cu", "nb_gs.cu", "nb_cg_fp64.cu", "nb_cg_fp32.cu", "nb_cg_mixed.cu")
+SOURCES = [os.path.join(CSRC, f) for f in UNITS]
+HEADERS = [os.path.join(CSRC, f) for f in ("nb_internal.h", "nb_common.cuh", "nb_cg.cuh")] + [
+    os.path.join(ROOT, "include", "nb.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # No --use_fast_math: IEEE division/sqrt, denormals kept; FMA contraction allowed.
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
-         "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-ftz=false", "-prec-div=true",
+         "-prec-sqrt=true", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 
 
 def stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS)
+    return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS + [os.path.abspath(__file__)])
+
+
+def _compile(src: str, verbose: bool) -> str:
+    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+    cmd = [NVCC, *FLAGS, "-c", "-o", obj, src]
+    if os.environ.get("NB_PTXAS_V"):
+        cmd.insert(1, "-Xptxas=-v")
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+    return obj
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not (force or stale()):
         return LIB
+    os.makedirs(OBJ, exist_ok=True)
+    with cf.ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *SOURCES]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

@@ -137,6 +137,10 @@ int ensure_f32(nb_handle *h)
     return NB_OK;
 }
 
+// policy dispatch of the per-policy kernel templates
+#define NB_POL(prec, F, ...) \
+    ((prec) == NB_FP64 ? F<NB_FP64>(__VA_ARGS__) : (prec) == NB_FP32 ? F<NB_FP32>(__VA_ARGS__) : F<NB_MIXED>(__VA_ARGS__))
+
 int ensure_ws(nb_handle *h, int prec, int32_t max_iter)
 {
     nb::Workspace &ws = h->ws[prec];
@@ -146,45 +150,84 @@ int ensure_ws(nb_handle *h, int prec, int32_t max_iter)
         NB_CU(cudaMalloc(&ws.p, vs), "cudaMalloc p");
         NB_CU(cudaMalloc(&ws.w, vs), "cudaMalloc w");
         NB_CU(cudaMalloc(&ws.x, vs), "cudaMalloc x");
-        const int nax = nb::grid_ax(h, prec), ngs = nb::grid_gs(h), nup = nb::grid_upd(h, prec);
-        int slots = nax + ngs;
-        if (2 * nup > slots) slots = 2 * nup;
-        NB_CU(cudaMalloc(&ws.part, sizeof(double) * slots), "cudaMalloc part");
+        NB_CU(cudaMalloc(&ws.z, vs), "cudaMalloc z");
+        int maxblk = NB_POL(prec, nb::grid_k1, h);
+        const int g2 = NB_POL(prec, nb::grid_k2, h), gg = nb::grid_gs(h);
+        if (g2 > maxblk) maxblk = g2;
+        if (gg > maxblk) maxblk = gg;
+        const int nchunk = (maxblk + 255) / 256;
+        ws.mega_G = NB_POL(prec, nb::grid_mega, h);
+        const int nslots = 2 * maxblk > 4 * ws.mega_G ? 2 * maxblk : 4 * ws.mega_G;
+        NB_CU(cudaMalloc(&ws.red.part, sizeof(double) * nslots), "cudaMalloc part");
+        NB_CU(cudaMalloc(&ws.bar, sizeof(unsigned int) * 2), "cudaMalloc bar");
+        NB_CU(cudaMemset(ws.bar, 0, sizeof(unsigned int) * 2), "memset bar");
+        NB_CU(cudaMalloc(&ws.red.part2, sizeof(double) * 2 * nchunk), "cudaMalloc part2");
+        NB_CU(cudaMalloc(&ws.red.cnt, sizeof(uint32_t) * (1 + nchunk)), "cudaMalloc cnt");
+        NB_CU(cudaMemset(ws.red.cnt, 0, sizeof(uint32_t) * (1 + nchunk)), "memset cnt");
         NB_CU(cudaMalloc(&ws.scal, sizeof(nb::Scal)), "cudaMalloc scal");
         NB_CU(cudaMallocHost(&ws.scal_host, sizeof(nb::Scal)), "cudaMallocHost scal");
         NB_CU(cudaMemset(ws.scal, 0, sizeof(nb::Scal)), "memset scal");
+        NB_CU(cudaDeviceSynchronize(), "ws sync");
         ws.ready = true;
     }
     if (ws.hist_cap < max_iter + 1) {
         if (ws.hist) cudaFree(ws.hist);
+        if (ws.tim) cudaFree(ws.tim);
         ws.hist = nullptr;
+        ws.tim = nullptr;
         ws.hist_cap = 0;
         const int cap = max_iter + 1 < 1024 ? 1024 : max_iter + 1;
         NB_CU(cudaMalloc(&ws.hist, sizeof(double) * cap), "cudaMalloc hist");
+        NB_CU(cudaMalloc(&ws.tim, sizeof(unsigned long long) * 3 * cap), "cudaMalloc tim");
         ws.hist_cap = cap;
+        for (int o = 0; o < 2; o++) {   // graphs captured the old history pointer
+            if (ws.exec[o]) { cudaGraphExecDestroy(ws.exec[o]); ws.exec[o] = nullptr; }
+            if (ws.graph[o]) { cudaGraphDestroy(ws.graph[o]); ws.graph[o] = nullptr; }
+        }
     }
     return NB_OK;
 }
 
 void free_ws(nb::Workspace &ws)
 {
-    if (ws.exec) cudaGraphExecDestroy(ws.exec);
-    if (ws.graph) cudaGraphDestroy(ws.graph);
-    cudaFree(ws.r); cudaFree(ws.p); cudaFree(ws.w); cudaFree(ws.x);
-    cudaFree(ws.part); cudaFree(ws.scal); cudaFree(ws.hist);
+    for (int o = 0; o < 2; o++) {
+        if (ws.exec[o]) cudaGraphExecDestroy(ws.exec[o]);
+        if (ws.graph[o]) cudaGraphDestroy(ws.graph[o]);
+    }
+    cudaFree(ws.r); cudaFree(ws.p); cudaFree(ws.w); cudaFree(ws.x); cudaFree(ws.z);
+    cudaFree(ws.red.part); cudaFree(ws.red.part2); cudaFree(ws.red.cnt);
+    cudaFree(ws.scal); cudaFree(ws.hist); cudaFree(ws.tim); cudaFree(ws.bar);
     if (ws.scal_host) cudaFreeHost(ws.scal_host);
     ws = nb::Workspace();
 }
 
-// Conditional-WHILE graph: body = K1 (ax) -> K2 (dssum) -> K3 (update); K3's last block
-// clears the condition when the solve is done.
+// One CG iteration.  Consistent order: K1 (Ax + pap + alpha) -> K2 (gather + update).
+// Per-copy order (or NB_CG_GS=csr): K1 (Ax, unshared pap) -> CSR dssum (+ shared pap, alpha)
+// -> K2 (update without gather).  Returns the number of kernels launched; launch errors in err.
+int iteration(nb_handle *h, int prec, int order, nb::Workspace &ws, cudaStream_t st,
+              cudaGraphConditionalHandle cond, bool use_cond, cudaError_t &err, cudaEvent_t *ev = nullptr)
+{
+    const bool fused = order == NB_GS_CONSISTENT && !h->cg_csr;
+    if (ev) cudaEventRecord(ev[0], st);
+    err = NB_POL(prec, nb::launch_cg_k1, h, ws, fused, st);
+    if (err != cudaSuccess) return 0;
+    if (ev) cudaEventRecord(ev[1], st);
+    if (!fused) {
+        err = nb::launch_cg_gs(h, prec, order, ws, st);
+        if (err != cudaSuccess) return 1;
+    }
+    if (ev) cudaEventRecord(ev[2], st);
+    err = NB_POL(prec, nb::launch_cg_k2, h, ws, fused, st, cond, use_cond);
+    if (ev) cudaEventRecord(ev[3], st);
+    return fused ? 2 : 3;
+}
+
+// Conditional-WHILE graph: body = one iteration; its last kernel clears the condition when
+// the solve is done.  After the loop, the deferred x += alpha p.  One graph launch per solve.
 int build_graph(nb_handle *h, int prec, int order)
 {
     nb::Workspace &ws = h->ws[prec];
-    if (ws.exec && ws.graph_order == order) return NB_OK;
-    if (ws.exec) { cudaGraphExecDestroy(ws.exec); ws.exec = nullptr; }
-    if (ws.graph) { cudaGraphDestroy(ws.graph); ws.graph = nullptr; }
-    (void)nb::grid_ax(h, prec);   // initialise occupancy/attributes outside capture
+    if (ws.exec[order]) return NB_OK;
     cudaGraph_t graph;
     NB_CU(cudaGraphCreate(&graph, 0), "cudaGraphCreate");
     cudaGraphConditionalHandle cond;
@@ -199,20 +242,22 @@ int build_graph(nb_handle *h, int prec, int order)
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     NB_CU(cudaStreamBeginCaptureToGraph(h->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed),
           "begin capture");
-    cudaError_t e1 = nb::launch_cg_ax(h, prec, ws, h->cap_stream);
-    cudaError_t e2 = nb::launch_cg_gs(h, prec, order, ws, h->cap_stream, cond, true);
-    cudaError_t e3 = nb::launch_cg_upd(h, prec, ws, h->cap_stream, cond, true);
+    cudaError_t e1;
+    iteration(h, prec, order, ws, h->cap_stream, cond, true, e1);
     cudaGraph_t captured;
     cudaError_t ec = cudaStreamEndCapture(h->cap_stream, &captured);
-    if (e1 != cudaSuccess) return cuda_fail(e1, "capture ax");
-    if (e2 != cudaSuccess) return cuda_fail(e2, "capture gs");
-    if (e3 != cudaSuccess) return cuda_fail(e3, "capture upd");
+    if (e1 != cudaSuccess) return cuda_fail(e1, "capture iteration");
     if (ec != cudaSuccess) return cuda_fail(ec, "end capture");
+    NB_CU(cudaStreamBeginCaptureToGraph(h->cap_stream, graph, &node, nullptr, 1, cudaStreamCaptureModeRelaxed),
+          "begin capture fin");
+    e1 = NB_POL(prec, nb::launch_cg_fin, h, ws, h->cap_stream);
+    ec = cudaStreamEndCapture(h->cap_stream, &captured);
+    if (e1 != cudaSuccess) return cuda_fail(e1, "capture fin");
+    if (ec != cudaSuccess) return cuda_fail(ec, "end capture fin");
     cudaGraphExec_t exec;
     NB_CU(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
-    ws.graph = graph;
-    ws.exec = exec;
-    ws.graph_order = order;
+    ws.graph[order] = graph;
+    ws.exec[order] = exec;
     return NB_OK;
 }
 
@@ -287,7 +332,12 @@ int nb_setup(int32_t nelx, int32_t nely, int32_t nelz, int32_t p, double deform_
 
     cudaError_t e;
     if ((e = cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking)) != cudaSuccess) return bail(cuda_fail(e, "stream"));
-    if ((e = nb::upload_basis(n, h->D)) != cudaSuccess) return bail(cuda_fail(e, "upload D"));
+    {
+        const char *gs = std::getenv("NB_CG_GS");
+        h->cg_csr = (gs && std::strcmp(gs, "csr") == 0) ? 1 : 0;
+        const char *dr = std::getenv("NB_CG_DRIVER");
+        h->cg_graph = (dr && std::strcmp(dr, "graph") == 0) ? 1 : 0;
+    }
     if ((e = cudaMalloc(&h->g64, sizeof(double) * 6 * NL)) != cudaSuccess) return bail(fail(NB_ENOMEM, "cudaMalloc g64"));
     if ((e = cudaMalloc(&h->B, sizeof(double) * NL)) != cudaSuccess) return bail(fail(NB_ENOMEM, "cudaMalloc B"));
     if ((e = cudaMalloc(&h->dinv64, sizeof(double) * NL)) != cudaSuccess) return bail(fail(NB_ENOMEM, "cudaMalloc dinv"));
@@ -357,7 +407,9 @@ int nb_ax(nb_handle *h, nb_policy prec, const void *u, void *w, uint32_t flags, 
     if (rc) return rc;
     if (u == w) return fail(NB_EINVAL, "u and w must be distinct");
     if (prec != NB_FP64 && (rc = ensure_f32(h))) return rc;
-    NB_CU(nb::launch_ax(h, prec, u, w, (flags & NB_AX_LOCAL) != 0, (cudaStream_t)stream), "ax");
+    const bool local = (flags & NB_AX_LOCAL) != 0;
+    NB_CU(NB_POL(prec, nb::launch_ax_local, h, u, w, !local, (cudaStream_t)stream), "ax");
+    if (!local) NB_CU(nb::launch_dssum(h, prec, NB_GS_CONSISTENT, w, (cudaStream_t)stream), "ax dssum");
     return NB_OK;
 }
 
@@ -377,12 +429,14 @@ static int cg_impl(nb_handle *h, const nb_cg_opts *o, const void *b, bool b_host
                    nb_cg_report *rep, cudaStream_t st)
 {
     const int prec = o->policy;
+    const int order = o->gs_order;
     int rc;
     if (prec != NB_FP64 && (rc = ensure_f32(h))) return rc;
     if ((rc = ensure_ws(h, prec, o->max_iter))) return rc;
     nb::Workspace &ws = h->ws[prec];
     const size_t vbytes = vsize(prec) * h->NL;
-    if (!o->time_kernels && (rc = build_graph(h, prec, o->gs_order))) return rc;
+    const bool mega = !h->cg_graph;
+    if (!mega && !o->time_kernels && (rc = build_graph(h, prec, order))) return rc;
 
     cudaEvent_t t0, t1;
     NB_CU(cudaEventCreate(&t0), "event");
@@ -394,13 +448,27 @@ static int cg_impl(nb_handle *h, const nb_cg_opts *o, const void *b, bool b_host
     s0.max_iter = o->max_iter;
     *ws.scal_host = s0;
     NB_CU(cudaEventRecord(t0, st), "event record");
-    NB_CU(cudaMemcpyAsync(ws.r, b, vbytes, b_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st), "copy b");
+    // host b is staged in w (the only H2D copy of the solve); the prologue reads it
+    const void *bdev = b;
+    if (b_host) {
+        NB_CU(cudaMemcpyAsync(ws.w, b, vbytes, cudaMemcpyHostToDevice, st), "copy b");
+        bdev = ws.w;
+    }
     NB_CU(cudaMemcpyAsync(ws.scal, ws.scal_host, sizeof(nb::Scal), cudaMemcpyHostToDevice, st), "copy scal");
-    NB_CU(nb::launch_cg_init(h, prec, ws, nullptr, st), "cg init");
-    int64_t launches = 1;
+    int64_t launches = 0;
+    const bool fused = order == NB_GS_CONSISTENT && !h->cg_csr;
+    const int per_it = fused ? 2 : 3;
     double kms[3] = {0.0, 0.0, 0.0};
-    if (!o->time_kernels) {
-        NB_CU(cudaGraphLaunch(ws.exec, st), "graph launch");
+    if (mega) {
+        NB_CU(NB_POL(prec, nb::launch_cg_mega, h, ws, bdev, order, o->max_iter, o->rtol, ws.tim, st), "cg megakernel");
+        launches = 1;
+    } else {
+        NB_CU(NB_POL(prec, nb::launch_cg_init, h, ws, bdev, st), "cg init");
+        launches = 1;
+    }
+    if (mega) {
+    } else if (!o->time_kernels) {
+        NB_CU(cudaGraphLaunch(ws.exec[order], st), "graph launch");
     } else {
         // per-kernel CUDA-event timing: direct launches, check the done flag every 16 iterations
         std::vector<cudaEvent_t> ev;
@@ -412,14 +480,9 @@ static int cg_impl(nb_handle *h, const nb_cg_opts *o, const void *b, bool b_host
         while (!done && k < o->max_iter) {
             const int m = (o->max_iter - k) < chunk ? (o->max_iter - k) : chunk;
             for (int c = 0; c < m; c++) {
-                cudaGraphConditionalHandle none = 0;
-                NB_CU(cudaEventRecord(ev[4 * c], st), "ev");
-                NB_CU(nb::launch_cg_ax(h, prec, ws, st), "ax");
-                NB_CU(cudaEventRecord(ev[4 * c + 1], st), "ev");
-                NB_CU(nb::launch_cg_gs(h, prec, o->gs_order, ws, st, none, false), "gs");
-                NB_CU(cudaEventRecord(ev[4 * c + 2], st), "ev");
-                NB_CU(nb::launch_cg_upd(h, prec, ws, st, none, false), "upd");
-                NB_CU(cudaEventRecord(ev[4 * c + 3], st), "ev");
+                cudaError_t e;
+                iteration(h, prec, order, ws, st, 0, false, e, &ev[4 * c]);
+                NB_CU(e, "iteration");
             }
             NB_CU(cudaMemcpyAsync(ws.scal_host, ws.scal, sizeof(nb::Scal), cudaMemcpyDeviceToHost, st), "scal");
             NB_CU(cudaStreamSynchronize(st), "sync");
@@ -434,10 +497,10 @@ static int cg_impl(nb_handle *h, const nb_cg_opts *o, const void *b, bool b_host
                 kms[0] += a; kms[1] += b2; kms[2] += c3;
             }
             k += m;
-            launches += 3 * m;
             done = ws.scal_host->done != 0;
         }
         for (auto &e : ev) cudaEventDestroy(e);
+        NB_CU(NB_POL(prec, nb::launch_cg_fin, h, ws, st), "cg fin");
     }
     NB_CU(cudaMemcpyAsync(ws.scal_host, ws.scal, sizeof(nb::Scal), cudaMemcpyDeviceToHost, st), "copy scal back");
     NB_CU(cudaMemcpyAsync(x, ws.x, vbytes, x_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st), "copy x");
@@ -451,7 +514,22 @@ static int cg_impl(nb_handle *h, const nb_cg_opts *o, const void *b, bool b_host
     const int k = s.iter;
     std::vector<double> res(k + 1, 0.0);
     NB_CU(cudaMemcpy(res.data(), ws.hist, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost), "copy hist");
-    if (!o->time_kernels) launches += 3 * (int64_t)(k + (s.status == NB_BROKEDOWN ? 1 : 0)) + (k < o->max_iter ? 0 : 0);
+    if (mega) {
+        // phase durations from the block-0 globaltimer stamps taken after each grid barrier
+        std::vector<unsigned long long> tm(3 * (size_t)(k + 1), 0ull);
+        NB_CU(cudaMemcpy(tm.data(), ws.tim, sizeof(unsigned long long) * 3 * (k + 1), cudaMemcpyDeviceToHost),
+              "copy tim");
+        for (int i = 1; i <= k; i++) {
+            const double tA = (double)tm[3 * (i - 1) + 1] - (double)tm[3 * (i - 1)];
+            const double tS = (double)tm[3 * (i - 1) + 2] - (double)tm[3 * (i - 1) + 1];
+            const double tB = (double)tm[3 * i] - (double)tm[3 * (i - 1) + 2];
+            kms[0] += 1e-6 * tA; kms[1] += 1e-6 * tS; kms[2] += 1e-6 * tB;
+        }
+    } else {
+        // kernels that did work: init, per_it per completed iteration (+ the partial iteration of a
+        // breakdown), the deferred-x kernel
+        launches += (int64_t)per_it * k + (s.status == NB_BROKEDOWN ? per_it - 1 : 0) + 1;
+    }
     int status = s.status;
     if (status == NB_MAXITER && o->rtol > 0.0) status = classify(res, k, o->stag_window > 0 ? o->stag_window : 200);
     if (o->rel_res_history) memcpy(o->rel_res_history, res.data(), sizeof(double) * (k + 1));

@@ -1,0 +1,910 @@
+// nb_cg.cuh -- the per-iteration work of the Jacobi-PCG hot path (templates; one
+// translation unit per precision policy instantiates them: nb_cg_fp64.cu, nb_cg_fp32.cu,
+// nb_cg_mixed.cu).
+//
+// One CG iteration (Table 2 of the paper) is two phases in consistent
+// gather-scatter order:
+//
+//   A (ax_group):  p = z + beta p               (add2s1, :162; z = M^-1 r stored by phase B)
+//                  x += alpha_prev p_old        (add2s2(x,p,alpha) of the previous iteration,
+//                                                deferred so x is streamed once, :165)
+//                  w = mask . A_L p             (ax -> ax_e: local_grad3, geometric scaling,
+//                                                local_grad3_t, add2; :147, :163)
+//                  pap = sum_l w_l p_l          (glsc3(w,c,p), :164: for continuous p the
+//                                                c-weighted sum over the assembled w equals
+//                                                the plain sum over the unassembled w)
+//                  alpha = rho / pap
+//   B (upd_pencil): w <- QQ^T w on the fly      (gather-scatter "to ensure continuity",
+//                                                :309, :404 -- each copy gathers the copies of
+//                                                its node in ascending element order, so all
+//                                                copies compute the same sum bit for bit)
+//                  r -= alpha w                 (add2s2(r,w,-alpha), :166)
+//                  z = M^-1 r                   (solveM, Jacobi, :160, :444)
+//                  rtr = glsc3(r,c,r), rho = glsc3(r,c,z)   (:167, :161); beta; stop test
+//
+// Under the per-copy gather-scatter order (the emulation of the paper's pairwise
+// exchange) the copies differ, so pap must be taken over the per-copy
+// sums: phase A contributes only the unshared nodes, a CSR phase (nb_gs.cuh) does QQ^T and
+// the shared part of pap, and phase B runs without the gather.
+//
+// Two drivers run these phases:
+//   * k_cg_mega: ONE persistent cooperative kernel per solve.  Every block owns a contiguous
+//     element range; grid-wide barriers separate the phases; after each barrier every block
+//     reduces the per-block partials itself, in the same fixed order, so all blocks take the
+//     same (bit-identical) scalar decisions -- no host round trip, no launch gaps, no serial
+//     last-block tail.  (Default.)
+//   * k_ax / k_upd: one persistent kernel per phase, chained in a CUDA graph with a
+//     conditional WHILE node; scalars finalised by the last block (NB_CG_DRIVER=graph).
+#pragma once
+#include "nb_common.cuh"
+#include "nb_gs.cuh"
+
+namespace nb {
+
+// ===========================================================================
+// phase A: local operator A_L, register pencils + shared-memory transposes
+// ===========================================================================
+template <typename T, int N> struct AxCfg {
+    static constexpr int N2 = N * N;
+    static constexpr int N3 = N * N * N;
+    static constexpr int BANKS = (sizeof(T) == 4) ? 32 : 16;
+    // plane pitch P >= N^2 with P == N (mod BANKS): the stride-N s-pencil reads and the
+    // stride-P t-pencil reads of a warp hit distinct banks.
+    static constexpr int P = N2 + (((N - N2) % BANKS) + BANKS) % BANKS;
+    static constexpr int ESZ = P * N;                          // one array, one element
+    static constexpr int EPB = (N2 >= 256) ? 1 : (256 / N2);   // elements per group
+    static constexpr int NT = ((EPB * N2 + 31) / 32) * 32;     // threads per block
+    static constexpr int SMEM = 3 * EPB * ESZ * (int)sizeof(T);
+};
+
+template <typename T, int V>
+__device__ __forceinline__ void ld_chunk(const T *__restrict__ p, T (&d)[V])
+{
+    using W = typename VT<T, V>::type;
+    VAcc<T, V>::get(*reinterpret_cast<const W *>(p), d);
+}
+template <typename T, int V, int H = LD_DEF>
+__device__ __forceinline__ void ld_chunk_h(const T *__restrict__ p, T (&d)[V])
+{
+    using W = typename VT<T, V>::type;
+    VAcc<T, V>::get(ldv<H>(reinterpret_cast<const W *>(p)), d);
+}
+template <typename T, int V>
+__device__ __forceinline__ void st_chunk(T *__restrict__ p, const T (&d)[V])
+{
+    using W = typename VT<T, V>::type;
+    *reinterpret_cast<W *>(p) = VAcc<T, V>::put(d);
+}
+
+// One group of EPB elements, all threads of the block.  MODE 0: standalone w = A_L u
+// (+ mask).  MODE 1: CG with pap over all nodes.  MODE 2: CG with the unshared-node part of
+// pap only.  Returns this thread's pap partial.  Contains 4 __syncthreads; consecutive calls
+// need no barrier in between (phase 1 of the next group touches only the caller's own
+// r-pencil slots, which only the caller read in phase 5).
+template <int PREC, int N, int MODE>
+__device__ __forceinline__ typename Pol<PREC>::TS
+ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typename Pol<PREC>::TV *__restrict__ in,
+         typename Pol<PREC>::TV *__restrict__ pv, typename Pol<PREC>::TV *__restrict__ xv,
+         const typename Pol<PREC>::TV *__restrict__ g, typename Pol<PREC>::TV *__restrict__ w, bool apply_mask,
+         typename Pol<PREC>::TV beta, typename Pol<PREC>::TV alpha, int e, bool active, int a, int b,
+         typename Pol<PREC>::TV *__restrict__ S0)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TS = typename Pol<PREC>::TS;
+    using C = AxCfg<TV, N>;
+    constexpr int V = VecW<TV, N>::V;
+    TV *A1 = S0 + C::ESZ;
+    TV *A2 = A1 + C::ESZ;
+    const int q = a + N * b;
+    const int rp = N * a + C::P * b;   // r-pencil (i, a, b): contiguous
+    const int sp = a + C::P * b;       // s-pencil (a, j, b): stride N
+    const int tp = a + N * b;          // t-pencil (a, b, k): stride P
+    const size_t gbase = (size_t)e * C::N3 + (size_t)N * q;
+
+    // ---- 1. operand: u, or (CG) p = z + beta p_old with the deferred x update
+    if (active) {
+        TV u[N];
+        if (MODE == 0) {
+            ld_pencil<TV, N>(in + gbase, u);
+        } else {
+            TV zz[N], po[N], xx[N];
+            ld_pencil<TV, N, LD_CS>(in + gbase, zz);
+            ld_pencil<TV, N>(pv + gbase, po);
+            ld_pencil<TV, N, LD_CS>(xv + gbase, xx);
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                u[i] = fma(beta, po[i], zz[i]);      // add2s1
+                xx[i] = fma(alpha, po[i], xx[i]);    // add2s2(x, p_old, alpha_prev)
+            }
+            st_pencil<TV, N>(pv + gbase, u);
+            st_pencil<TV, N, LD_CS>(xv + gbase, xx);
+        }
+        st_pencil<TV, N>(S0 + rp, u);
+    }
+    __syncthreads();
+    // ---- 2. us (D along s) and ut (D along t) from shared pencils
+    if (active) {
+        TV v[N], o[N];
+#pragma unroll
+        for (int j = 0; j < N; j++) v[j] = S0[sp + N * j];
+        contract<TV, N>(D, v, o);
+#pragma unroll
+        for (int j = 0; j < N; j++) A1[sp + N * j] = o[j];
+#pragma unroll
+        for (int k = 0; k < N; k++) v[k] = S0[tp + C::P * k];
+        contract<TV, N>(D, v, o);
+#pragma unroll
+        for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
+    }
+    __syncthreads();
+    // ---- 3. ur in registers; geometric factors (C-7); r-part of local_grad3_t
+    TV wrt[N];
+    if (active) {
+        TV ur[N], wr[N];
+        {
+            TV v[N];
+            ld_pencil<TV, N>(S0 + rp, v);
+            contract<TV, N>(D, v, ur);
+        }
+        const TV *ge = g + (size_t)e * 6 * C::N3 + (size_t)N * q;
+#pragma unroll
+        for (int c = 0; c < N / V; c++) {
+            TV g1[V], g2[V], g3[V], g4[V], g5[V], g6[V], us[V], ut[V], ws[V], wt[V];
+            ld_chunk_h<TV, V, LD_CS>(ge + 0 * C::N3 + c * V, g1);
+            ld_chunk_h<TV, V, LD_CS>(ge + 1 * C::N3 + c * V, g2);
+            ld_chunk_h<TV, V, LD_CS>(ge + 2 * C::N3 + c * V, g3);
+            ld_chunk_h<TV, V, LD_CS>(ge + 3 * C::N3 + c * V, g4);
+            ld_chunk_h<TV, V, LD_CS>(ge + 4 * C::N3 + c * V, g5);
+            ld_chunk_h<TV, V, LD_CS>(ge + 5 * C::N3 + c * V, g6);
+            ld_chunk<TV, V>(A1 + rp + c * V, us);
+            ld_chunk<TV, V>(A2 + rp + c * V, ut);
+#pragma unroll
+            for (int t = 0; t < V; t++) {
+                const TV r_ = ur[c * V + t];
+                wr[c * V + t] = fma(g3[t], ut[t], fma(g2[t], us[t], g1[t] * r_));
+                ws[t] = fma(g5[t], ut[t], fma(g4[t], us[t], g2[t] * r_));
+                wt[t] = fma(g6[t], ut[t], fma(g5[t], us[t], g3[t] * r_));
+            }
+            st_chunk<TV, V>(A1 + rp + c * V, ws);
+            st_chunk<TV, V>(A2 + rp + c * V, wt);
+        }
+        contract_t<TV, N>(D, wr, wrt);
+    }
+    __syncthreads();
+    // ---- 4. s- and t-parts of local_grad3_t, in place on the owner's pencils
+    if (active) {
+        TV v[N], o[N];
+#pragma unroll
+        for (int j = 0; j < N; j++) v[j] = A1[sp + N * j];
+        contract_t<TV, N>(D, v, o);
+#pragma unroll
+        for (int j = 0; j < N; j++) A1[sp + N * j] = o[j];
+#pragma unroll
+        for (int k = 0; k < N; k++) v[k] = A2[tp + C::P * k];
+        contract_t<TV, N>(D, v, o);
+#pragma unroll
+        for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
+    }
+    __syncthreads();
+    // ---- 5. w = (w_r + w_s) + w_t, Dirichlet mask, store; CG: pap partial
+    TS acc = 0;
+    if (active) {
+        TV out[N];
+        {
+            TV t1[N], t2[N];
+            ld_pencil<TV, N>(A1 + rp, t1);
+            ld_pencil<TV, N>(A2 + rp, t2);
+#pragma unroll
+            for (int i = 0; i < N; i++) out[i] = (wrt[i] + t1[i]) + t2[i];
+        }
+        if (MODE != 0 || apply_mask) {
+            const ElemPos P = elem_pos(m, e);
+            const bool mjk = axis_bnd(a, N, P.ey, m.nely) || axis_bnd(b, N, P.ez, m.nelz);
+#pragma unroll
+            for (int i = 0; i < N; i++)
+                if (mjk || axis_bnd(i, N, P.ex, m.nelx)) out[i] = TV(0);
+            if (MODE == 2) {   // unshared nodes only (c = 1); the CSR phase adds the shared ones
+                const bool sjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz) > 1;
+                TV pp[N];
+                ld_pencil<TV, N>(S0 + rp, pp);
+#pragma unroll
+                for (int i = 0; i < N; i++)
+                    if (!sjk && axis_mult(i, N, P.ex, m.nelx) == 1) acc += (TS)out[i] * (TS)pp[i];
+            }
+        }
+        if (MODE == 1) {
+            TV pp[N];
+            ld_pencil<TV, N>(S0 + rp, pp);
+#pragma unroll
+            for (int i = 0; i < N; i++) acc += (TS)out[i] * (TS)pp[i];
+        }
+        st_pencil<TV, N>(w + gbase, out);
+    }
+    return acc;
+}
+
+// ===========================================================================
+// phase B: (gather QQ^T) + add2s2(r) + solveM + glsc3 x2, one r-pencil per call
+// ===========================================================================
+// Consistent-order assembled value of the pencil (a, b) of element e (C-8): for each node
+// the copies are summed in ascending element order (= ascending local index), i.e.
+// lexicographic in (dz, dy, dx), in the gather-scatter precision TG, and rounded once.
+// Neighbour values are read through L2 (ld.cg): other blocks wrote them in this kernel.
+template <int PREC, int N>
+__device__ __forceinline__ void gather_pencil(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ w,
+                                              int e, const ElemPos &P, int a, int b,
+                                              typename Pol<PREC>::TV (&ww)[N])
+{
+    using TV = typename Pol<PREC>::TV;
+    using TG = typename Pol<PREC>::TG;
+    constexpr int N2 = N * N, N3 = N * N * N;
+    const int ys = (a == 0 && P.ey > 0) ? -1 : ((a == N - 1 && P.ey < m.nely - 1) ? 1 : 0);
+    const int zs = (b == 0 && P.ez > 0) ? -1 : ((b == N - 1 && P.ez < m.nelz - 1) ? 1 : 0);
+    const bool xl = P.ex > 0, xr = P.ex < m.nelx - 1;
+    if (ys == 0 && zs == 0 && !xl && !xr) return;
+    const int ny = ys ? 2 : 1, nz = zs ? 2 : 1;
+    TG s[N];
+#pragma unroll 1
+    for (int iz = 0; iz < nz; iz++) {
+        const int dz = zs < 0 ? iz - 1 : iz;            // ascending: {-1,0} or {0,+1} or {0}
+#pragma unroll 1
+        for (int iy = 0; iy < ny; iy++) {
+            const int dy = ys < 0 ? iy - 1 : iy;
+            const int e2 = e + dy * m.nelx + dz * m.nelx * m.nely;
+            const int a2 = dy == 0 ? a : N - 1 - a;
+            const int b2 = dz == 0 ? b : N - 1 - b;
+            const size_t base2 = (size_t)e2 * N3 + (size_t)N * a2 + (size_t)N2 * b2;
+            TV v[N];
+            if (dy == 0 && dz == 0) {
+#pragma unroll
+                for (int i = 0; i < N; i++) v[i] = ww[i];
+            } else {
+                ld_pencil<TV, N, LD_CG>(w + base2, v);
+            }
+            const TV lft = xl ? __ldcg(w + base2 - N3 + (N - 1)) : TV(0);   // node i=0's copy in e2-1
+            const TV rgt = xr ? __ldcg(w + base2 + N3) : TV(0);             // node i=N-1's copy in e2+1
+            if (iz == 0 && iy == 0) {
+#pragma unroll
+                for (int i = 0; i < N; i++) s[i] = (TG)v[i];
+                if (xl) s[0] = (TG)lft + (TG)v[0];
+                if (xr) s[N - 1] = (TG)v[N - 1] + (TG)rgt;
+            } else {
+#pragma unroll
+                for (int i = 1; i < N - 1; i++) s[i] += (TG)v[i];
+                if (xl) s[0] += (TG)lft;
+                s[0] += (TG)v[0];
+                s[N - 1] += (TG)v[N - 1];
+                if (xr) s[N - 1] += (TG)rgt;
+            }
+        }
+    }
+    const bool yz = ys != 0 || zs != 0;
+#pragma unroll
+    for (int i = 0; i < N; i++)
+        if (yz || (i == 0 && xl) || (i == N - 1 && xr)) ww[i] = (TV)s[i];
+}
+
+template <int PREC, int N, int GATHER>
+__device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ w,
+                                           typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
+                                           const typename Pol<PREC>::TJ *__restrict__ dinv,
+                                           typename Pol<PREC>::TV alpha, int64_t pid, typename Pol<PREC>::TS &rtr,
+                                           typename Pol<PREC>::TS &rho)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TJ = typename Pol<PREC>::TJ;
+    using TS = typename Pol<PREC>::TS;
+    constexpr int N2 = N * N;
+    const int e = (int)(pid / N2);
+    const int q = (int)(pid - (int64_t)e * N2);
+    const int a = q % N, b = q / N;
+    const size_t base = (size_t)pid * N;
+    const ElemPos P = elem_pos(m, e);
+    TV ww[N], rr[N], zz[N];
+    TJ dd[N];
+    ld_pencil<TV, N, LD_CG>(w + base, ww);
+    ld_pencil<TV, N>(r + base, rr);
+    ld_pencil<TJ, N, LD_NC>(dinv + base, dd);
+    if (GATHER) gather_pencil<PREC, N>(m, w, e, P, a, b, ww);
+    const int mjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz);
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+        rr[i] = fma(-alpha, ww[i], rr[i]);                   // add2s2(r, w, -alpha)
+        zz[i] = (TV)((TJ)rr[i] * dd[i]);                     // solveM
+        const TS c = (TS)1 / (TS)(mjk * axis_mult(i, N, P.ex, m.nelx));
+        const TS rs = (TS)rr[i];
+        rtr += (rs * c) * rs;                                // glsc3(r, c, r)
+        rho += (rs * c) * (TS)zz[i];                         // glsc3(r, c, z)
+    }
+    st_pencil<TV, N>(r + base, rr);
+    st_pencil<TV, N>(z + base, zz);
+}
+
+// CG prologue for one pencil: r = b, x = 0, p = 0, z = M^-1 r; rtr0 and rho_1 partials.
+template <int PREC, int N>
+__device__ __forceinline__ void init_pencil(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ bvec,
+                                            typename Pol<PREC>::TV *__restrict__ x, typename Pol<PREC>::TV *__restrict__ pv,
+                                            typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
+                                            const typename Pol<PREC>::TJ *__restrict__ dinv, int64_t pid,
+                                            typename Pol<PREC>::TS &rtr, typename Pol<PREC>::TS &rho)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TJ = typename Pol<PREC>::TJ;
+    using TS = typename Pol<PREC>::TS;
+    constexpr int N2 = N * N;
+    const int e = (int)(pid / N2);
+    const int q = (int)(pid - (int64_t)e * N2);
+    const int a = q % N, b = q / N;
+    const size_t base = (size_t)pid * N;
+    const ElemPos P = elem_pos(m, e);
+    TV rr[N], zz[N], zero[N];
+    TJ dd[N];
+    ld_pencil<TV, N>(bvec + base, rr);
+    ld_pencil<TJ, N, LD_NC>(dinv + base, dd);
+    const int mjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz);
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+        zero[i] = TV(0);
+        zz[i] = (TV)((TJ)rr[i] * dd[i]);
+        const TS c = (TS)1 / (TS)(mjk * axis_mult(i, N, P.ex, m.nelx));
+        const TS rs = (TS)rr[i];
+        rtr += (rs * c) * rs;
+        rho += (rs * c) * (TS)zz[i];
+    }
+    st_pencil<TV, N>(r + base, rr);
+    st_pencil<TV, N>(z + base, zz);
+    st_pencil<TV, N>(x + base, zero);
+    st_pencil<TV, N>(pv + base, zero);
+}
+
+// contiguous even split of [0, n) over `parts`
+__device__ __forceinline__ int64_t split(int64_t n, int parts, int i) { return n * i / parts; }
+
+// ===========================================================================
+// persistent cooperative megakernel: the whole solve in one launch
+// ===========================================================================
+struct MegaArgs {
+    MeshDev m;
+    const void *b;
+    void *x, *p, *r, *z, *w;
+    const void *g, *dinv;
+    const int32_t *gs_off, *gs_idx;
+    int32_t nseg;
+    int32_t order;          // NB_GS_CONSISTENT / NB_GS_PER_COPY
+    int32_t max_iter;
+    double rtol;
+    double *hist;           // [max_iter + 1]
+    unsigned long long *tim;  // nullable: [3 * (max_iter + 1)] globaltimer stamps (block 0)
+    double *partA, *partS, *partB;   // per-block partials, [G], [G], [2G]
+    unsigned int *bar;      // [2] grid barrier: arrival count, generation
+    Scal *scal;             // result scalars (written by block 0)
+};
+
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int *p)
+{
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned int *p, unsigned int v)
+{
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Grid-wide barrier of a cooperative launch (all blocks co-resident): arrival counter +
+// generation word with release/acquire ordering.  The gpu-scope fences make every block's
+// global writes before the barrier visible to every block after it.
+__device__ __forceinline__ void grid_barrier(unsigned int *bar)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int gen = ld_acquire_u32(bar + 1);
+        __threadfence();
+        const unsigned int prev = atomicAdd(bar, 1u);
+        if (prev == gridDim.x - 1) {
+            bar[0] = 0;
+            __threadfence();
+            st_release_u32(bar + 1, gen + 1);
+        } else {
+            while (ld_acquire_u32(bar + 1) == gen) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// every block: sum part[i*K + k] over all G blocks in a fixed order (same result everywhere)
+template <typename TS>
+__device__ __forceinline__ TS all_blocks_sum(const double *part, int G, int K, int k, TS *sh)
+{
+    __shared__ TS bc;
+    TS s = 0;
+    for (int i = threadIdx.x; i < G; i += blockDim.x) s += (TS)__ldcg(part + (size_t)i * K + k);
+    s = block_sum<TS>(s, sh);
+    if (threadIdx.x == 0) bc = s;
+    __syncthreads();
+    const TS r = bc;
+    __syncthreads();
+    return r;
+}
+
+template <int PREC, int N, int FUSED>
+__global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT)
+k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TJ = typename Pol<PREC>::TJ;
+    using TS = typename Pol<PREC>::TS;
+    using C = AxCfg<TV, N>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    __shared__ TS sh[32];
+    const MeshDev &m = A.m;
+    const int G = gridDim.x, bk = blockIdx.x, tid = threadIdx.x;
+    TV *x = (TV *)A.x, *pv = (TV *)A.p, *r = (TV *)A.r, *z = (TV *)A.z, *w = (TV *)A.w;
+    const TV *g = (const TV *)A.g;
+    const TJ *dinv = (const TJ *)A.dinv;
+    const bool t0 = (bk == 0 && tid == 0);
+
+    // element range of this block, as whole groups of EPB elements
+    const int64_t ngroups = ((int64_t)m.E + C::EPB - 1) / C::EPB;
+    const int64_t g0 = split(ngroups, G, bk), g1 = split(ngroups, G, bk + 1);
+    const int el = tid / C::N2;
+    const int q = tid - el * C::N2;
+    const int a = q % N, b = q / N;
+    TV *S0 = reinterpret_cast<TV *>(smraw) + (el < C::EPB ? el : 0) * 3 * C::ESZ;
+    const int64_t p0 = min((int64_t)m.E, g0 * C::EPB) * C::N2, p1 = min((int64_t)m.E, g1 * C::EPB) * C::N2;
+
+    // ---- prologue: r = b, x = p = 0, z = M^-1 r; rtr0, rho_1
+    {
+        TS rtr = 0, rho = 0;
+        for (int64_t pid = p0 + tid; pid < p1; pid += blockDim.x)
+            init_pencil<PREC, N>(m, (const TV *)A.b, x, pv, r, z, dinv, pid, rtr, rho);
+        rtr = block_sum<TS>(rtr, sh);
+        rho = block_sum<TS>(rho, sh);
+        if (tid == 0) { A.partB[2 * bk] = (double)rtr; A.partB[2 * bk + 1] = (double)rho; }
+    }
+    grid_barrier(A.bar);
+    if (t0 && A.tim) A.tim[0] = globaltimer();
+    const TS rtr0 = all_blocks_sum<TS>(A.partB, G, 2, 0, sh);
+    TS rho = all_blocks_sum<TS>(A.partB, G, 2, 1, sh);
+    TS rtr = rtr0, beta = 0, alpha = 0, pap = 0;
+    int it = 0, status = NB_MAXITER;
+    bool pending = false, done = false;
+    if (t0) A.hist[0] = rtr0 == (TS)0 ? 0.0 : 1.0;
+    if (rtr0 == (TS)0) { status = NB_CONVERGED; done = true; }
+    else if (!isfinite((double)rtr0)) { status = NB_BROKEDOWN; done = true; }
+    else if (A.max_iter <= 0) { status = NB_MAXITER; done = true; }
+
+    while (!done) {
+        // ---- phase A: p update, deferred x update, w = mask A_L p, pap partial
+        TS acc = 0;
+        {
+            const TV bv = (TV)beta, av = pending ? (TV)alpha : TV(0);
+            for (int64_t gr = g0; gr < g1; gr++) {
+                const int e = (int)(gr * C::EPB) + el;
+                const bool active = el < C::EPB && e < m.E;
+                acc += ax_group<PREC, N, FUSED ? 1 : 2>(m, D, z, pv, x, g, w, true, bv, av, e, active, a, b, S0);
+            }
+        }
+        acc = block_sum<TS>(acc, sh);
+        if (tid == 0) A.partA[bk] = (double)acc;
+        grid_barrier(A.bar);
+        if (t0 && A.tim) A.tim[3 * it + 1] = globaltimer();
+        pap = all_blocks_sum<TS>(A.partA, G, 1, 0, sh);
+        if (!FUSED) {
+            // ---- CSR gather-scatter phase: per-copy (or consistent) QQ^T, shared pap partial
+            const int64_t s0 = split(A.nseg, G, bk), s1 = split(A.nseg, G, bk + 1);
+            TS acc2 = 0;
+            for (int64_t s = s0 + tid; s < s1; s += blockDim.x) {
+                if (A.order == NB_GS_CONSISTENT)
+                    acc2 += gs_segment<PREC, NB_GS_CONSISTENT, 1, TV, typename Pol<PREC>::TG, LD_CG>(
+                        (int32_t)s, A.gs_off, A.gs_idx, w, pv);
+                else
+                    acc2 += gs_segment<PREC, NB_GS_PER_COPY, 1, TV, typename Pol<PREC>::TG, LD_CG>(
+                        (int32_t)s, A.gs_off, A.gs_idx, w, pv);
+            }
+            acc2 = block_sum<TS>(acc2, sh);
+            if (tid == 0) A.partS[bk] = (double)acc2;
+            grid_barrier(A.bar);
+            pap = pap + all_blocks_sum<TS>(A.partS, G, 1, 0, sh);
+        }
+        if (t0 && A.tim) A.tim[3 * it + 2] = globaltimer();
+        if (!(pap > (TS)0) || !isfinite((double)pap) || !isfinite((double)rho)) {
+            status = NB_BROKEDOWN;
+            pending = false;     // x already holds x_k (alpha_prev p_old applied in phase A)
+            break;
+        }
+        alpha = rho / pap;
+        pending = true;
+        // ---- phase B: (gather) r -= alpha w, z = M^-1 r, rtr and rho partials
+        {
+            TS prtr = 0, prho = 0;
+            const TV av = (TV)alpha;
+            for (int64_t pid = p0 + tid; pid < p1; pid += blockDim.x)
+                upd_pencil<PREC, N, FUSED>(m, w, r, z, dinv, av, pid, prtr, prho);
+            prtr = block_sum<TS>(prtr, sh);
+            prho = block_sum<TS>(prho, sh);
+            if (tid == 0) { A.partB[2 * bk] = (double)prtr; A.partB[2 * bk + 1] = (double)prho; }
+        }
+        grid_barrier(A.bar);
+        rtr = all_blocks_sum<TS>(A.partB, G, 2, 0, sh);
+        const TS rho_new = all_blocks_sum<TS>(A.partB, G, 2, 1, sh);
+        it++;
+        const double res = sqrt((double)rtr / (double)rtr0);
+        if (t0) {
+            A.hist[it] = res;
+            if (A.tim) A.tim[3 * it] = globaltimer();
+        }
+        if (!isfinite((double)rtr) || !isfinite((double)rho_new)) { status = NB_BROKEDOWN; done = true; }
+        else if (res <= A.rtol || rtr == (TS)0) { status = NB_CONVERGED; done = true; }
+        else if (it >= A.max_iter) { status = NB_MAXITER; done = true; }
+        beta = rho_new / rho;
+        rho = rho_new;
+    }
+    // ---- epilogue: the deferred x += alpha p of the last iteration (own elements)
+    if (pending) {
+        const TV av = (TV)alpha;
+        const int64_t l0 = p0 * N, l1 = p1 * N;
+        for (int64_t l = l0 + tid; l < l1; l += blockDim.x) x[l] = fma(av, pv[l], x[l]);
+    }
+    if (t0) {
+        Scal *s = A.scal;
+        s->rho = (double)rho; s->beta = (double)beta; s->alpha = (double)alpha; s->pap = (double)pap;
+        s->rtr = (double)rtr; s->rtr0 = (double)rtr0; s->iter = it; s->status = status; s->done = 1;
+        s->pending = 0;
+    }
+}
+
+// ===========================================================================
+// graph driver: one persistent kernel per phase, last-block finalize
+// ===========================================================================
+template <int PREC, int N, int MODE>
+__global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT)
+k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
+     const typename Pol<PREC>::TV *__restrict__ in, typename Pol<PREC>::TV *__restrict__ pv,
+     typename Pol<PREC>::TV *__restrict__ xv, const typename Pol<PREC>::TV *__restrict__ g,
+     typename Pol<PREC>::TV *__restrict__ w, int apply_mask, Scal *__restrict__ scal, const RedWs rw)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TS = typename Pol<PREC>::TS;
+    using C = AxCfg<TV, N>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    if (MODE != 0 && scal->done) return;   // grid-uniform
+    const int tid = threadIdx.x;
+    const int el = tid / C::N2;
+    const int q = tid - el * C::N2;
+    const int a = q % N, b = q / N;
+    TV *S0 = reinterpret_cast<TV *>(smraw) + (el < C::EPB ? el : 0) * 3 * C::ESZ;
+    TV beta = 0, alpha = 0;
+    if (MODE != 0) {
+        beta = (TV)(TS)scal->beta;
+        alpha = scal->pending ? (TV)(TS)scal->alpha : TV(0);
+    }
+    const int64_t ngroups = ((int64_t)m.E + C::EPB - 1) / C::EPB;
+    const int64_t g0 = split(ngroups, gridDim.x, blockIdx.x), g1 = split(ngroups, gridDim.x, blockIdx.x + 1);
+    TS acc = 0;
+    for (int64_t gr = g0; gr < g1; gr++) {
+        const int e = (int)(gr * C::EPB) + el;
+        const bool active = el < C::EPB && e < m.E;
+        acc += ax_group<PREC, N, MODE>(m, D, in, pv, xv, g, w, apply_mask != 0, beta, alpha, e, active, a, b, S0);
+    }
+    if (MODE == 0) return;
+    __shared__ TS red[32];
+    TS v[1] = {block_sum<TS>(acc, red)};
+    TS tot[1];
+    if (grid_reduce<TS, 1>(v, rw, tot) && tid == 0) {
+        if (MODE == 2) {
+            scal->pap = (double)tot[0];
+        } else {
+            const TS pap = tot[0];
+            const TS rho = (TS)scal->rho;
+            scal->pap = (double)pap;
+            if (!(pap > (TS)0) || !isfinite((double)pap) || !isfinite((double)rho)) {
+                scal->status = NB_BROKEDOWN;
+                scal->done = 1;
+                scal->pending = 0;
+            } else {
+                scal->alpha = (double)(rho / pap);
+                scal->pending = 1;
+            }
+        }
+    }
+}
+
+constexpr int UPD_NT = 256;
+
+template <int PREC, int N, int GATHER>
+__global__ void __launch_bounds__(UPD_NT)
+k_upd(const MeshDev m, const typename Pol<PREC>::TV *__restrict__ w, typename Pol<PREC>::TV *__restrict__ r,
+      typename Pol<PREC>::TV *__restrict__ z, const typename Pol<PREC>::TJ *__restrict__ dinv,
+      Scal *__restrict__ scal, const RedWs rw, double *__restrict__ hist, cudaGraphConditionalHandle cond,
+      int use_cond)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TS = typename Pol<PREC>::TS;
+    if (scal->done) {
+        if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    const TV alpha = (TV)(TS)scal->alpha;
+    TS rtr = 0, rho = 0;
+    const int64_t np = (int64_t)m.E * N * N;
+    const int64_t p0 = split(np, gridDim.x, blockIdx.x), p1 = split(np, gridDim.x, blockIdx.x + 1);
+    for (int64_t pid = p0 + threadIdx.x; pid < p1; pid += UPD_NT)
+        upd_pencil<PREC, N, GATHER>(m, w, r, z, dinv, alpha, pid, rtr, rho);
+    __shared__ TS red[32];
+    TS v[2];
+    v[0] = block_sum<TS>(rtr, red);
+    v[1] = block_sum<TS>(rho, red);
+    TS tot[2];
+    if (grid_reduce<TS, 2>(v, rw, tot) && threadIdx.x == 0) {
+        const TS trtr = tot[0], trho = tot[1];
+        const int it = scal->iter + 1;
+        const double res = sqrt((double)trtr / scal->rtr0);
+        hist[it] = res;
+        int done = 0;
+        if (!isfinite((double)trtr) || !isfinite((double)trho)) {
+            scal->status = NB_BROKEDOWN;
+            done = 1;
+        } else if (res <= scal->rtol || trtr == (TS)0) {
+            scal->status = NB_CONVERGED;
+            done = 1;
+        } else if (it >= scal->max_iter) {
+            scal->status = NB_MAXITER;
+            done = 1;
+        }
+        const TS rho_old = (TS)scal->rho;
+        scal->beta = (double)(trho / rho_old);
+        scal->rho = (double)trho;
+        scal->rtr = (double)trtr;
+        scal->iter = it;
+        scal->done = done;
+        if (done && use_cond) cudaGraphSetConditional(cond, 0);
+    }
+}
+
+template <int PREC, int N>
+__global__ void __launch_bounds__(UPD_NT)
+k_init(const MeshDev m, const typename Pol<PREC>::TV *__restrict__ bvec, typename Pol<PREC>::TV *__restrict__ x,
+       typename Pol<PREC>::TV *__restrict__ pv, typename Pol<PREC>::TV *__restrict__ r,
+       typename Pol<PREC>::TV *__restrict__ z, const typename Pol<PREC>::TJ *__restrict__ dinv,
+       Scal *__restrict__ scal, const RedWs rw, double *__restrict__ hist)
+{
+    using TS = typename Pol<PREC>::TS;
+    TS rtr = 0, rho = 0;
+    const int64_t np = (int64_t)m.E * N * N;
+    const int64_t p0 = split(np, gridDim.x, blockIdx.x), p1 = split(np, gridDim.x, blockIdx.x + 1);
+    for (int64_t pid = p0 + threadIdx.x; pid < p1; pid += UPD_NT)
+        init_pencil<PREC, N>(m, bvec, x, pv, r, z, dinv, pid, rtr, rho);
+    __shared__ TS red[32];
+    TS v[2];
+    v[0] = block_sum<TS>(rtr, red);
+    v[1] = block_sum<TS>(rho, red);
+    TS tot[2];
+    if (grid_reduce<TS, 2>(v, rw, tot) && threadIdx.x == 0) {
+        const TS trtr = tot[0], trho = tot[1];
+        scal->rtr0 = (double)trtr;
+        scal->rtr = (double)trtr;
+        scal->rho = (double)trho;
+        scal->beta = 0.0;
+        scal->alpha = 0.0;
+        scal->pending = 0;
+        scal->iter = 0;
+        hist[0] = 1.0;
+        if (trtr == (TS)0) {
+            scal->status = NB_CONVERGED;
+            scal->done = 1;
+            hist[0] = 0.0;
+        } else if (!isfinite((double)trtr)) {
+            scal->status = NB_BROKEDOWN;
+            scal->done = 1;
+        } else if (scal->max_iter <= 0) {
+            scal->status = NB_MAXITER;
+            scal->done = 1;
+        }
+    }
+}
+
+// the deferred x += alpha p of the last iteration
+template <int PREC>
+__global__ void __launch_bounds__(256)
+k_fin(int64_t n, typename Pol<PREC>::TV *__restrict__ x, const typename Pol<PREC>::TV *__restrict__ pv,
+      Scal *__restrict__ scal)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TS = typename Pol<PREC>::TS;
+    if (!scal->pending) return;
+    const TV alpha = (TV)(TS)scal->alpha;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = fma(alpha, pv[i], x[i]);
+}
+
+// ===========================================================================
+// launchers
+// ===========================================================================
+template <typename K>
+static int occupancy(K kern, int nt, int smem)
+{
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, nt, smem);
+    return o > 0 ? o : 1;
+}
+
+template <int PREC, int N, int MODE>
+static int ax_grid_t(const nb_handle *h)
+{
+    using TV = typename Pol<PREC>::TV;
+    using C = AxCfg<TV, N>;
+    static int occ = -1;
+    if (occ < 0) {
+        cudaFuncSetAttribute(k_ax<PREC, N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        occ = occupancy(k_ax<PREC, N, MODE>, C::NT, C::SMEM);
+    }
+    const int64_t ngroups = (h->E + C::EPB - 1) / C::EPB;
+    int64_t grid = (int64_t)h->sm_count * occ;
+    if (grid > ngroups) grid = ngroups;
+    return (int)(grid < 1 ? 1 : grid);
+}
+
+template <int PREC, int N, int MODE>
+static cudaError_t ax_launch_t(const nb_handle *h, const void *in, void *pv, void *xv, void *w, int apply_mask,
+                               Scal *scal, const RedWs &rw, cudaStream_t st)
+{
+    using TV = typename Pol<PREC>::TV;
+    using C = AxCfg<TV, N>;
+    const int grid = ax_grid_t<PREC, N, MODE>(h);
+    const TV *g = (const TV *)(sizeof(TV) == 8 ? (const void *)h->g64 : (const void *)h->g32);
+    k_ax<PREC, N, MODE><<<grid, C::NT, C::SMEM, st>>>(h->md(), make_dmat<TV, N>(h->D), (const TV *)in, (TV *)pv,
+                                                      (TV *)xv, g, (TV *)w, apply_mask, scal, rw);
+    return cudaGetLastError();
+}
+
+template <int PREC>
+cudaError_t launch_ax_local(const nb_handle *h, const void *u, void *w, bool mask, cudaStream_t st)
+{
+    RedWs none = {nullptr, nullptr, nullptr};
+    NB_DISPATCH_N(h->n, return (ax_launch_t<PREC, NN, 0>(h, u, nullptr, nullptr, w, mask ? 1 : 0, nullptr, none, st)))
+}
+
+template <int PREC>
+int grid_k1(const nb_handle *h)
+{
+    NB_DISPATCH_N(h->n, return (ax_grid_t<PREC, NN, 1>(h) > ax_grid_t<PREC, NN, 2>(h) ? ax_grid_t<PREC, NN, 1>(h)
+                                                                                         : ax_grid_t<PREC, NN, 2>(h)))
+}
+template <int PREC>
+int grid_k2(const nb_handle *h)
+{
+    const int64_t np = h->E * h->n * h->n;
+    return grid_for(np, UPD_NT, h->sm_count, 4);
+}
+
+template <int PREC>
+cudaError_t launch_cg_init(const nb_handle *h, Workspace &ws, const void *b, cudaStream_t st)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TJ = typename Pol<PREC>::TJ;
+    const TJ *dinv = (const TJ *)(PREC == NB_FP32 ? (const void *)h->dinv32 : (const void *)h->dinv64);
+    const int grid = grid_k2<PREC>(h);
+    NB_DISPATCH_N(h->n, (k_init<PREC, NN><<<grid, UPD_NT, 0, st>>>(h->md(), (const TV *)b, (TV *)ws.x, (TV *)ws.p,
+                                                                   (TV *)ws.r, (TV *)ws.z, dinv, ws.scal, ws.red,
+                                                                   ws.hist));
+                 break)
+    return cudaGetLastError();
+}
+
+template <int PREC>
+cudaError_t launch_cg_k1(const nb_handle *h, Workspace &ws, bool with_pap, cudaStream_t st)
+{
+    if (with_pap) {
+        NB_DISPATCH_N(h->n, return (ax_launch_t<PREC, NN, 1>(h, ws.z, ws.p, ws.x, ws.w, 1, ws.scal, ws.red, st)))
+    }
+    NB_DISPATCH_N(h->n, return (ax_launch_t<PREC, NN, 2>(h, ws.z, ws.p, ws.x, ws.w, 1, ws.scal, ws.red, st)))
+}
+
+template <int PREC>
+cudaError_t launch_cg_k2(const nb_handle *h, Workspace &ws, bool gather, cudaStream_t st,
+                         cudaGraphConditionalHandle cond, bool use_cond)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TJ = typename Pol<PREC>::TJ;
+    const TJ *dinv = (const TJ *)(PREC == NB_FP32 ? (const void *)h->dinv32 : (const void *)h->dinv64);
+    const int grid = grid_k2<PREC>(h);
+    const int uc = use_cond ? 1 : 0;
+    if (gather) {
+        NB_DISPATCH_N(h->n, (k_upd<PREC, NN, 1><<<grid, UPD_NT, 0, st>>>(h->md(), (const TV *)ws.w, (TV *)ws.r,
+                                                                         (TV *)ws.z, dinv, ws.scal, ws.red, ws.hist,
+                                                                         cond, uc));
+                     break)
+    } else {
+        NB_DISPATCH_N(h->n, (k_upd<PREC, NN, 0><<<grid, UPD_NT, 0, st>>>(h->md(), (const TV *)ws.w, (TV *)ws.r,
+                                                                         (TV *)ws.z, dinv, ws.scal, ws.red, ws.hist,
+                                                                         cond, uc));
+                     break)
+    }
+    return cudaGetLastError();
+}
+
+template <int PREC>
+cudaError_t launch_cg_fin(const nb_handle *h, Workspace &ws, cudaStream_t st)
+{
+    using TV = typename Pol<PREC>::TV;
+    const int grid = grid_for(h->NL, 256, h->sm_count, 8);
+    k_fin<PREC><<<grid, 256, 0, st>>>(h->NL, (TV *)ws.x, (const TV *)ws.p, ws.scal);
+    return cudaGetLastError();
+}
+
+// ---- megakernel ----
+template <int PREC, int N, int FUSED>
+static int mega_grid_t(const nb_handle *h)
+{
+    using TV = typename Pol<PREC>::TV;
+    using C = AxCfg<TV, N>;
+    static int occ = -1;
+    if (occ < 0) {
+        cudaFuncSetAttribute(k_cg_mega<PREC, N, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        occ = occupancy(k_cg_mega<PREC, N, FUSED>, C::NT, C::SMEM);
+    }
+    return h->sm_count * occ;
+}
+
+template <int PREC>
+int grid_mega(const nb_handle *h)
+{
+    NB_DISPATCH_N(h->n, return (mega_grid_t<PREC, NN, 1>(h) > mega_grid_t<PREC, NN, 0>(h) ? mega_grid_t<PREC, NN, 1>(h)
+                                                                                            : mega_grid_t<PREC, NN, 0>(h)))
+}
+
+template <int PREC, int N, int FUSED>
+static cudaError_t mega_launch_t(const nb_handle *h, const MegaArgs &args, cudaStream_t st)
+{
+    using TV = typename Pol<PREC>::TV;
+    using C = AxCfg<TV, N>;
+    const int grid = mega_grid_t<PREC, N, FUSED>(h);
+    DMat<TV, N> D = make_dmat<TV, N>(h->D);
+    void *params[2] = {(void *)&args, (void *)&D};
+    return cudaLaunchCooperativeKernel((const void *)k_cg_mega<PREC, N, FUSED>, dim3(grid), dim3(C::NT), params,
+                                       (size_t)C::SMEM, st);
+}
+
+template <int PREC>
+cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int order, int max_iter, double rtol,
+                           unsigned long long *tim, cudaStream_t st)
+{
+    MegaArgs A;
+    A.m = h->md();
+    A.b = b;
+    A.x = ws.x; A.p = ws.p; A.r = ws.r; A.z = ws.z; A.w = ws.w;
+    A.g = (sizeof(typename Pol<PREC>::TV) == 8) ? (const void *)h->g64 : (const void *)h->g32;
+    A.dinv = PREC == NB_FP32 ? (const void *)h->dinv32 : (const void *)h->dinv64;
+    A.gs_off = h->gs_off; A.gs_idx = h->gs_idx; A.nseg = (int32_t)h->nseg;
+    A.order = order; A.max_iter = max_iter; A.rtol = rtol;
+    A.hist = ws.hist; A.tim = tim;
+    A.partA = ws.red.part; A.partS = ws.red.part + ws.mega_G; A.partB = ws.red.part + 2 * ws.mega_G;
+    A.bar = ws.bar;
+    A.scal = ws.scal;
+    const bool fused = order == NB_GS_CONSISTENT && !h->cg_csr;
+    if (fused) { NB_DISPATCH_N(h->n, return (mega_launch_t<PREC, NN, 1>(h, A, st))) }
+    NB_DISPATCH_N(h->n, return (mega_launch_t<PREC, NN, 0>(h, A, st)))
+}
+
+#define NB_INSTANTIATE_CG(P)                                                                                  \
+    template cudaError_t launch_ax_local<P>(const nb_handle *, const void *, void *, bool, cudaStream_t);      \
+    template int grid_k1<P>(const nb_handle *);                                                               \
+    template int grid_k2<P>(const nb_handle *);                                                               \
+    template int grid_mega<P>(const nb_handle *);                                                             \
+    template cudaError_t launch_cg_init<P>(const nb_handle *, Workspace &, const void *, cudaStream_t);        \
+    template cudaError_t launch_cg_k1<P>(const nb_handle *, Workspace &, bool, cudaStream_t);                 \
+    template cudaError_t launch_cg_k2<P>(const nb_handle *, Workspace &, bool, cudaStream_t,                  \
+                                         cudaGraphConditionalHandle, bool);                                   \
+    template cudaError_t launch_cg_fin<P>(const nb_handle *, Workspace &, cudaStream_t);                      \
+    template cudaError_t launch_cg_mega<P>(const nb_handle *, Workspace &, const void *, int, int, double,    \
+                                           unsigned long long *, cudaStream_t);
+
+}  // namespace nb

@@ -18,42 +18,36 @@ template <> struct Pol<NB_FP32> { using TV = float;  using TG = float;  using TS
 template <> struct Pol<NB_MIXED> { using TV = float; using TG = double; using TS = double; using TJ = double; };
 
 // ---------------------------------------------------------------------------
-// GLL derivative matrix in constant memory, one n*n block per order (n = 2..16).
-// Indices are compile-time constants after unrolling, so every D entry is a
-// constant-bank operand of the FMA (no register or shared-memory traffic).
+// GLL derivative matrix passed by value in kernel-parameter space
+// (__grid_constant__): after unrolling every D entry is a compile-time offset
+// into the constant bank, i.e. an immediate operand of the FMA -- no register,
+// shared-memory or global traffic for D.
 // ---------------------------------------------------------------------------
-// (defined here: this header is included by exactly one translation unit, nb_kernels.cu)
-__constant__ double c_D64[17 * 256];
-__constant__ float c_D32[17 * 256];
-
-template <typename T> __device__ __forceinline__ T cD(int i);
-template <> __device__ __forceinline__ double cD<double>(int i) { return c_D64[i]; }
-template <> __device__ __forceinline__ float cD<float>(int i) { return c_D32[i]; }
-
-// D[row][col] for order N (D[i][j] = l_j'(x_i))
-template <typename T, int N> __device__ __forceinline__ T Dm(int row, int col) { return cD<T>(N * 256 + row * N + col); }
+template <typename T, int N> struct DMat {
+    T d[N * N];   // d[i*N + j] = l_j'(x_i)
+};
 
 // o[i] = sum_l D[i][l] v[l]  (local_grad3 direction)
 template <typename T, int N>
-__device__ __forceinline__ void contract(const T (&v)[N], T (&o)[N])
+__device__ __forceinline__ void contract(const DMat<T, N> &D, const T (&v)[N], T (&o)[N])
 {
 #pragma unroll
     for (int i = 0; i < N; i++) {
-        T s = Dm<T, N>(i, 0) * v[0];
+        T s = D.d[i * N] * v[0];
 #pragma unroll
-        for (int l = 1; l < N; l++) s = fma(Dm<T, N>(i, l), v[l], s);
+        for (int l = 1; l < N; l++) s = fma(D.d[i * N + l], v[l], s);
         o[i] = s;
     }
 }
 // o[i] = sum_l D[l][i] v[l]  (local_grad3_t direction)
 template <typename T, int N>
-__device__ __forceinline__ void contract_t(const T (&v)[N], T (&o)[N])
+__device__ __forceinline__ void contract_t(const DMat<T, N> &D, const T (&v)[N], T (&o)[N])
 {
 #pragma unroll
     for (int i = 0; i < N; i++) {
-        T s = Dm<T, N>(0, i) * v[0];
+        T s = D.d[i] * v[0];
 #pragma unroll
-        for (int l = 1; l < N; l++) s = fma(Dm<T, N>(l, i), v[l], s);
+        for (int l = 1; l < N; l++) s = fma(D.d[l * N + i], v[l], s);
         o[i] = s;
     }
 }
@@ -62,8 +56,7 @@ __device__ __forceinline__ void contract_t(const T (&v)[N], T (&o)[N])
 // pencil (N contiguous values) loads/stores with the widest aligned vector type
 // ---------------------------------------------------------------------------
 template <typename T, int N> struct VecW {
-    static constexpr int bytes = (int)sizeof(T);
-    static constexpr int V = (bytes == 4) ? ((N % 4 == 0) ? 4 : (N % 2 == 0 ? 2 : 1)) : ((N % 2 == 0) ? 2 : 1);
+    static constexpr int V = (sizeof(T) == 4) ? ((N % 4 == 0) ? 4 : (N % 2 == 0 ? 2 : 1)) : ((N % 2 == 0) ? 2 : 1);
 };
 template <typename T, int V> struct VT { using type = T; };
 template <> struct VT<float, 4> { using type = float4; };
@@ -88,7 +81,23 @@ template <> struct VAcc<double, 2> {
     static __device__ __forceinline__ double2 put(const double *d) { return make_double2(d[0], d[1]); }
 };
 
-template <typename T, int N>
+// cache hints: DEF = default, CS = streaming (evict-first), NC = read-only path,
+// CG = L2 only (data written by other blocks of the same kernel)
+enum { LD_DEF = 0, LD_CS = 1, LD_NC = 2, LD_CG = 3 };
+template <int H, typename W> __device__ __forceinline__ W ldv(const W *p)
+{
+    if (H == LD_CS) return __ldcs(p);
+    if (H == LD_NC) return __ldg(p);
+    if (H == LD_CG) return __ldcg(p);
+    return *p;
+}
+template <int H, typename W> __device__ __forceinline__ void stv(W *p, const W &v)
+{
+    if (H == LD_CS) __stcs(p, v);
+    else *p = v;
+}
+
+template <typename T, int N, int H = LD_DEF>
 __device__ __forceinline__ void ld_pencil(const T *__restrict__ src, T (&v)[N])
 {
     constexpr int V = VecW<T, N>::V;
@@ -96,45 +105,34 @@ __device__ __forceinline__ void ld_pencil(const T *__restrict__ src, T (&v)[N])
     const W *s = reinterpret_cast<const W *>(src);
 #pragma unroll
     for (int c = 0; c < N / V; c++) {
-        W t = s[c];
+        W t = ldv<H>(s + c);
         VAcc<T, V>::get(t, &v[c * V]);
     }
 }
-template <typename T, int N>
-__device__ __forceinline__ void ld_pencil_stream(const T *__restrict__ src, T (&v)[N])
-{
-    constexpr int V = VecW<T, N>::V;
-    using W = typename VT<T, V>::type;
-    const W *s = reinterpret_cast<const W *>(src);
-#pragma unroll
-    for (int c = 0; c < N / V; c++) {
-        W t = __ldcs(s + c);
-        VAcc<T, V>::get(t, &v[c * V]);
-    }
-}
-template <typename T, int N>
+template <typename T, int N, int H = LD_DEF>
 __device__ __forceinline__ void st_pencil(T *__restrict__ dst, const T (&v)[N])
 {
     constexpr int V = VecW<T, N>::V;
     using W = typename VT<T, V>::type;
     W *d = reinterpret_cast<W *>(dst);
 #pragma unroll
-    for (int c = 0; c < N / V; c++) d[c] = VAcc<T, V>::put(&v[c * V]);
+    for (int c = 0; c < N / V; c++) stv<H>(d + c, VAcc<T, V>::put(&v[c * V]));
 }
 
 // ---------------------------------------------------------------------------
 // lattice helpers: multiplicity and mask are analytic on the box
+// (int32 is enough: n_local < 2^31 is enforced at setup)
 // ---------------------------------------------------------------------------
 struct ElemPos {
     int32_t ex, ey, ez;
 };
-__device__ __forceinline__ ElemPos elem_pos(const MeshDev &m, int64_t e)
+__device__ __forceinline__ ElemPos elem_pos(const MeshDev &m, int32_t e)
 {
     ElemPos r;
-    int64_t t = e / m.nelx;
-    r.ex = (int32_t)(e - t * m.nelx);
-    r.ey = (int32_t)(t % m.nely);
-    r.ez = (int32_t)(t / m.nely);
+    const int32_t t = e / m.nelx;
+    r.ex = e - t * m.nelx;
+    r.ez = t / m.nely;
+    r.ey = t - r.ez * m.nely;
     return r;
 }
 // multiplicity factor along one axis for local index i of element coordinate ex (nel elements)
@@ -148,8 +146,7 @@ __device__ __forceinline__ bool axis_bnd(int i, int n, int ex, int nel)
 }
 
 // ---------------------------------------------------------------------------
-// deterministic reductions: warp shuffle tree -> shared -> one value per block
-// (blockDim.x must be a multiple of 32)
+// deterministic reductions
 // ---------------------------------------------------------------------------
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v)
@@ -158,10 +155,11 @@ __device__ __forceinline__ T warp_sum(T v)
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     return v;
 }
+// block sum (fixed tree); result valid in thread 0.  Any blockDim (padded warps contribute 0).
 template <typename T>
 __device__ __forceinline__ T block_sum(T v, T *sh)
 {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
     v = warp_sum(v);
     __syncthreads();
     if (lane == 0) sh[wid] = v;
@@ -171,30 +169,62 @@ __device__ __forceinline__ T block_sum(T v, T *sh)
         r = (lane < nw) ? sh[lane] : T(0);
         r = warp_sum(r);
     }
-    return r;  // valid in thread 0
-}
-// sum of n values (fixed order: thread-strided sequential, then tree), all threads of the block
-template <typename T>
-__device__ __forceinline__ T block_sum_array(const double *src, int n, int stride, T *sh)
-{
-    T v = 0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) v += (T)__ldcg(src + (int64_t)i * stride);
-    return block_sum<T>(v, sh);
+    return r;
 }
 
-// last-block-done election: returns true in every thread of the last block to finish
-__device__ __forceinline__ bool last_block(uint32_t *cnt)
+// Two-level deterministic grid reduction of K values (H4 of SURVEY.md §7): block partials
+// -> per-chunk (256 blocks) partial, reduced by the chunk's last block to finish -> total,
+// reduced by the last chunk reducer.  Every sum runs in a fixed index order, so results are
+// bit-reproducible; no floating-point atomics.  Counters self-reset.  Call from every
+// thread of every block; v valid in thread 0.  Returns true in all threads of the single
+// block that holds the total (valid in thread 0).
+constexpr int RED_CHUNK = 256;
+template <typename TS, int K>
+__device__ __forceinline__ bool grid_reduce(const TS (&v)[K], const RedWs &rw, TS (&tot)[K])
 {
-    __shared__ bool am_last;
-    __threadfence();
-    __syncthreads();
+    __shared__ TS sh[32];
+    __shared__ int flag;
+    const int nblk = gridDim.x;
+    const int b = blockIdx.x;
+    const int chunk = b / RED_CHUNK;
+    const int nchunk = (nblk + RED_CHUNK - 1) / RED_CHUNK;
+    const int csz = min(RED_CHUNK, nblk - chunk * RED_CHUNK);
     if (threadIdx.x == 0) {
-        uint32_t prev = atomicAdd(cnt, 1u);
-        am_last = (prev == gridDim.x - 1);
+#pragma unroll
+        for (int k = 0; k < K; k++) rw.part[(size_t)b * K + k] = (double)v[k];
+        __threadfence();
+        const uint32_t prev = atomicAdd(&rw.cnt[1 + chunk], 1u);
+        flag = (prev == (uint32_t)(csz - 1));
     }
     __syncthreads();
-    if (am_last) __threadfence();
-    return am_last;
+    if (!flag) return false;
+    __threadfence();
+    TS c[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        TS s = 0;
+        for (int i = threadIdx.x; i < csz; i += blockDim.x) s += (TS)__ldcg(rw.part + (size_t)(chunk * RED_CHUNK + i) * K + k);
+        c[k] = block_sum<TS>(s, sh);
+    }
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; k++) rw.part2[(size_t)chunk * K + k] = (double)c[k];
+        rw.cnt[1 + chunk] = 0;
+        __threadfence();
+        const uint32_t prev = atomicAdd(&rw.cnt[0], 1u);
+        flag = (prev == (uint32_t)(nchunk - 1));
+    }
+    __syncthreads();
+    if (!flag) return false;
+    __threadfence();
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        TS s = 0;
+        for (int i = threadIdx.x; i < nchunk; i += blockDim.x) s += (TS)__ldcg(rw.part2 + (size_t)i * K + k);
+        tot[k] = block_sum<TS>(s, sh);
+    }
+    if (threadIdx.x == 0) rw.cnt[0] = 0;
+    return true;
 }
 
 // ---------------------------------------------------------------------------
@@ -210,6 +240,44 @@ __device__ __forceinline__ uint64_t splitmix(uint64_t seed, uint64_t stream, uin
 __device__ __forceinline__ double unif(uint64_t seed, uint64_t stream, uint64_t i)
 {
     return (double)(splitmix(seed, stream, i) >> 11) * 0x1.0p-52 - 1.0;
+}
+
+// order dispatch (n = p+1 in [2,16])
+#define NB_DISPATCH_N(n, CALL)                 \
+    switch (n) {                               \
+    case 2: { constexpr int NN = 2; CALL; }    \
+    case 3: { constexpr int NN = 3; CALL; }    \
+    case 4: { constexpr int NN = 4; CALL; }    \
+    case 5: { constexpr int NN = 5; CALL; }    \
+    case 6: { constexpr int NN = 6; CALL; }    \
+    case 7: { constexpr int NN = 7; CALL; }    \
+    case 8: { constexpr int NN = 8; CALL; }    \
+    case 9: { constexpr int NN = 9; CALL; }    \
+    case 10: { constexpr int NN = 10; CALL; }  \
+    case 11: { constexpr int NN = 11; CALL; }  \
+    case 12: { constexpr int NN = 12; CALL; }  \
+    case 13: { constexpr int NN = 13; CALL; }  \
+    case 14: { constexpr int NN = 14; CALL; }  \
+    case 15: { constexpr int NN = 15; CALL; }  \
+    case 16: { constexpr int NN = 16; CALL; }  \
+    default: return cudaErrorInvalidValue;     \
+    }
+
+template <typename T, int N>
+inline DMat<T, N> make_dmat(const double *D)
+{
+    DMat<T, N> m;
+    for (int i = 0; i < N * N; i++) m.d[i] = (T)D[i];
+    return m;
+}
+
+inline int grid_for(int64_t work, int threads, int sm_count, int per_sm = 8)
+{
+    int64_t g = (work + threads - 1) / threads;
+    int64_t cap = (int64_t)sm_count * per_sm;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
 }
 
 }  // namespace nb

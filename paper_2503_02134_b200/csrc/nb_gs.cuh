@@ -1,0 +1,61 @@
+// nb_gs.cuh -- one gather-scatter segment (direct stiffness summation over the copies of one
+// shared global node), shared by the CSR kernel (nb_gs.cu) and the
+// per-copy phase of the CG megakernel (nb_cg.cuh).  gslib's gs_op / jl_gs_gather in the
+// paper, accumulated in the policy's gather-scatter precision
+// (the mixed strategy keeps the GS in double).
+//   NB_GS_CONSISTENT: s = sum of the copies in ascending local index, written to every copy.
+//   NB_GS_PER_COPY  : copy l receives w_l + sum_{m != l, ascending} w_m -- the arithmetic of
+//                     the paper's pairwise exchange, where each rank adds its neighbours'
+//                     contributions to its own (Table 3).
+// With PAP = 1 it returns the segment's part of pap = glsc3(w, c, p).
+#pragma once
+#include "nb_common.cuh"
+
+namespace nb {
+
+template <int PREC, int ORDER, int PAP, typename TVX, typename TGX, int H>
+__device__ __forceinline__ typename Pol<PREC>::TS gs_segment(int32_t s, const int32_t *__restrict__ off,
+                                                             const int32_t *__restrict__ idx, TVX *__restrict__ w,
+                                                             const TVX *__restrict__ pv)
+{
+    using TS = typename Pol<PREC>::TS;
+    TS acc = 0;
+    const int32_t a0 = __ldg(off + s);
+    const int32_t cnt = __ldg(off + s + 1) - a0;
+    int32_t id[8];
+    TVX v[8];
+#pragma unroll
+    for (int c = 0; c < 8; c++)
+        if (c < cnt) id[c] = __ldg(idx + a0 + c);
+#pragma unroll
+    for (int c = 0; c < 8; c++)
+        if (c < cnt) v[c] = ldv<H>(w + id[c]);
+    if (ORDER == NB_GS_CONSISTENT) {
+        TGX t = (TGX)v[0];
+#pragma unroll
+        for (int c = 1; c < 8; c++)
+            if (c < cnt) t += (TGX)v[c];
+        const TVX tv = (TVX)t;
+#pragma unroll
+        for (int c = 0; c < 8; c++)
+            if (c < cnt) w[id[c]] = tv;
+        if (PAP) acc += (TS)tv * (TS)ldv<H>(pv + id[0]);   // sum_copies c w p = sigma p (p continuous)
+    } else {
+        const TS cinv = (TS)1 / (TS)cnt;
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            if (c < cnt) {
+                TGX t = (TGX)v[c];
+#pragma unroll
+                for (int r = 0; r < 8; r++)
+                    if (r < cnt && r != c) t += (TGX)v[r];
+                const TVX tv = (TVX)t;
+                w[id[c]] = tv;
+                if (PAP) acc += ((TS)tv * cinv) * (TS)ldv<H>(pv + id[c]);
+            }
+        }
+    }
+    return acc;
+}
+
+}  // namespace nb

@@ -1,5 +1,5 @@
 // nb_internal.h -- private declarations shared by the host layer (nb_api.cu) and the
-// kernel translation unit (nb_kernels.cu).  No torch, no oracle.
+// kernel translation units.  No torch, no oracle.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -11,42 +11,51 @@ namespace nb {
 // Device-resident CG scalars.  Values of the policy's scalar
 // precision (float under NB_FP32, double otherwise) are stored widened to double.
 struct Scal {
-    double rho;        // rho_k = glsc3(r, c, z) of the current iteration
-    double beta;       // beta_k used by the p update of the current iteration
-    double alpha;      // alpha_k
-    double pap;        // pap_k
-    double rtr;        // rtr_k after the update
+    double rho;        // rho_k = glsc3(r, c, z) for the next p update
+    double beta;       // beta used by the next p update
+    double alpha;      // alpha of the last completed pap
+    double pap;
+    double rtr;        // rtr after the last update
     double rtr0;
     double rtol;
     int32_t iter;      // completed iterations
     int32_t max_iter;
-    int32_t done;      // 1: no further updates
+    int32_t done;      // 1: no further updates (kernels no-op)
     int32_t status;    // NB_CONVERGED / NB_MAXITER / NB_BROKEDOWN (stagnation decided on host)
-    uint32_t cnt_gs;   // last-block-done counters
-    uint32_t cnt_upd;
-    uint32_t cnt_init;
-    uint32_t pad;
+    int32_t pending;   // 1: x += alpha*p of the last iteration not yet applied (deferred x update)
+    int32_t pad;
 };
 
-// Geometry/maps needed by kernels, passed by value.
+// Scratch of the deterministic two-level grid reductions (nb_common.cuh grid_reduce).
+struct RedWs {
+    double *part;      // [max_blocks * 2]
+    double *part2;     // [max_chunks * 2]
+    uint32_t *cnt;     // [1 + max_chunks], zero, self-resetting
+};
+
+// Geometry needed by kernels, passed by value.
 struct MeshDev {
     int32_t nelx, nely, nelz, p, n;
-    int64_t E, NL, NX, NY, NZ, NG;
+    int32_t E;
+    int64_t NL, NX, NY, NZ, NG;
     int32_t nseg;
 };
 
 struct Workspace {          // per-policy CG workspace (lazily allocated)
     bool ready = false;
-    void *r = nullptr, *p = nullptr, *w = nullptr, *x = nullptr;
-    double *part = nullptr;     // per-block partials (2 slots per block)
+    void *r = nullptr, *p = nullptr, *w = nullptr, *x = nullptr, *z = nullptr;
+    RedWs red = {nullptr, nullptr, nullptr};
     Scal *scal = nullptr;       // device scalars
     Scal *scal_host = nullptr;  // pinned mirror
     double *hist = nullptr;     // device history, capacity hist_cap
     int32_t hist_cap = 0;
-    // conditional-while graph cache
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    int32_t graph_order = -1;
+    // megakernel: grid size, barrier words [2], globaltimer stamps [3 * hist_cap]
+    int32_t mega_G = 0;
+    unsigned int *bar = nullptr;
+    unsigned long long *tim = nullptr;
+    // conditional-while graph cache (one per gs order)
+    cudaGraph_t graph[2] = {nullptr, nullptr};
+    cudaGraphExec_t exec[2] = {nullptr, nullptr};
 };
 
 }  // namespace nb
@@ -69,12 +78,14 @@ struct nb_handle {
     int32_t *gs_off = nullptr;  // [nseg+1]
     int32_t *gs_idx = nullptr;  // [ncopies]
     int32_t *flag = nullptr;    // device error flags for setup checks
-    cudaStream_t cap_stream = nullptr;   // private stream used for graph capture
+    cudaStream_t cap_stream = nullptr;   // private stream used for graph capture / setup
+    int cg_csr = 0;             // 1: consistent-order CG also through the CSR dssum kernel (A/B)
+    int cg_graph = 0;           // 1: per-phase kernels in a CUDA graph instead of the megakernel
     nb::Workspace ws[3];
     nb::MeshDev md() const {
         nb::MeshDev m;
         m.nelx = nelx; m.nely = nely; m.nelz = nelz; m.p = p; m.n = n;
-        m.E = E; m.NL = NL; m.NX = NX; m.NY = NY; m.NZ = NZ; m.NG = NG;
+        m.E = (int32_t)E; m.NL = NL; m.NX = NX; m.NY = NY; m.NZ = NZ; m.NG = NG;
         m.nseg = (int32_t)nseg;
         return m;
     }
@@ -85,8 +96,7 @@ namespace nb {
 // C-3 deformation phases phi_a = pi (1 + U(seed, 3, a)) (host, nb_api.cu)
 void deform_phases(uint64_t seed, double ph[3]);
 
-// ---- launchers implemented in nb_kernels.cu (all asynchronous on `st`) ----
-cudaError_t upload_basis(int n, const double *D);
+// ---- setup launchers (nb_setup_k.cu), asynchronous on `st` unless stated ----
 cudaError_t launch_geometry(const nb_handle *h, const double phi[3], cudaStream_t st);
 cudaError_t launch_jacobi(nb_handle *h, double *diag_scratch, cudaStream_t st);
 cudaError_t build_gs(nb_handle *h, cudaStream_t st);   // allocates gs_off/gs_idx (synchronizes)
@@ -94,18 +104,28 @@ cudaError_t launch_cast(const double *src, float *dst, int64_t n, cudaStream_t s
 cudaError_t launch_maps(const nb_handle *h, int64_t *gid, uint8_t *mask, cudaStream_t st);
 cudaError_t launch_rhs(const nb_handle *h, int kind, double noise, uint64_t seed, int prec,
                        void *b, cudaStream_t st);
-cudaError_t launch_ax(const nb_handle *h, int prec, const void *u, void *w, bool local, cudaStream_t st);
-cudaError_t launch_dssum(const nb_handle *h, int prec, int order, void *u, cudaStream_t st);
 
-// CG pieces
-int grid_ax(const nb_handle *h, int prec);
+// ---- CSR gather-scatter (nb_gs.cu) ----
 int grid_gs(const nb_handle *h);
-int grid_upd(const nb_handle *h, int prec);
-cudaError_t launch_cg_init(const nb_handle *h, int prec, Workspace &ws, const void *b, cudaStream_t st);
-cudaError_t launch_cg_ax(const nb_handle *h, int prec, Workspace &ws, cudaStream_t st);
-cudaError_t launch_cg_gs(const nb_handle *h, int prec, int order, Workspace &ws, cudaStream_t st,
-                         cudaGraphConditionalHandle cond, bool use_cond);
-cudaError_t launch_cg_upd(const nb_handle *h, int prec, Workspace &ws, cudaStream_t st,
-                          cudaGraphConditionalHandle cond, bool use_cond);
+cudaError_t launch_dssum(const nb_handle *h, int prec, int order, void *u, cudaStream_t st);
+// CG K2 (per-copy path, or consistent with cg_csr): w <- QQ^T w, pap partials, alpha finalize
+cudaError_t launch_cg_gs(const nb_handle *h, int prec, int order, Workspace &ws, cudaStream_t st);
+
+// ---- Ax + CG kernels, one translation unit per policy (nb_cg_<policy>.cu) ----
+template <int PREC> cudaError_t launch_ax_local(const nb_handle *h, const void *u, void *w, bool mask, cudaStream_t st);
+template <int PREC> int grid_k1(const nb_handle *h);
+template <int PREC> int grid_k2(const nb_handle *h);
+template <int PREC> cudaError_t launch_cg_init(const nb_handle *h, Workspace &ws, const void *b, cudaStream_t st);
+// K1: p = z + beta p; x += alpha_prev p_old; w = mask A_L p; (with_pap) pap + alpha finalize
+template <int PREC> cudaError_t launch_cg_k1(const nb_handle *h, Workspace &ws, bool with_pap, cudaStream_t st);
+// K2': (gather) w <- QQ^T w on the fly; r -= alpha w; z = M^-1 r; rtr, rho; beta/status finalize
+template <int PREC> cudaError_t launch_cg_k2(const nb_handle *h, Workspace &ws, bool gather, cudaStream_t st,
+                                            cudaGraphConditionalHandle cond, bool use_cond);
+// deferred x += alpha p of the last iteration
+template <int PREC> cudaError_t launch_cg_fin(const nb_handle *h, Workspace &ws, cudaStream_t st);
+// the whole solve as one persistent cooperative kernel (grid size: grid_mega)
+template <int PREC> int grid_mega(const nb_handle *h);
+template <int PREC> cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int order,
+                                              int max_iter, double rtol, unsigned long long *tim, cudaStream_t st);
 
 }  // namespace nb
