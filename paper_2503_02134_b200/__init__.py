@@ -63,7 +63,7 @@ def lib(auto_build: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    if auto_build:
+    if auto_build and not os.environ.get("NB_NO_BUILD"):
         _build_lib()
     if not os.path.exists(LIB):
         raise ImportError(f"{LIB} missing: the CUDA library must be built (python -m paper_2503_02134_b200._build)")

@@ -14,16 +14,17 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
-LIB = os.path.join(PKG, "libnb.so")
+LIB = os.environ.get("NB_LIBPATH") or os.path.join(PKG, "libnb.so")
 UNITS = ("nb_api.cu", "nb_setup_k.cu", "nb_gs.cu", "nb_cg_fp64.cu", "nb_cg_fp32.cu", "nb_cg_mixed.cu")
 SOURCES = [os.path.join(CSRC, f) for f in UNITS]
-HEADERS = [os.path.join(CSRC, f) for f in ("nb_internal.h", "nb_common.cuh", "nb_cg.cuh")] + [
+HEADERS = [os.path.join(CSRC, f) for f in ("nb_internal.h", "nb_common.cuh", "nb_cg.cuh", "nb_gs.cuh", "nb_tma.cuh", "nb_mega_tma.cuh")] + [
     os.path.join(ROOT, "include", "nb.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # No --use_fast_math: IEEE division/sqrt, denormals kept; FMA contraction allowed.
 FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-ftz=false", "-prec-div=true",
          "-prec-sqrt=true", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+FLAGS += [f for f in os.environ.get("NB_NVCC_EXTRA", "").split() if f]   # experiment variants only
 
 
 def stale() -> bool:
@@ -34,7 +35,7 @@ def stale() -> bool:
 
 
 def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + os.environ.get("NB_OBJ_TAG", "") + ".o")
     cmd = [NVCC, *FLAGS, "-c", "-o", obj, src]
     if os.environ.get("NB_PTXAS_V"):
         cmd.insert(1, "-Xptxas=-v")

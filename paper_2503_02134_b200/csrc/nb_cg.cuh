@@ -10,9 +10,10 @@
 //                                                deferred so x is streamed once, :165)
 //                  w = mask . A_L p             (ax -> ax_e: local_grad3, geometric scaling,
 //                                                local_grad3_t, add2; :147, :163)
-//                  pap = sum_l w_l p_l          (glsc3(w,c,p), :164: for continuous p the
-//                                                c-weighted sum over the assembled w equals
-//                                                the plain sum over the unassembled w)
+//                  pap = p^T A_L p              (glsc3(w,c,p), :164: for continuous p, zero on
+//                                                the Dirichlet nodes, the c-weighted sum over
+//                                                the assembled w equals p^T A_L p, taken here
+//                                                in its energy form (Dp)^T G (Dp))
 //                  alpha = rho / pap
 //   B (upd_pencil): w <- QQ^T w on the fly      (gather-scatter "to ensure continuity",
 //                                                :309, :404 -- each copy gathers the copies of
@@ -54,7 +55,22 @@ template <typename T, int N> struct AxCfg {
     static constexpr int ESZ = P * N;                          // one array, one element
     static constexpr int EPB = (N2 >= 256) ? 1 : (256 / N2);   // elements per group
     static constexpr int NT = ((EPB * N2 + 31) / 32) * 32;     // threads per block
-    static constexpr int SMEM = 3 * EPB * ESZ * (int)sizeof(T);
+    static constexpr int SMEM_A = 3 * EPB * ESZ * (int)sizeof(T);
+    // phase B staging per element: r (T), dinv (at most 8 B), 16-byte aligned; then the
+    // x-partner exchange (2 T per pencil)
+    static constexpr int OFF_D = ((N3 * (int)sizeof(T) + 15) / 16) * 16;
+    static constexpr int SLOT = ((OFF_D + N3 * 8 + 15) / 16) * 16;
+    static constexpr int SMEM_B = EPB * SLOT + 2 * EPB * N2 * (int)sizeof(T);
+    static constexpr int SMEM = SMEM_A > SMEM_B ? SMEM_A : SMEM_B;
+    // resident blocks per SM the register allocation must allow (launch bound); fp64 pencils
+    // need twice the registers
+#ifndef NB_MINB_MODE
+#define NB_MINB_MODE 3
+#endif
+    static constexpr int MINB = NB_MINB_MODE == 0 ? 1
+                              : NB_MINB_MODE == 3 ? ((sizeof(T) == 4) ? (NT <= 128 ? 4 : 2) : 1)
+                              : NB_MINB_MODE == 1 ? ((sizeof(T) == 4) ? ((NT <= 128) ? 8 : (NT <= 256 ? 4 : 2)) : ((NT <= 128) ? 4 : 2))
+                                                  : ((sizeof(T) == 4) ? ((NT <= 128) ? 6 : (NT <= 256 ? 3 : 1)) : 1);
 };
 
 template <typename T, int V>
@@ -81,8 +97,21 @@ __device__ __forceinline__ void st_chunk(T *__restrict__ p, const T (&d)[V])
 // pap only.  Returns this thread's pap partial.  Contains 4 __syncthreads; consecutive calls
 // need no barrier in between (phase 1 of the next group touches only the caller's own
 // r-pencil slots, which only the caller read in phase 5).
+// Variants kept for A/B measurement (tools/var_run.sh); defaults are the measured best:
+// NB_AXV 0: w_r^T in registers, pap = sum w p (p from shared); 1: energy form, w_r^T via shared.
+// NB_BV  0: phase B streams pencils per thread (no block barriers); 1: element groups with a
+//           shared-memory x-partner exchange and cp.async staging of r / dinv.
+#ifndef NB_AXV
+#define NB_AXV 0
+#endif
+#ifndef NB_BV
+#define NB_BV 0
+#endif
+#ifndef NB_PHASE_ATTR
+#define NB_PHASE_ATTR __forceinline__
+#endif
 template <int PREC, int N, int MODE>
-__device__ __forceinline__ typename Pol<PREC>::TS
+__device__ NB_PHASE_ATTR typename Pol<PREC>::TS
 ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typename Pol<PREC>::TV *__restrict__ in,
          typename Pol<PREC>::TV *__restrict__ pv, typename Pol<PREC>::TV *__restrict__ xv,
          const typename Pol<PREC>::TV *__restrict__ g, typename Pol<PREC>::TV *__restrict__ w, bool apply_mask,
@@ -137,6 +166,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
     }
     __syncthreads();
+#if NB_AXV == 0
     // ---- 3. ur in registers; geometric factors (C-7); r-part of local_grad3_t
     TV wrt[N];
     if (active) {
@@ -186,7 +216,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
     }
     __syncthreads();
-    // ---- 5. w = (w_r + w_s) + w_t, Dirichlet mask, store; CG: pap partial
+    // ---- 5. w = (w_r + w_s) + w_t, Dirichlet mask, store; CG: pap partial (p from S0)
     TS acc = 0;
     if (active) {
         TV out[N];
@@ -220,6 +250,93 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         }
         st_pencil<TV, N>(w + gbase, out);
     }
+#else
+    // ---- 3. ur in registers; geometric factors (C-7); r-part of local_grad3_t.
+    // CG (MODE 1): pap = p^T A_L p accumulated here in its energy form
+    // sum_nodes (ur, us, ut) . G (ur, us, ut) = sum (ur wr + us ws + ut wt) -- identical to
+    // sum_l p_l (A_L p)_l = glsc3(w, c, p) for continuous p vanishing on the Dirichlet nodes,
+    // a sum of non-negative terms (G is SPD), and needs neither p nor w afterwards.
+    TS acc = 0;
+    if (active) {
+        TV wr[N];
+        {
+            TV v[N];
+            ld_pencil<TV, N>(S0 + rp, v);
+            contract<TV, N>(D, v, wr);   // ur (overwritten by wr below)
+        }
+        const TV *ge = g + (size_t)e * 6 * C::N3 + (size_t)N * q;
+#pragma unroll
+        for (int c = 0; c < N / V; c++) {
+            TV g1[V], g2[V], g3[V], g4[V], g5[V], g6[V], us[V], ut[V], ws[V], wt[V];
+            ld_chunk_h<TV, V, LD_CS>(ge + 0 * C::N3 + c * V, g1);
+            ld_chunk_h<TV, V, LD_CS>(ge + 1 * C::N3 + c * V, g2);
+            ld_chunk_h<TV, V, LD_CS>(ge + 2 * C::N3 + c * V, g3);
+            ld_chunk_h<TV, V, LD_CS>(ge + 3 * C::N3 + c * V, g4);
+            ld_chunk_h<TV, V, LD_CS>(ge + 4 * C::N3 + c * V, g5);
+            ld_chunk_h<TV, V, LD_CS>(ge + 5 * C::N3 + c * V, g6);
+            ld_chunk<TV, V>(A1 + rp + c * V, us);
+            ld_chunk<TV, V>(A2 + rp + c * V, ut);
+#pragma unroll
+            for (int t = 0; t < V; t++) {
+                const TV r_ = wr[c * V + t];
+                const TV wr_ = fma(g3[t], ut[t], fma(g2[t], us[t], g1[t] * r_));
+                ws[t] = fma(g5[t], ut[t], fma(g4[t], us[t], g2[t] * r_));
+                wt[t] = fma(g6[t], ut[t], fma(g5[t], us[t], g3[t] * r_));
+                if (MODE == 1) acc += ((TS)r_ * (TS)wr_ + (TS)us[t] * (TS)ws[t]) + (TS)ut[t] * (TS)wt[t];
+                wr[c * V + t] = wr_;
+            }
+            st_chunk<TV, V>(A1 + rp + c * V, ws);
+            st_chunk<TV, V>(A2 + rp + c * V, wt);
+        }
+        TV o[N];
+        contract_t<TV, N>(D, wr, o);
+        st_pencil<TV, N>(S0 + rp, o);    // own r-pencil slots: only this thread reads them again
+    }
+    __syncthreads();
+    // ---- 4. s- and t-parts of local_grad3_t, in place on the owner's pencils
+    if (active) {
+        TV v[N], o[N];
+#pragma unroll
+        for (int j = 0; j < N; j++) v[j] = A1[sp + N * j];
+        contract_t<TV, N>(D, v, o);
+#pragma unroll
+        for (int j = 0; j < N; j++) A1[sp + N * j] = o[j];
+#pragma unroll
+        for (int k = 0; k < N; k++) v[k] = A2[tp + C::P * k];
+        contract_t<TV, N>(D, v, o);
+#pragma unroll
+        for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
+    }
+    __syncthreads();
+    // ---- 5. w = (w_r + w_s) + w_t, Dirichlet mask, store
+    if (active) {
+        TV out[N];
+        {
+            TV t0[N], t1[N], t2[N];
+            ld_pencil<TV, N>(S0 + rp, t0);
+            ld_pencil<TV, N>(A1 + rp, t1);
+            ld_pencil<TV, N>(A2 + rp, t2);
+#pragma unroll
+            for (int i = 0; i < N; i++) out[i] = (t0[i] + t1[i]) + t2[i];
+        }
+        if (MODE != 0 || apply_mask) {
+            const ElemPos P = elem_pos(m, e);
+            const bool mjk = axis_bnd(a, N, P.ey, m.nely) || axis_bnd(b, N, P.ez, m.nelz);
+#pragma unroll
+            for (int i = 0; i < N; i++)
+                if (mjk || axis_bnd(i, N, P.ex, m.nelx)) out[i] = TV(0);
+            if (MODE == 2) {   // unshared nodes only (c = 1); the CSR phase adds the shared ones
+                const bool sjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz) > 1;
+                TV pp[N];
+                ld_pencil<TV, N>(pv + gbase, pp);   // written by this thread in step 1
+#pragma unroll
+                for (int i = 0; i < N; i++)
+                    if (!sjk && axis_mult(i, N, P.ex, m.nelx) == 1) acc += (TS)out[i] * (TS)pp[i];
+            }
+        }
+        st_pencil<TV, N>(w + gbase, out);
+    }
+#endif
     return acc;
 }
 
@@ -233,7 +350,8 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
 template <int PREC, int N>
 __device__ __forceinline__ void gather_pencil(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ w,
                                               int e, const ElemPos &P, int a, int b,
-                                              typename Pol<PREC>::TV (&ww)[N])
+                                              typename Pol<PREC>::TV (&ww)[N], typename Pol<PREC>::TV own_l,
+                                              typename Pol<PREC>::TV own_r)
 {
     using TV = typename Pol<PREC>::TV;
     using TG = typename Pol<PREC>::TG;
@@ -242,39 +360,54 @@ __device__ __forceinline__ void gather_pencil(const MeshDev &m, const typename P
     const int zs = (b == 0 && P.ez > 0) ? -1 : ((b == N - 1 && P.ez < m.nelz - 1) ? 1 : 0);
     const bool xl = P.ex > 0, xr = P.ex < m.nelx - 1;
     if (ys == 0 && zs == 0 && !xl && !xr) return;
-    const int ny = ys ? 2 : 1, nz = zs ? 2 : 1;
+    // Issue every neighbour load first (one L2 round trip), then sum in the fixed order.
+    // Copies of the pencil's nodes: own (0,0), y-neighbour (0,1), z-neighbour (1,0) and the
+    // yz-diagonal neighbour (1,1); each with its x-partners for the end nodes.
+    TV vy[N], vz[N], vyz[N];
+    TV ly = 0, ry = 0, lz = 0, rz = 0, lyz = 0, ryz = 0;
+    const size_t base = ((size_t)e * N2 + (size_t)(a + N * b)) * N;
+    const int64_t sy = (int64_t)ys * (m.nelx * (int64_t)N3) + (int64_t)(ys ? (N - 1 - 2 * a) : 0) * N;
+    const int64_t sz = (int64_t)zs * ((int64_t)m.nelx * m.nely * N3) + (int64_t)(zs ? (N - 1 - 2 * b) : 0) * N2;
+    if (ys) {
+        ld_pencil<TV, N, LD_CG>(w + base + sy, vy);
+        if (xl) ly = __ldcg(w + base + sy - N3 + (N - 1));
+        if (xr) ry = __ldcg(w + base + sy + N3);
+    }
+    if (zs) {
+        ld_pencil<TV, N, LD_CG>(w + base + sz, vz);
+        if (xl) lz = __ldcg(w + base + sz - N3 + (N - 1));
+        if (xr) rz = __ldcg(w + base + sz + N3);
+    }
+    if (ys && zs) {
+        ld_pencil<TV, N, LD_CG>(w + base + sy + sz, vyz);
+        if (xl) lyz = __ldcg(w + base + sy + sz - N3 + (N - 1));
+        if (xr) ryz = __ldcg(w + base + sy + sz + N3);
+    }
+    // ascending element order: lexicographic (dz, dy, dx); a negative offset comes first
     TG s[N];
-#pragma unroll 1
-    for (int iz = 0; iz < nz; iz++) {
-        const int dz = zs < 0 ? iz - 1 : iz;            // ascending: {-1,0} or {0,+1} or {0}
-#pragma unroll 1
-        for (int iy = 0; iy < ny; iy++) {
-            const int dy = ys < 0 ? iy - 1 : iy;
-            const int e2 = e + dy * m.nelx + dz * m.nelx * m.nely;
-            const int a2 = dy == 0 ? a : N - 1 - a;
-            const int b2 = dz == 0 ? b : N - 1 - b;
-            const size_t base2 = (size_t)e2 * N3 + (size_t)N * a2 + (size_t)N2 * b2;
-            TV v[N];
-            if (dy == 0 && dz == 0) {
 #pragma unroll
-                for (int i = 0; i < N; i++) v[i] = ww[i];
-            } else {
-                ld_pencil<TV, N, LD_CG>(w + base2, v);
-            }
-            const TV lft = xl ? __ldcg(w + base2 - N3 + (N - 1)) : TV(0);   // node i=0's copy in e2-1
-            const TV rgt = xr ? __ldcg(w + base2 + N3) : TV(0);             // node i=N-1's copy in e2+1
-            if (iz == 0 && iy == 0) {
+    for (int iz = 0; iz < 2; iz++) {
 #pragma unroll
-                for (int i = 0; i < N; i++) s[i] = (TG)v[i];
-                if (xl) s[0] = (TG)lft + (TG)v[0];
-                if (xr) s[N - 1] = (TG)v[N - 1] + (TG)rgt;
-            } else {
+        for (int iy = 0; iy < 2; iy++) {
+            if (iz == 1 && !zs) continue;
+            if (iy == 1 && !ys) continue;
+            const bool zf = zs ? ((zs < 0) == (iz == 0)) : false;   // this combo uses the z-neighbour
+            const bool yf = ys ? ((ys < 0) == (iy == 0)) : false;
+            const bool first = (iz == 0 && iy == 0);
 #pragma unroll
-                for (int i = 1; i < N - 1; i++) s[i] += (TG)v[i];
-                if (xl) s[0] += (TG)lft;
-                s[0] += (TG)v[0];
-                s[N - 1] += (TG)v[N - 1];
-                if (xr) s[N - 1] += (TG)rgt;
+            for (int i = 0; i < N; i++) {
+                const TV v = zf ? (yf ? vyz[i] : vz[i]) : (yf ? vy[i] : ww[i]);
+                if (i == 0 && xl) {
+                    const TV l = zf ? (yf ? lyz : lz) : (yf ? ly : own_l);
+                    s[0] = first ? (TG)l : s[0] + (TG)l;
+                    s[0] += (TG)v;
+                } else {
+                    s[i] = first ? (TG)v : s[i] + (TG)v;
+                }
+                if (i == N - 1 && xr) {
+                    const TV rr = zf ? (yf ? ryz : rz) : (yf ? ry : own_r);
+                    s[N - 1] += (TG)rr;
+                }
             }
         }
     }
@@ -305,7 +438,12 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
     ld_pencil<TV, N, LD_CG>(w + base, ww);
     ld_pencil<TV, N>(r + base, rr);
     ld_pencil<TJ, N, LD_NC>(dinv + base, dd);
-    if (GATHER) gather_pencil<PREC, N>(m, w, e, P, a, b, ww);
+    if (GATHER) {
+        constexpr int N3 = N * N * N;
+        const TV ol = P.ex > 0 ? __ldcg(w + base - N3 + (N - 1)) : TV(0);
+        const TV orr = P.ex < m.nelx - 1 ? __ldcg(w + base + N3) : TV(0);
+        gather_pencil<PREC, N>(m, w, e, P, a, b, ww, ol, orr);
+    }
     const int mjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz);
 #pragma unroll
     for (int i = 0; i < N; i++) {
@@ -318,6 +456,74 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
     }
     st_pencil<TV, N>(r + base, rr);
     st_pencil<TV, N>(z + base, zz);
+}
+
+// Phase B for one group of EPB elements with the phase-A thread mapping (all threads of the
+// block call it).  The x-partners of the own pencil come from the neighbouring element's
+// thread through shared memory when that element is in the same group (xch: EPB*N^2*2 TV).
+template <int PREC, int N, int GATHER>
+__device__ NB_PHASE_ATTR void upd_group(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ w,
+                                        typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
+                                        const typename Pol<PREC>::TJ *__restrict__ dinv,
+                                        typename Pol<PREC>::TV alpha, int e, bool active, int el, int a, int b,
+                                        int e_end, unsigned char *__restrict__ smem,
+                                        typename Pol<PREC>::TS &rtr, typename Pol<PREC>::TS &rho)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TJ = typename Pol<PREC>::TJ;
+    using TS = typename Pol<PREC>::TS;
+    using C = AxCfg<TV, N>;
+    constexpr int N2 = N * N, N3 = N * N * N;
+    const int q = a + N * b;
+    const size_t base = ((size_t)e * N2 + q) * N;
+    // shared staging of this element slot: r [N^3] TV | dinv [N^3] TJ; then the x-partner exchange
+    TV *sr = reinterpret_cast<TV *>(smem + (size_t)(el < C::EPB ? el : 0) * C::SLOT);
+    TJ *sd = reinterpret_cast<TJ *>(reinterpret_cast<unsigned char *>(sr) + C::OFF_D);
+    TV *xch = reinterpret_cast<TV *>(smem + (size_t)C::EPB * C::SLOT);
+    TV ww[N];
+    ElemPos P;
+    if (active) {
+        // r and dinv go to shared memory asynchronously: not held in registers during the gather
+        cp_pencil_async<TV, N>(sr + q * N, r + base);
+        cp_pencil_async<TJ, N>(sd + q * N, dinv + base);
+        cp_async_commit();
+        ld_pencil<TV, N, LD_CG>(w + base, ww);
+        P = elem_pos(m, e);
+    }
+    if (GATHER) {
+        if (active) {
+            xch[2 * (el * N2 + q)] = ww[0];
+            xch[2 * (el * N2 + q) + 1] = ww[N - 1];
+        }
+        __syncthreads();
+        if (active) {
+            TV ol = 0, orr = 0;
+            if (P.ex > 0) ol = el > 0 ? xch[2 * ((el - 1) * N2 + q) + 1] : __ldcg(w + base - N3 + (N - 1));
+            if (P.ex < m.nelx - 1)
+                orr = (el + 1 < C::EPB && e + 1 < e_end) ? xch[2 * ((el + 1) * N2 + q)] : __ldcg(w + base + N3);
+            gather_pencil<PREC, N>(m, w, e, P, a, b, ww, ol, orr);
+        }
+        __syncthreads();
+    }
+    if (active) {
+        cp_async_wait_all();   // own copies only: no barrier needed
+        TV rr[N], zz[N];
+        TJ dd[N];
+        ld_pencil<TV, N>(sr + q * N, rr);
+        ld_pencil<TJ, N>(sd + q * N, dd);
+        const int mjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz);
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            rr[i] = fma(-alpha, ww[i], rr[i]);                   // add2s2(r, w, -alpha)
+            zz[i] = (TV)((TJ)rr[i] * dd[i]);                     // solveM
+            const TS c = (TS)1 / (TS)(mjk * axis_mult(i, N, P.ex, m.nelx));
+            const TS rs = (TS)rr[i];
+            rtr += (rs * c) * rs;                                // glsc3(r, c, r)
+            rho += (rs * c) * (TS)zz[i];                         // glsc3(r, c, z)
+        }
+        st_pencil<TV, N>(r + base, rr);
+        st_pencil<TV, N>(z + base, zz);
+    }
 }
 
 // CG prologue for one pencil: r = b, x = 0, p = 0, z = M^-1 r; rtr0 and rho_1 partials.
@@ -435,7 +641,7 @@ __device__ __forceinline__ TS all_blocks_sum(const double *part, int G, int K, i
 }
 
 template <int PREC, int N, int FUSED>
-__global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT)
+__global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT, AxCfg<typename Pol<PREC>::TV, N>::MINB)
 k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D)
 {
     using TV = typename Pol<PREC>::TV;
@@ -444,128 +650,179 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
     using C = AxCfg<TV, N>;
     extern __shared__ __align__(16) unsigned char smraw[];
     __shared__ TS sh[32];
-    const MeshDev &m = A.m;
-    const int G = gridDim.x, bk = blockIdx.x, tid = threadIdx.x;
-    TV *x = (TV *)A.x, *pv = (TV *)A.p, *r = (TV *)A.r, *z = (TV *)A.z, *w = (TV *)A.w;
-    const TV *g = (const TV *)A.g;
-    const TJ *dinv = (const TJ *)A.dinv;
-    const bool t0 = (bk == 0 && tid == 0);
-
-    // element range of this block, as whole groups of EPB elements
-    const int64_t ngroups = ((int64_t)m.E + C::EPB - 1) / C::EPB;
-    const int64_t g0 = split(ngroups, G, bk), g1 = split(ngroups, G, bk + 1);
-    const int el = tid / C::N2;
-    const int q = tid - el * C::N2;
-    const int a = q % N, b = q / N;
-    TV *S0 = reinterpret_cast<TV *>(smraw) + (el < C::EPB ? el : 0) * 3 * C::ESZ;
-    const int64_t p0 = min((int64_t)m.E, g0 * C::EPB) * C::N2, p1 = min((int64_t)m.E, g1 * C::EPB) * C::N2;
+    // Solver state lives in shared memory, not registers: it is live across both phases,
+    // and every register it held would be taken from the phases' pencils (occupancy).
+    struct State {
+        TS rtr0, rho, rtr, beta, alpha, pap;
+        int it, status, pending, done;
+    };
+    __shared__ State st;
+    const int tid = threadIdx.x;
+    const bool t0 = (blockIdx.x == 0 && tid == 0);
+#define NB_G0 split(((int64_t)A.m.E + C::EPB - 1) / C::EPB, gridDim.x, blockIdx.x)
+#define NB_G1 split(((int64_t)A.m.E + C::EPB - 1) / C::EPB, gridDim.x, blockIdx.x + 1)
+#define NB_EL (threadIdx.x / C::N2)
+#define NB_A ((threadIdx.x - NB_EL * C::N2) % N)
+#define NB_B ((threadIdx.x - NB_EL * C::N2) / N)
+#define NB_S0 (reinterpret_cast<TV *>(smraw) + (NB_EL < C::EPB ? NB_EL : 0) * 3 * C::ESZ)
 
     // ---- prologue: r = b, x = p = 0, z = M^-1 r; rtr0, rho_1
     {
+        const int64_t p0 = min((int64_t)A.m.E, NB_G0 * C::EPB) * C::N2;
+        const int64_t p1 = min((int64_t)A.m.E, NB_G1 * C::EPB) * C::N2;
         TS rtr = 0, rho = 0;
+#pragma unroll 1
         for (int64_t pid = p0 + tid; pid < p1; pid += blockDim.x)
-            init_pencil<PREC, N>(m, (const TV *)A.b, x, pv, r, z, dinv, pid, rtr, rho);
+            init_pencil<PREC, N>(A.m, (const TV *)A.b, (TV *)A.x, (TV *)A.p, (TV *)A.r, (TV *)A.z,
+                                 (const TJ *)A.dinv, pid, rtr, rho);
         rtr = block_sum<TS>(rtr, sh);
         rho = block_sum<TS>(rho, sh);
-        if (tid == 0) { A.partB[2 * bk] = (double)rtr; A.partB[2 * bk + 1] = (double)rho; }
+        if (tid == 0) { A.partB[2 * blockIdx.x] = (double)rtr; A.partB[2 * blockIdx.x + 1] = (double)rho; }
     }
     grid_barrier(A.bar);
     if (t0 && A.tim) A.tim[0] = globaltimer();
-    const TS rtr0 = all_blocks_sum<TS>(A.partB, G, 2, 0, sh);
-    TS rho = all_blocks_sum<TS>(A.partB, G, 2, 1, sh);
-    TS rtr = rtr0, beta = 0, alpha = 0, pap = 0;
-    int it = 0, status = NB_MAXITER;
-    bool pending = false, done = false;
-    if (t0) A.hist[0] = rtr0 == (TS)0 ? 0.0 : 1.0;
-    if (rtr0 == (TS)0) { status = NB_CONVERGED; done = true; }
-    else if (!isfinite((double)rtr0)) { status = NB_BROKEDOWN; done = true; }
-    else if (A.max_iter <= 0) { status = NB_MAXITER; done = true; }
-
-    while (!done) {
-        // ---- phase A: p update, deferred x update, w = mask A_L p, pap partial
-        TS acc = 0;
-        {
-            const TV bv = (TV)beta, av = pending ? (TV)alpha : TV(0);
-            for (int64_t gr = g0; gr < g1; gr++) {
-                const int e = (int)(gr * C::EPB) + el;
-                const bool active = el < C::EPB && e < m.E;
-                acc += ax_group<PREC, N, FUSED ? 1 : 2>(m, D, z, pv, x, g, w, true, bv, av, e, active, a, b, S0);
-            }
+    {
+        const TS rtr0 = all_blocks_sum<TS>(A.partB, gridDim.x, 2, 0, sh);
+        const TS rho = all_blocks_sum<TS>(A.partB, gridDim.x, 2, 1, sh);
+        if (tid == 0) {
+            st.rtr0 = rtr0; st.rho = rho; st.rtr = rtr0; st.beta = 0; st.alpha = 0; st.pap = 0;
+            st.it = 0; st.status = NB_MAXITER; st.pending = 0; st.done = 0;
+            if (rtr0 == (TS)0) { st.status = NB_CONVERGED; st.done = 1; }
+            else if (!isfinite((double)rtr0)) { st.status = NB_BROKEDOWN; st.done = 1; }
+            else if (A.max_iter <= 0) { st.status = NB_MAXITER; st.done = 1; }
+            if (blockIdx.x == 0) A.hist[0] = rtr0 == (TS)0 ? 0.0 : 1.0;
         }
-        acc = block_sum<TS>(acc, sh);
-        if (tid == 0) A.partA[bk] = (double)acc;
+        __syncthreads();
+    }
+
+#pragma unroll 1
+    while (!st.done) {
+        // ---- phase A: p update, deferred x update, w = mask A_L p, pap partial
+        {
+            TS acc = 0;
+            const TV bv = (TV)st.beta, av = st.pending ? (TV)st.alpha : TV(0);
+            const int64_t g1 = NB_G1;
+#pragma unroll 1
+            for (int64_t gr = NB_G0; gr < g1; gr++) {
+                const int e = (int)(gr * C::EPB) + NB_EL;
+                const bool active = NB_EL < C::EPB && e < A.m.E;
+                acc += ax_group<PREC, N, FUSED ? 1 : 2>(A.m, D, (const TV *)A.z, (TV *)A.p, (TV *)A.x,
+                                                        (const TV *)A.g, (TV *)A.w, true, bv, av, e, active, NB_A,
+                                                        NB_B, NB_S0);
+            }
+            acc = block_sum<TS>(acc, sh);
+            if (tid == 0) A.partA[blockIdx.x] = (double)acc;
+        }
         grid_barrier(A.bar);
-        if (t0 && A.tim) A.tim[3 * it + 1] = globaltimer();
-        pap = all_blocks_sum<TS>(A.partA, G, 1, 0, sh);
+        if (t0 && A.tim) A.tim[3 * st.it + 1] = globaltimer();
+        TS pap = all_blocks_sum<TS>(A.partA, gridDim.x, 1, 0, sh);
         if (!FUSED) {
             // ---- CSR gather-scatter phase: per-copy (or consistent) QQ^T, shared pap partial
-            const int64_t s0 = split(A.nseg, G, bk), s1 = split(A.nseg, G, bk + 1);
+            const int64_t s0 = split(A.nseg, gridDim.x, blockIdx.x), s1 = split(A.nseg, gridDim.x, blockIdx.x + 1);
             TS acc2 = 0;
             for (int64_t s = s0 + tid; s < s1; s += blockDim.x) {
                 if (A.order == NB_GS_CONSISTENT)
                     acc2 += gs_segment<PREC, NB_GS_CONSISTENT, 1, TV, typename Pol<PREC>::TG, LD_CG>(
-                        (int32_t)s, A.gs_off, A.gs_idx, w, pv);
+                        (int32_t)s, A.gs_off, A.gs_idx, (TV *)A.w, (const TV *)A.p);
                 else
                     acc2 += gs_segment<PREC, NB_GS_PER_COPY, 1, TV, typename Pol<PREC>::TG, LD_CG>(
-                        (int32_t)s, A.gs_off, A.gs_idx, w, pv);
+                        (int32_t)s, A.gs_off, A.gs_idx, (TV *)A.w, (const TV *)A.p);
             }
             acc2 = block_sum<TS>(acc2, sh);
-            if (tid == 0) A.partS[bk] = (double)acc2;
+            if (tid == 0) A.partS[blockIdx.x] = (double)acc2;
             grid_barrier(A.bar);
-            pap = pap + all_blocks_sum<TS>(A.partS, G, 1, 0, sh);
+            pap = pap + all_blocks_sum<TS>(A.partS, gridDim.x, 1, 0, sh);
         }
-        if (t0 && A.tim) A.tim[3 * it + 2] = globaltimer();
-        if (!(pap > (TS)0) || !isfinite((double)pap) || !isfinite((double)rho)) {
-            status = NB_BROKEDOWN;
-            pending = false;     // x already holds x_k (alpha_prev p_old applied in phase A)
-            break;
+        if (t0 && A.tim) A.tim[3 * st.it + 2] = globaltimer();
+        if (tid == 0) {
+            st.pap = pap;
+            if (!(pap > (TS)0) || !isfinite((double)pap) || !isfinite((double)st.rho)) {
+                st.status = NB_BROKEDOWN;
+                st.pending = 0;     // x already holds x_k (alpha_prev p_old applied in phase A)
+                st.done = 2;
+            } else {
+                st.alpha = st.rho / pap;
+                st.pending = 1;
+            }
         }
-        alpha = rho / pap;
-        pending = true;
+        __syncthreads();
+        if (st.done) break;
         // ---- phase B: (gather) r -= alpha w, z = M^-1 r, rtr and rho partials
         {
             TS prtr = 0, prho = 0;
-            const TV av = (TV)alpha;
-            for (int64_t pid = p0 + tid; pid < p1; pid += blockDim.x)
-                upd_pencil<PREC, N, FUSED>(m, w, r, z, dinv, av, pid, prtr, prho);
+            const TV av = (TV)st.alpha;
+            const int64_t g1 = NB_G1;
+            const int e_end = (int)min((int64_t)A.m.E, g1 * C::EPB);
+#if NB_BV == 1
+#pragma unroll 1
+            for (int64_t gr = NB_G0; gr < g1; gr++) {
+                const int e = (int)(gr * C::EPB) + NB_EL;
+                const bool active = NB_EL < C::EPB && e < e_end;
+                upd_group<PREC, N, FUSED>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, (const TJ *)A.dinv, av, e,
+                                          active, NB_EL, NB_A, NB_B, e_end, smraw, prtr, prho);
+            }
+#else
+            (void)e_end;
+            const int64_t p1 = (int64_t)e_end * C::N2;
+#pragma unroll 1
+            for (int64_t pid = NB_G0 * C::EPB * C::N2 + tid; pid < p1; pid += blockDim.x)
+                upd_pencil<PREC, N, FUSED>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, (const TJ *)A.dinv, av, pid,
+                                           prtr, prho);
+#endif
             prtr = block_sum<TS>(prtr, sh);
             prho = block_sum<TS>(prho, sh);
-            if (tid == 0) { A.partB[2 * bk] = (double)prtr; A.partB[2 * bk + 1] = (double)prho; }
+            if (tid == 0) { A.partB[2 * blockIdx.x] = (double)prtr; A.partB[2 * blockIdx.x + 1] = (double)prho; }
         }
         grid_barrier(A.bar);
-        rtr = all_blocks_sum<TS>(A.partB, G, 2, 0, sh);
-        const TS rho_new = all_blocks_sum<TS>(A.partB, G, 2, 1, sh);
-        it++;
-        const double res = sqrt((double)rtr / (double)rtr0);
-        if (t0) {
-            A.hist[it] = res;
-            if (A.tim) A.tim[3 * it] = globaltimer();
+        {
+            const TS rtr = all_blocks_sum<TS>(A.partB, gridDim.x, 2, 0, sh);
+            const TS rho_new = all_blocks_sum<TS>(A.partB, gridDim.x, 2, 1, sh);
+            if (tid == 0) {
+                const int it = st.it + 1;
+                const double res = sqrt((double)rtr / (double)st.rtr0);
+                if (blockIdx.x == 0) {
+                    A.hist[it] = res;
+                    if (A.tim) A.tim[3 * it] = globaltimer();
+                }
+                if (!isfinite((double)rtr) || !isfinite((double)rho_new)) { st.status = NB_BROKEDOWN; st.done = 1; }
+                else if (res <= A.rtol || rtr == (TS)0) { st.status = NB_CONVERGED; st.done = 1; }
+                else if (it >= A.max_iter) { st.status = NB_MAXITER; st.done = 1; }
+                st.beta = rho_new / st.rho;
+                st.rho = rho_new;
+                st.rtr = rtr;
+                st.it = it;
+            }
+            __syncthreads();
         }
-        if (!isfinite((double)rtr) || !isfinite((double)rho_new)) { status = NB_BROKEDOWN; done = true; }
-        else if (res <= A.rtol || rtr == (TS)0) { status = NB_CONVERGED; done = true; }
-        else if (it >= A.max_iter) { status = NB_MAXITER; done = true; }
-        beta = rho_new / rho;
-        rho = rho_new;
     }
     // ---- epilogue: the deferred x += alpha p of the last iteration (own elements)
-    if (pending) {
-        const TV av = (TV)alpha;
-        const int64_t l0 = p0 * N, l1 = p1 * N;
+    if (st.pending) {
+        const TV av = (TV)st.alpha;
+        const int64_t l0 = min((int64_t)A.m.E, NB_G0 * C::EPB) * C::N3;
+        const int64_t l1 = min((int64_t)A.m.E, NB_G1 * C::EPB) * C::N3;
+        TV *x = (TV *)A.x;
+        const TV *pv = (const TV *)A.p;
         for (int64_t l = l0 + tid; l < l1; l += blockDim.x) x[l] = fma(av, pv[l], x[l]);
     }
     if (t0) {
         Scal *s = A.scal;
-        s->rho = (double)rho; s->beta = (double)beta; s->alpha = (double)alpha; s->pap = (double)pap;
-        s->rtr = (double)rtr; s->rtr0 = (double)rtr0; s->iter = it; s->status = status; s->done = 1;
+        s->rho = (double)st.rho; s->beta = (double)st.beta; s->alpha = (double)st.alpha; s->pap = (double)st.pap;
+        s->rtr = (double)st.rtr; s->rtr0 = (double)st.rtr0; s->iter = st.it; s->status = st.status; s->done = 1;
         s->pending = 0;
     }
+#undef NB_G0
+#undef NB_G1
+#undef NB_EL
+#undef NB_A
+#undef NB_B
+#undef NB_S0
 }
 
 // ===========================================================================
 // graph driver: one persistent kernel per phase, last-block finalize
 // ===========================================================================
 template <int PREC, int N, int MODE>
-__global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT)
+__global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT, AxCfg<typename Pol<PREC>::TV, N>::MINB)
 k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
      const typename Pol<PREC>::TV *__restrict__ in, typename Pol<PREC>::TV *__restrict__ pv,
      typename Pol<PREC>::TV *__restrict__ xv, const typename Pol<PREC>::TV *__restrict__ g,
@@ -589,6 +846,7 @@ k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
     const int64_t ngroups = ((int64_t)m.E + C::EPB - 1) / C::EPB;
     const int64_t g0 = split(ngroups, gridDim.x, blockIdx.x), g1 = split(ngroups, gridDim.x, blockIdx.x + 1);
     TS acc = 0;
+#pragma unroll 1
     for (int64_t gr = g0; gr < g1; gr++) {
         const int e = (int)(gr * C::EPB) + el;
         const bool active = el < C::EPB && e < m.E;
@@ -838,60 +1096,6 @@ cudaError_t launch_cg_fin(const nb_handle *h, Workspace &ws, cudaStream_t st)
     const int grid = grid_for(h->NL, 256, h->sm_count, 8);
     k_fin<PREC><<<grid, 256, 0, st>>>(h->NL, (TV *)ws.x, (const TV *)ws.p, ws.scal);
     return cudaGetLastError();
-}
-
-// ---- megakernel ----
-template <int PREC, int N, int FUSED>
-static int mega_grid_t(const nb_handle *h)
-{
-    using TV = typename Pol<PREC>::TV;
-    using C = AxCfg<TV, N>;
-    static int occ = -1;
-    if (occ < 0) {
-        cudaFuncSetAttribute(k_cg_mega<PREC, N, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        occ = occupancy(k_cg_mega<PREC, N, FUSED>, C::NT, C::SMEM);
-    }
-    return h->sm_count * occ;
-}
-
-template <int PREC>
-int grid_mega(const nb_handle *h)
-{
-    NB_DISPATCH_N(h->n, return (mega_grid_t<PREC, NN, 1>(h) > mega_grid_t<PREC, NN, 0>(h) ? mega_grid_t<PREC, NN, 1>(h)
-                                                                                            : mega_grid_t<PREC, NN, 0>(h)))
-}
-
-template <int PREC, int N, int FUSED>
-static cudaError_t mega_launch_t(const nb_handle *h, const MegaArgs &args, cudaStream_t st)
-{
-    using TV = typename Pol<PREC>::TV;
-    using C = AxCfg<TV, N>;
-    const int grid = mega_grid_t<PREC, N, FUSED>(h);
-    DMat<TV, N> D = make_dmat<TV, N>(h->D);
-    void *params[2] = {(void *)&args, (void *)&D};
-    return cudaLaunchCooperativeKernel((const void *)k_cg_mega<PREC, N, FUSED>, dim3(grid), dim3(C::NT), params,
-                                       (size_t)C::SMEM, st);
-}
-
-template <int PREC>
-cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int order, int max_iter, double rtol,
-                           unsigned long long *tim, cudaStream_t st)
-{
-    MegaArgs A;
-    A.m = h->md();
-    A.b = b;
-    A.x = ws.x; A.p = ws.p; A.r = ws.r; A.z = ws.z; A.w = ws.w;
-    A.g = (sizeof(typename Pol<PREC>::TV) == 8) ? (const void *)h->g64 : (const void *)h->g32;
-    A.dinv = PREC == NB_FP32 ? (const void *)h->dinv32 : (const void *)h->dinv64;
-    A.gs_off = h->gs_off; A.gs_idx = h->gs_idx; A.nseg = (int32_t)h->nseg;
-    A.order = order; A.max_iter = max_iter; A.rtol = rtol;
-    A.hist = ws.hist; A.tim = tim;
-    A.partA = ws.red.part; A.partS = ws.red.part + ws.mega_G; A.partB = ws.red.part + 2 * ws.mega_G;
-    A.bar = ws.bar;
-    A.scal = ws.scal;
-    const bool fused = order == NB_GS_CONSISTENT && !h->cg_csr;
-    if (fused) { NB_DISPATCH_N(h->n, return (mega_launch_t<PREC, NN, 1>(h, A, st))) }
-    NB_DISPATCH_N(h->n, return (mega_launch_t<PREC, NN, 0>(h, A, st)))
 }
 
 #define NB_INSTANTIATE_CG(P)                                                                                  \

@@ -120,6 +120,29 @@ __device__ __forceinline__ void st_pencil(T *__restrict__ dst, const T (&v)[N])
 }
 
 // ---------------------------------------------------------------------------
+// asynchronous global -> shared copies (cp.async, LDGSTS): stage a pencil in shared memory
+// without holding it in registers.  .cg (L2 only) for 16-byte chunks, .ca otherwise.
+// ---------------------------------------------------------------------------
+template <int B>
+__device__ __forceinline__ void cp_async(void *s, const void *g)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+    if (B == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(sa), "l"(g), "n"(B) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <typename T, int N>
+__device__ __forceinline__ void cp_pencil_async(T *sdst, const T *gsrc)
+{
+    constexpr int V = VecW<T, N>::V;
+#pragma unroll
+    for (int c = 0; c < N / V; c++) cp_async<V * (int)sizeof(T)>(sdst + c * V, gsrc + c * V);
+}
+
+// ---------------------------------------------------------------------------
 // lattice helpers: multiplicity and mask are analytic on the box
 // (int32 is enough: n_local < 2^31 is enforced at setup)
 // ---------------------------------------------------------------------------
@@ -242,7 +265,14 @@ __device__ __forceinline__ double unif(uint64_t seed, uint64_t stream, uint64_t 
     return (double)(splitmix(seed, stream, i) >> 11) * 0x1.0p-52 - 1.0;
 }
 
-// order dispatch (n = p+1 in [2,16])
+// order dispatch (n = p+1 in [2,16]); NB_ONLY_N (experiments) compiles a single order
+#ifdef NB_ONLY_N
+#define NB_DISPATCH_N(n, CALL)                            \
+    switch (n) {                                          \
+    case NB_ONLY_N: { constexpr int NN = NB_ONLY_N; CALL; } \
+    default: return cudaErrorInvalidValue;                \
+    }
+#else
 #define NB_DISPATCH_N(n, CALL)                 \
     switch (n) {                               \
     case 2: { constexpr int NN = 2; CALL; }    \
@@ -262,6 +292,7 @@ __device__ __forceinline__ double unif(uint64_t seed, uint64_t stream, uint64_t 
     case 16: { constexpr int NN = 16; CALL; }  \
     default: return cudaErrorInvalidValue;     \
     }
+#endif
 
 template <typename T, int N>
 inline DMat<T, N> make_dmat(const double *D)
