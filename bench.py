@@ -214,7 +214,7 @@ def run_ours(args):
         solve()
     clocks = Clocks(dev)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    iters, launches, statuses = [], 0, set()
+    iters, launches, statuses, lib_ms = [], 0, set(), []
     barrier_sync(world)
     clocks.start()
     for s in range(args.steps):
@@ -225,6 +225,7 @@ def run_ours(args):
         iters.append(rep.iterations)
         statuses.add(rep.status)
         launches += rep.kernel_launches
+        lib_ms.append(rep.solve_ms)
     barrier_sync(world)
     ck = clocks.stop()
     step_ms = [a.elapsed_time(b2) for a, b2 in ev]
@@ -233,7 +234,8 @@ def run_ours(args):
     dof_iter = sum_over_ranks(float(NL * sum(iters)), world)
     value = dof_iter / t_max
 
-    # per-kernel durations: the same solve with CUDA events around every launch (same stream)
+    # per-phase device time of the same solve: the megakernel's block 0 stamps %globaltimer after
+    # every grid barrier (nb_cg_report k_ax_ms / k_upd_ms); graph driver: CUDA events per launch
     kt = [solve(time_kernels=True) for _ in range(max(1, min(args.steps, 3)))]
     it_k = sum(r.iterations for r in kt)
     k1_ms = sum(r.k_ax_ms for r in kt) / it_k
@@ -248,10 +250,11 @@ def run_ours(args):
     ax_ms = time_launches(lambda: nb.nb_ax(mesh.h, pol, u, wv, nb.NB_AX_LOCAL), 50, st)
     gs_ms = time_launches(lambda: nb.nb_dssum(mesh.h, pol, nb.NB_GS_CONSISTENT, wv), 50, st)
     gs_bytes = info.n_shared_copies * (2 * vs + 4) + (info.n_shared_global + 1) * 4
+    # DRAM traffic of the solve kernel from the committed ncu capture (profiles/), per iteration
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(f"k_ax_{args.policy}_configs1")
+            traffic = json.load(f).get(f"{args.policy}_configs1_dram_bytes_per_iteration")
     except Exception:
         pass
 
@@ -309,19 +312,24 @@ def run_ours(args):
                                n_local=NL, l2="256 MiB write between steps (outside the step events)",
                                parallelism="replicas" if world > 1 else "single GPU"),
                 "time_to_rtol_ms": ms_per_step,
-                "roofline": {"bound": "hbm", "kernel": "K1 k_ax (Jacobi p-update + deferred x + local Ax + mask + pap)",
+                "step_ms": {"events_around_call": step_ms, "library_device_ms": lib_ms},
+                "roofline": {"bound": "hbm",
+                             "kernel": "k_cg_mega phase A (Jacobi p-update + deferred x update + local Ax + mask + pap), "
+                                       "per CG iteration",
                              "achieved": k1_ach, "peak": peak, "unit": "GB/s", "frac": k1_ach / peak,
-                             "traffic": traffic, "peak_source": peak_src,
+                             "traffic": traffic, "traffic_note": "ncu dram read+write of the whole megakernel "
+                                                                 "(both phases) per iteration, profiles/",
+                             "alg_bytes_per_iteration": k1_bytes + k2_bytes, "peak_source": peak_src,
                              "alg_bytes_per_launch": k1_bytes, "avg_launch_us": 1e3 * k1_ms,
                              "share_of_iteration": k1_ms / (k1_ms + k2_ms)},
                 "kernels": {
-                    "K1_ax": {"avg_launch_us": 1e3 * k1_ms, "alg_bytes": k1_bytes, "GBps": k1_ach, "frac": k1_ach / peak},
-                    "K2_gather_update": {"avg_launch_us": 1e3 * k2_ms, "alg_bytes": k2_bytes, "GBps": k2_ach,
-                                         "frac": k2_ach / peak},
-                    "ax_local": {"avg_launch_us": 1e3 * ax_ms, "alg_bytes": AX_BYTES[pol] * NL,
+                    "phaseA_ax": {"avg_us": 1e3 * k1_ms, "alg_bytes": k1_bytes, "GBps": k1_ach, "frac": k1_ach / peak},
+                    "phaseB_gather_update": {"avg_us": 1e3 * k2_ms, "alg_bytes": k2_bytes, "GBps": k2_ach,
+                                             "frac": k2_ach / peak},
+                    "ax_local": {"avg_us": 1e3 * ax_ms, "alg_bytes": AX_BYTES[pol] * NL,
                                  "GBps": AX_BYTES[pol] * NL / (ax_ms * 1e-3) / 1e9,
                                  "frac": AX_BYTES[pol] * NL / (ax_ms * 1e-3) / 1e9 / peak},
-                    "dssum_csr": {"avg_launch_us": 1e3 * gs_ms, "alg_bytes": gs_bytes,
+                    "dssum_csr": {"avg_us": 1e3 * gs_ms, "alg_bytes": gs_bytes,
                                   "GBps": gs_bytes / (gs_ms * 1e-3) / 1e9,
                                   "frac": gs_bytes / (gs_ms * 1e-3) / 1e9 / peak}},
                 "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": NL * vs, "d2h_bytes_per_step": NL * vs},

@@ -61,14 +61,18 @@ template <typename T, int N> struct AxCfg {
     static constexpr int OFF_D = ((N3 * (int)sizeof(T) + 15) / 16) * 16;
     static constexpr int SLOT = ((OFF_D + N3 * 8 + 15) / 16) * 16;
     static constexpr int SMEM_B = EPB * SLOT + 2 * EPB * N2 * (int)sizeof(T);
-    static constexpr int SMEM = SMEM_A > SMEM_B ? SMEM_A : SMEM_B;
+    // phase B (streamed pencils, NB_BV 2): per-thread staging slot for r and dinv
+    static constexpr int SLOTP = ((N * (int)sizeof(T) + 15) / 16) * 16 + ((N * 8 + 15) / 16) * 16;
+    static constexpr int SMEM_P = NT * SLOTP;
+    static constexpr int SMEM_AB = SMEM_A > SMEM_B ? SMEM_A : SMEM_B;
+    static constexpr int SMEM = SMEM_AB > SMEM_P ? SMEM_AB : SMEM_P;
     // resident blocks per SM the register allocation must allow (launch bound); fp64 pencils
     // need twice the registers
 #ifndef NB_MINB_MODE
 #define NB_MINB_MODE 3
 #endif
     static constexpr int MINB = NB_MINB_MODE == 0 ? 1
-                              : NB_MINB_MODE == 3 ? ((sizeof(T) == 4) ? (NT <= 128 ? 4 : 2) : 1)
+                              : NB_MINB_MODE == 3 ? ((sizeof(T) == 4) ? (NT <= 128 ? 4 : 2) : (N <= 8 ? 1 : 2))
                               : NB_MINB_MODE == 1 ? ((sizeof(T) == 4) ? ((NT <= 128) ? 8 : (NT <= 256 ? 4 : 2)) : ((NT <= 128) ? 4 : 2))
                                                   : ((sizeof(T) == 4) ? ((NT <= 128) ? 6 : (NT <= 256 ? 3 : 1)) : 1);
 };
@@ -98,11 +102,17 @@ __device__ __forceinline__ void st_chunk(T *__restrict__ p, const T (&d)[V])
 // need no barrier in between (phase 1 of the next group touches only the caller's own
 // r-pencil slots, which only the caller read in phase 5).
 // Variants kept for A/B measurement (tools/var_run.sh); defaults are the measured best:
-// NB_AXV 0: w_r^T in registers, pap = sum w p (p from shared); 1: energy form, w_r^T via shared.
+// NB_AXV32 / NB_AXV64 (phase-A step 3 for 4- / 8-byte data): 0: w_r^T in registers, pap =
+//   sum w p (p from shared); 1: energy-form pap, w_r^T via shared; 2: register-lean, the
+//   geometric factors streamed chunk by chunk through a non-unrolled loop.
 // NB_BV  0: phase B streams pencils per thread (no block barriers); 1: element groups with a
-//           shared-memory x-partner exchange and cp.async staging of r / dinv.
-#ifndef NB_AXV
-#define NB_AXV 0
+//           shared-memory x-partner exchange and cp.async staging of r / dinv; 2: streamed
+//           pencils with r / dinv staged through a per-thread shared slot (cp.async).
+#ifndef NB_AXV32
+#define NB_AXV32 0
+#endif
+#ifndef NB_AXV64
+#define NB_AXV64 2
 #endif
 #ifndef NB_BV
 #define NB_BV 0
@@ -122,6 +132,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
     using TS = typename Pol<PREC>::TS;
     using C = AxCfg<TV, N>;
     constexpr int V = VecW<TV, N>::V;
+    constexpr int AXV = sizeof(TV) == 8 ? NB_AXV64 : NB_AXV32;
     TV *A1 = S0 + C::ESZ;
     TV *A2 = A1 + C::ESZ;
     const int q = a + N * b;
@@ -166,7 +177,8 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
     }
     __syncthreads();
-#if NB_AXV == 0
+    TS acc = 0;
+    if constexpr (AXV == 0) {
     // ---- 3. ur in registers; geometric factors (C-7); r-part of local_grad3_t
     TV wrt[N];
     if (active) {
@@ -217,7 +229,6 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
     }
     __syncthreads();
     // ---- 5. w = (w_r + w_s) + w_t, Dirichlet mask, store; CG: pap partial (p from S0)
-    TS acc = 0;
     if (active) {
         TV out[N];
         {
@@ -250,13 +261,12 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         }
         st_pencil<TV, N>(w + gbase, out);
     }
-#else
+    } else if constexpr (AXV == 1) {
     // ---- 3. ur in registers; geometric factors (C-7); r-part of local_grad3_t.
     // CG (MODE 1): pap = p^T A_L p accumulated here in its energy form
     // sum_nodes (ur, us, ut) . G (ur, us, ut) = sum (ur wr + us ws + ut wt) -- identical to
     // sum_l p_l (A_L p)_l = glsc3(w, c, p) for continuous p vanishing on the Dirichlet nodes,
     // a sum of non-negative terms (G is SPD), and needs neither p nor w afterwards.
-    TS acc = 0;
     if (active) {
         TV wr[N];
         {
@@ -336,7 +346,93 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         }
         st_pencil<TV, N>(w + gbase, out);
     }
-#endif
+    } else {
+    // ---- 3. (register-lean) ur to the owner's S0 slots; the geometric factors streamed in
+    // chunks of V values (loop not unrolled: one chunk of operands live at a time); pap in
+    // energy form (MODE 1); w_r^T back into S0.
+    if (active) {
+        {
+            TV v[N], o[N];
+            ld_pencil<TV, N>(S0 + rp, v);
+            contract<TV, N>(D, v, o);
+            st_pencil<TV, N>(S0 + rp, o);
+        }
+        const TV *ge = g + (size_t)e * 6 * C::N3 + (size_t)N * q;
+#pragma unroll 1
+        for (int c = 0; c < N / V; c++) {
+            TV g1[V], g2[V], g3[V], g4[V], g5[V], g6[V], ur[V], us[V], ut[V], wr[V], ws[V], wt[V];
+            ld_chunk<TV, V>(ge + 0 * C::N3 + c * V, g1);
+            ld_chunk<TV, V>(ge + 1 * C::N3 + c * V, g2);
+            ld_chunk<TV, V>(ge + 2 * C::N3 + c * V, g3);
+            ld_chunk<TV, V>(ge + 3 * C::N3 + c * V, g4);
+            ld_chunk<TV, V>(ge + 4 * C::N3 + c * V, g5);
+            ld_chunk<TV, V>(ge + 5 * C::N3 + c * V, g6);
+            ld_chunk<TV, V>(S0 + rp + c * V, ur);
+            ld_chunk<TV, V>(A1 + rp + c * V, us);
+            ld_chunk<TV, V>(A2 + rp + c * V, ut);
+#pragma unroll
+            for (int t = 0; t < V; t++) {
+                wr[t] = fma(g3[t], ut[t], fma(g2[t], us[t], g1[t] * ur[t]));
+                ws[t] = fma(g5[t], ut[t], fma(g4[t], us[t], g2[t] * ur[t]));
+                wt[t] = fma(g6[t], ut[t], fma(g5[t], us[t], g3[t] * ur[t]));
+                if (MODE == 1) acc += ((TS)ur[t] * (TS)wr[t] + (TS)us[t] * (TS)ws[t]) + (TS)ut[t] * (TS)wt[t];
+            }
+            st_chunk<TV, V>(S0 + rp + c * V, wr);
+            st_chunk<TV, V>(A1 + rp + c * V, ws);
+            st_chunk<TV, V>(A2 + rp + c * V, wt);
+        }
+        {
+            TV v[N], o[N];
+            ld_pencil<TV, N>(S0 + rp, v);
+            contract_t<TV, N>(D, v, o);
+            st_pencil<TV, N>(S0 + rp, o);
+        }
+    }
+    __syncthreads();
+    // ---- 4. s- and t-parts of local_grad3_t, in place on the owner's pencils
+    if (active) {
+        TV v[N], o[N];
+#pragma unroll
+        for (int j = 0; j < N; j++) v[j] = A1[sp + N * j];
+        contract_t<TV, N>(D, v, o);
+#pragma unroll
+        for (int j = 0; j < N; j++) A1[sp + N * j] = o[j];
+#pragma unroll
+        for (int k = 0; k < N; k++) v[k] = A2[tp + C::P * k];
+        contract_t<TV, N>(D, v, o);
+#pragma unroll
+        for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
+    }
+    __syncthreads();
+    // ---- 5. w = (w_r + w_s) + w_t, Dirichlet mask, store
+    if (active) {
+        TV out[N];
+        {
+            TV t0[N], t1[N], t2[N];
+            ld_pencil<TV, N>(S0 + rp, t0);
+            ld_pencil<TV, N>(A1 + rp, t1);
+            ld_pencil<TV, N>(A2 + rp, t2);
+#pragma unroll
+            for (int i = 0; i < N; i++) out[i] = (t0[i] + t1[i]) + t2[i];
+        }
+        if (MODE != 0 || apply_mask) {
+            const ElemPos P = elem_pos(m, e);
+            const bool mjk = axis_bnd(a, N, P.ey, m.nely) || axis_bnd(b, N, P.ez, m.nelz);
+#pragma unroll
+            for (int i = 0; i < N; i++)
+                if (mjk || axis_bnd(i, N, P.ex, m.nelx)) out[i] = TV(0);
+            if (MODE == 2) {   // unshared nodes only (c = 1); the CSR phase adds the shared ones
+                const bool sjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz) > 1;
+                TV pp[N];
+                ld_pencil<TV, N>(pv + gbase, pp);   // written by this thread in step 1
+#pragma unroll
+                for (int i = 0; i < N; i++)
+                    if (!sjk && axis_mult(i, N, P.ex, m.nelx) == 1) acc += (TS)out[i] * (TS)pp[i];
+            }
+        }
+        st_pencil<TV, N>(w + gbase, out);
+    }
+    }
     return acc;
 }
 
@@ -417,32 +513,47 @@ __device__ __forceinline__ void gather_pencil(const MeshDev &m, const typename P
         if (yz || (i == 0 && xl) || (i == N - 1 && xr)) ww[i] = (TV)s[i];
 }
 
-template <int PREC, int N, int GATHER>
+// STG: r and dinv are staged through this thread's private shared-memory slot `stg` with
+// cp.async (LDGSTS), so they are in flight during the gather without occupying registers.
+template <int PREC, int N, int GATHER, bool STG = false>
 __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ w,
                                            typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
                                            const typename Pol<PREC>::TJ *__restrict__ dinv,
                                            typename Pol<PREC>::TV alpha, int64_t pid, typename Pol<PREC>::TS &rtr,
-                                           typename Pol<PREC>::TS &rho)
+                                           typename Pol<PREC>::TS &rho, unsigned char *stg = nullptr)
 {
     using TV = typename Pol<PREC>::TV;
     using TJ = typename Pol<PREC>::TJ;
     using TS = typename Pol<PREC>::TS;
     constexpr int N2 = N * N;
+    constexpr int OFFD = ((N * (int)sizeof(TV) + 15) / 16) * 16;
     const int e = (int)(pid / N2);
     const int q = (int)(pid - (int64_t)e * N2);
     const int a = q % N, b = q / N;
     const size_t base = (size_t)pid * N;
-    const ElemPos P = elem_pos(m, e);
     TV ww[N], rr[N], zz[N];
     TJ dd[N];
+    if (STG) {
+        cp_pencil_async<TV, N>(reinterpret_cast<TV *>(stg), r + base);
+        cp_pencil_async<TJ, N>(reinterpret_cast<TJ *>(stg + OFFD), dinv + base);
+        cp_async_commit();
+    }
+    const ElemPos P = elem_pos(m, e);
     ld_pencil<TV, N, LD_CG>(w + base, ww);
-    ld_pencil<TV, N>(r + base, rr);
-    ld_pencil<TJ, N, LD_NC>(dinv + base, dd);
+    if (!STG) {
+        ld_pencil<TV, N>(r + base, rr);
+        ld_pencil<TJ, N, LD_NC>(dinv + base, dd);
+    }
     if (GATHER) {
         constexpr int N3 = N * N * N;
         const TV ol = P.ex > 0 ? __ldcg(w + base - N3 + (N - 1)) : TV(0);
         const TV orr = P.ex < m.nelx - 1 ? __ldcg(w + base + N3) : TV(0);
         gather_pencil<PREC, N>(m, w, e, P, a, b, ww, ol, orr);
+    }
+    if (STG) {
+        cp_async_wait_all();
+        ld_pencil<TV, N>(reinterpret_cast<const TV *>(stg), rr);
+        ld_pencil<TJ, N>(reinterpret_cast<const TJ *>(stg + OFFD), dd);
     }
     const int mjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz);
 #pragma unroll
@@ -611,33 +722,47 @@ __device__ __forceinline__ void grid_barrier(unsigned int *bar)
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned int gen = ld_acquire_u32(bar + 1);
-        __threadfence();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");   // this block's writes before the arrival
         const unsigned int prev = atomicAdd(bar, 1u);
         if (prev == gridDim.x - 1) {
             bar[0] = 0;
-            __threadfence();
-            st_release_u32(bar + 1, gen + 1);
+            st_release_u32(bar + 1, gen + 1);              // orders the reset before the release
         } else {
-            while (ld_acquire_u32(bar + 1) == gen) __nanosleep(32);
+            while (ld_acquire_u32(bar + 1) == gen) __nanosleep(20);
         }
-        __threadfence();
     }
     __syncthreads();
 }
 
-// every block: sum part[i*K + k] over all G blocks in a fixed order (same result everywhere)
-template <typename TS>
-__device__ __forceinline__ TS all_blocks_sum(const double *part, int G, int K, int k, TS *sh)
+// every block: sum part[i*K + k] over all G blocks in a fixed order (same result everywhere);
+// K values per block are summed in one pass (one L2 round trip)
+template <typename TS, int K>
+__device__ __forceinline__ void all_blocks_sum(const double *part, int G, TS (&out)[K], TS *sh)
 {
-    __shared__ TS bc;
-    TS s = 0;
-    for (int i = threadIdx.x; i < G; i += blockDim.x) s += (TS)__ldcg(part + (size_t)i * K + k);
-    s = block_sum<TS>(s, sh);
-    if (threadIdx.x == 0) bc = s;
+    __shared__ TS bc[K];
+    TS s[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) s[k] = 0;
+    for (int i = threadIdx.x; i < G; i += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < K; k++) s[k] += (TS)__ldcg(part + (size_t)i * K + k);
+    }
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        const TS t = block_sum<TS>(s[k], sh);
+        if (threadIdx.x == 0) bc[k] = t;
+    }
     __syncthreads();
-    const TS r = bc;
+#pragma unroll
+    for (int k = 0; k < K; k++) out[k] = bc[k];
     __syncthreads();
-    return r;
+}
+template <typename TS>
+__device__ __forceinline__ TS all_blocks_sum1(const double *part, int G, TS *sh)
+{
+    TS o[1];
+    all_blocks_sum<TS, 1>(part, G, o, sh);
+    return o[0];
 }
 
 template <int PREC, int N, int FUSED>
@@ -682,8 +807,9 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
     grid_barrier(A.bar);
     if (t0 && A.tim) A.tim[0] = globaltimer();
     {
-        const TS rtr0 = all_blocks_sum<TS>(A.partB, gridDim.x, 2, 0, sh);
-        const TS rho = all_blocks_sum<TS>(A.partB, gridDim.x, 2, 1, sh);
+        TS tot2[2];
+        all_blocks_sum<TS, 2>(A.partB, gridDim.x, tot2, sh);
+        const TS rtr0 = tot2[0], rho = tot2[1];
         if (tid == 0) {
             st.rtr0 = rtr0; st.rho = rho; st.rtr = rtr0; st.beta = 0; st.alpha = 0; st.pap = 0;
             st.it = 0; st.status = NB_MAXITER; st.pending = 0; st.done = 0;
@@ -715,7 +841,7 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
         }
         grid_barrier(A.bar);
         if (t0 && A.tim) A.tim[3 * st.it + 1] = globaltimer();
-        TS pap = all_blocks_sum<TS>(A.partA, gridDim.x, 1, 0, sh);
+        TS pap = all_blocks_sum1<TS>(A.partA, gridDim.x, sh);
         if (!FUSED) {
             // ---- CSR gather-scatter phase: per-copy (or consistent) QQ^T, shared pap partial
             const int64_t s0 = split(A.nseg, gridDim.x, blockIdx.x), s1 = split(A.nseg, gridDim.x, blockIdx.x + 1);
@@ -731,7 +857,7 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
             acc2 = block_sum<TS>(acc2, sh);
             if (tid == 0) A.partS[blockIdx.x] = (double)acc2;
             grid_barrier(A.bar);
-            pap = pap + all_blocks_sum<TS>(A.partS, gridDim.x, 1, 0, sh);
+            pap = pap + all_blocks_sum1<TS>(A.partS, gridDim.x, sh);
         }
         if (t0 && A.tim) A.tim[3 * st.it + 2] = globaltimer();
         if (tid == 0) {
@@ -764,10 +890,11 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
 #else
             (void)e_end;
             const int64_t p1 = (int64_t)e_end * C::N2;
+            unsigned char *slot = smraw + (size_t)tid * C::SLOTP;
 #pragma unroll 1
             for (int64_t pid = NB_G0 * C::EPB * C::N2 + tid; pid < p1; pid += blockDim.x)
-                upd_pencil<PREC, N, FUSED>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, (const TJ *)A.dinv, av, pid,
-                                           prtr, prho);
+                upd_pencil<PREC, N, FUSED, NB_BV == 2>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, (const TJ *)A.dinv,
+                                                       av, pid, prtr, prho, slot);
 #endif
             prtr = block_sum<TS>(prtr, sh);
             prho = block_sum<TS>(prho, sh);
@@ -775,8 +902,9 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
         }
         grid_barrier(A.bar);
         {
-            const TS rtr = all_blocks_sum<TS>(A.partB, gridDim.x, 2, 0, sh);
-            const TS rho_new = all_blocks_sum<TS>(A.partB, gridDim.x, 2, 1, sh);
+            TS tot2[2];
+            all_blocks_sum<TS, 2>(A.partB, gridDim.x, tot2, sh);
+            const TS rtr = tot2[0], rho_new = tot2[1];
             if (tid == 0) {
                 const int it = st.it + 1;
                 const double res = sqrt((double)rtr / (double)st.rtr0);

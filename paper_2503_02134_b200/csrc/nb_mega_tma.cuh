@@ -307,8 +307,9 @@ k_cg_mega_tma(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<t
     grid_barrier(A.bar);
     if (t0 && A.tim) A.tim[0] = globaltimer();
     {
-        const TS rtr0 = all_blocks_sum<TS>(A.partB, gridDim.x, 2, 0, sh);
-        const TS rho = all_blocks_sum<TS>(A.partB, gridDim.x, 2, 1, sh);
+        TS tot2[2];
+        all_blocks_sum<TS, 2>(A.partB, gridDim.x, tot2, sh);
+        const TS rtr0 = tot2[0], rho = tot2[1];
         if (tid == 0) {
             st.rtr0 = rtr0; st.rho = rho; st.rtr = rtr0; st.beta = 0; st.alpha = 0; st.pap = 0;
             st.it = 0; st.status = NB_MAXITER; st.pending = 0; st.done = 0;
@@ -348,7 +349,7 @@ k_cg_mega_tma(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<t
         }
         grid_barrier(A.bar);
         if (t0 && A.tim) A.tim[3 * st.it + 1] = globaltimer();
-        TS pap = all_blocks_sum<TS>(A.partA, gridDim.x, 1, 0, sh);
+        TS pap = all_blocks_sum1<TS>(A.partA, gridDim.x, sh);
         if (!FUSED) {
             const int64_t s0 = split(A.nseg, gridDim.x, blockIdx.x), s1 = split(A.nseg, gridDim.x, blockIdx.x + 1);
             TS acc2 = 0;
@@ -364,7 +365,7 @@ k_cg_mega_tma(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<t
             acc2 = block_sum<TS>(acc2, sh);
             if (tid == 0) A.partS[blockIdx.x] = (double)acc2;
             grid_barrier(A.bar);
-            pap = pap + all_blocks_sum<TS>(A.partS, gridDim.x, 1, 0, sh);
+            pap = pap + all_blocks_sum1<TS>(A.partS, gridDim.x, sh);
         }
         if (t0 && A.tim) A.tim[3 * st.it + 2] = globaltimer();
         if (tid == 0) {
@@ -407,8 +408,9 @@ k_cg_mega_tma(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<t
         }
         grid_barrier(A.bar);
         {
-            const TS rtr = all_blocks_sum<TS>(A.partB, gridDim.x, 2, 0, sh);
-            const TS rho_new = all_blocks_sum<TS>(A.partB, gridDim.x, 2, 1, sh);
+            TS tot2[2];
+            all_blocks_sum<TS, 2>(A.partB, gridDim.x, tot2, sh);
+            const TS rtr = tot2[0], rho_new = tot2[1];
             if (tid == 0) {
                 const int it = st.it + 1;
                 const double res = sqrt((double)rtr / (double)st.rtr0);
