@@ -734,10 +734,38 @@ __device__ __forceinline__ void grid_barrier(unsigned int *bar)
     __syncthreads();
 }
 
-// every block: sum part[i*K + k] over all G blocks in a fixed order (same result everywhere);
-// K values per block are summed in one pass (one L2 round trip)
+// Megakernel grid barrier, thread 0 of each block, after a __syncthreads that ordered the
+// block's writes before it: one fire-and-forget release-add on a monotone arrival counter
+// (zeroed before the launch), then acquire-polls until all blocks of this epoch arrived.
+__device__ __forceinline__ void grid_arrive_wait(unsigned int *cnt, unsigned int target)
+{
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+    while ((int)(ld_acquire_u32(cnt) - target) < 0) {
+    }
+}
+
+// K values summed over the block in a fixed tree; result valid in thread 0 (sh: >= 32*K)
 template <typename TS, int K>
-__device__ __forceinline__ void all_blocks_sum(const double *part, int G, TS (&out)[K], TS *sh)
+__device__ __forceinline__ void block_reduce(TS (&v)[K], TS *sh)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int k = 0; k < K; k++) v[k] = warp_sum(v[k]);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; k++) sh[wid * K + k] = v[k];
+    }
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int k = 0; k < K; k++) v[k] = warp_sum(lane < nw ? sh[lane * K + k] : TS(0));
+    }
+}
+
+// every block: sum part[i*K + k] over all G blocks in a fixed order (bit-identical in every
+// block), one pass over the partials; result in every thread
+template <typename TS, int K>
+__device__ __forceinline__ void all_blocks_reduce(const double *part, int G, TS (&out)[K], TS *sh)
 {
     __shared__ TS bc[K];
     TS s[K];
@@ -747,14 +775,23 @@ __device__ __forceinline__ void all_blocks_sum(const double *part, int G, TS (&o
 #pragma unroll
         for (int k = 0; k < K; k++) s[k] += (TS)__ldcg(part + (size_t)i * K + k);
     }
+    block_reduce<TS, K>(s, sh);   // caller: sh free (a __syncthreads since its last use)
+    if (threadIdx.x == 0) {
 #pragma unroll
-    for (int k = 0; k < K; k++) {
-        const TS t = block_sum<TS>(s[k], sh);
-        if (threadIdx.x == 0) bc[k] = t;
+        for (int k = 0; k < K; k++) bc[k] = s[k];
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < K; k++) out[k] = bc[k];
+}
+
+// every block: sum part[i*K + k] over all G blocks in a fixed order (same result everywhere);
+// K values per block are summed in one pass (one L2 round trip)
+template <typename TS, int K>
+__device__ __forceinline__ void all_blocks_sum(const double *part, int G, TS (&out)[K], TS *sh)
+{
+    __syncthreads();
+    all_blocks_reduce<TS, K>(part, G, out, sh);
     __syncthreads();
 }
 template <typename TS>
@@ -774,7 +811,7 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
     using TS = typename Pol<PREC>::TS;
     using C = AxCfg<TV, N>;
     extern __shared__ __align__(16) unsigned char smraw[];
-    __shared__ TS sh[32];
+    __shared__ TS sh[64];
     // Solver state lives in shared memory, not registers: it is live across both phases,
     // and every register it held would be taken from the phases' pencils (occupancy).
     struct State {
@@ -784,33 +821,41 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
     __shared__ State st;
     const int tid = threadIdx.x;
     const bool t0 = (blockIdx.x == 0 && tid == 0);
+    unsigned int tgt = 0;   // grid-barrier arrival target (thread 0)
 #define NB_G0 split(((int64_t)A.m.E + C::EPB - 1) / C::EPB, gridDim.x, blockIdx.x)
 #define NB_G1 split(((int64_t)A.m.E + C::EPB - 1) / C::EPB, gridDim.x, blockIdx.x + 1)
 #define NB_EL (threadIdx.x / C::N2)
 #define NB_A ((threadIdx.x - NB_EL * C::N2) % N)
 #define NB_B ((threadIdx.x - NB_EL * C::N2) / N)
 #define NB_S0 (reinterpret_cast<TV *>(smraw) + (NB_EL < C::EPB ? NB_EL : 0) * 3 * C::ESZ)
+    // block partials -> grid barrier (thread 0) -> every block sums all partials in fixed order
+#define NB_GRID_REDUCE(K, VALS, PART, TOT)                                             \
+    do {                                                                                \
+        block_reduce<TS, K>(VALS, sh);                                                  \
+        if (tid == 0) {                                                                 \
+            _Pragma("unroll") for (int k_ = 0; k_ < K; k_++)                            \
+                (PART)[(size_t)blockIdx.x * K + k_] = (double)VALS[k_];                 \
+            tgt += gridDim.x;                                                           \
+            grid_arrive_wait(A.bar, tgt);                                               \
+        }                                                                               \
+        __syncthreads();                                                                \
+        all_blocks_reduce<TS, K>(PART, gridDim.x, TOT, sh);                             \
+    } while (0)
 
     // ---- prologue: r = b, x = p = 0, z = M^-1 r; rtr0, rho_1
     {
         const int64_t p0 = min((int64_t)A.m.E, NB_G0 * C::EPB) * C::N2;
         const int64_t p1 = min((int64_t)A.m.E, NB_G1 * C::EPB) * C::N2;
-        TS rtr = 0, rho = 0;
+        TS v[2] = {0, 0};
 #pragma unroll 1
         for (int64_t pid = p0 + tid; pid < p1; pid += blockDim.x)
             init_pencil<PREC, N>(A.m, (const TV *)A.b, (TV *)A.x, (TV *)A.p, (TV *)A.r, (TV *)A.z,
-                                 (const TJ *)A.dinv, pid, rtr, rho);
-        rtr = block_sum<TS>(rtr, sh);
-        rho = block_sum<TS>(rho, sh);
-        if (tid == 0) { A.partB[2 * blockIdx.x] = (double)rtr; A.partB[2 * blockIdx.x + 1] = (double)rho; }
-    }
-    grid_barrier(A.bar);
-    if (t0 && A.tim) A.tim[0] = globaltimer();
-    {
-        TS tot2[2];
-        all_blocks_sum<TS, 2>(A.partB, gridDim.x, tot2, sh);
-        const TS rtr0 = tot2[0], rho = tot2[1];
+                                 (const TJ *)A.dinv, pid, v[0], v[1]);
+        TS tot[2];
+        NB_GRID_REDUCE(2, v, A.partB, tot);
+        if (t0 && A.tim) A.tim[0] = globaltimer();
         if (tid == 0) {
+            const TS rtr0 = tot[0], rho = tot[1];
             st.rtr0 = rtr0; st.rho = rho; st.rtr = rtr0; st.beta = 0; st.alpha = 0; st.pap = 0;
             st.it = 0; st.status = NB_MAXITER; st.pending = 0; st.done = 0;
             if (rtr0 == (TS)0) { st.status = NB_CONVERGED; st.done = 1; }
@@ -824,40 +869,39 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
 #pragma unroll 1
     while (!st.done) {
         // ---- phase A: p update, deferred x update, w = mask A_L p, pap partial
+        TS pap;
         {
-            TS acc = 0;
+            TS v[1] = {0};
             const TV bv = (TV)st.beta, av = st.pending ? (TV)st.alpha : TV(0);
             const int64_t g1 = NB_G1;
 #pragma unroll 1
             for (int64_t gr = NB_G0; gr < g1; gr++) {
                 const int e = (int)(gr * C::EPB) + NB_EL;
                 const bool active = NB_EL < C::EPB && e < A.m.E;
-                acc += ax_group<PREC, N, FUSED ? 1 : 2>(A.m, D, (const TV *)A.z, (TV *)A.p, (TV *)A.x,
-                                                        (const TV *)A.g, (TV *)A.w, true, bv, av, e, active, NB_A,
-                                                        NB_B, NB_S0);
+                v[0] += ax_group<PREC, N, FUSED ? 1 : 2>(A.m, D, (const TV *)A.z, (TV *)A.p, (TV *)A.x,
+                                                         (const TV *)A.g, (TV *)A.w, true, bv, av, e, active, NB_A,
+                                                         NB_B, NB_S0);
             }
-            acc = block_sum<TS>(acc, sh);
-            if (tid == 0) A.partA[blockIdx.x] = (double)acc;
+            TS tot[1];
+            NB_GRID_REDUCE(1, v, A.partA, tot);
+            pap = tot[0];
         }
-        grid_barrier(A.bar);
         if (t0 && A.tim) A.tim[3 * st.it + 1] = globaltimer();
-        TS pap = all_blocks_sum1<TS>(A.partA, gridDim.x, sh);
         if (!FUSED) {
             // ---- CSR gather-scatter phase: per-copy (or consistent) QQ^T, shared pap partial
             const int64_t s0 = split(A.nseg, gridDim.x, blockIdx.x), s1 = split(A.nseg, gridDim.x, blockIdx.x + 1);
-            TS acc2 = 0;
+            TS v[1] = {0};
             for (int64_t s = s0 + tid; s < s1; s += blockDim.x) {
                 if (A.order == NB_GS_CONSISTENT)
-                    acc2 += gs_segment<PREC, NB_GS_CONSISTENT, 1, TV, typename Pol<PREC>::TG, LD_CG>(
+                    v[0] += gs_segment<PREC, NB_GS_CONSISTENT, 1, TV, typename Pol<PREC>::TG, LD_CG>(
                         (int32_t)s, A.gs_off, A.gs_idx, (TV *)A.w, (const TV *)A.p);
                 else
-                    acc2 += gs_segment<PREC, NB_GS_PER_COPY, 1, TV, typename Pol<PREC>::TG, LD_CG>(
+                    v[0] += gs_segment<PREC, NB_GS_PER_COPY, 1, TV, typename Pol<PREC>::TG, LD_CG>(
                         (int32_t)s, A.gs_off, A.gs_idx, (TV *)A.w, (const TV *)A.p);
             }
-            acc2 = block_sum<TS>(acc2, sh);
-            if (tid == 0) A.partS[blockIdx.x] = (double)acc2;
-            grid_barrier(A.bar);
-            pap = pap + all_blocks_sum1<TS>(A.partS, gridDim.x, sh);
+            TS tot[1];
+            NB_GRID_REDUCE(1, v, A.partS, tot);
+            pap = pap + tot[0];
         }
         if (t0 && A.tim) A.tim[3 * st.it + 2] = globaltimer();
         if (tid == 0) {
@@ -875,7 +919,7 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
         if (st.done) break;
         // ---- phase B: (gather) r -= alpha w, z = M^-1 r, rtr and rho partials
         {
-            TS prtr = 0, prho = 0;
+            TS v[2] = {0, 0};
             const TV av = (TV)st.alpha;
             const int64_t g1 = NB_G1;
             const int e_end = (int)min((int64_t)A.m.E, g1 * C::EPB);
@@ -885,27 +929,20 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
                 const int e = (int)(gr * C::EPB) + NB_EL;
                 const bool active = NB_EL < C::EPB && e < e_end;
                 upd_group<PREC, N, FUSED>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, (const TJ *)A.dinv, av, e,
-                                          active, NB_EL, NB_A, NB_B, e_end, smraw, prtr, prho);
+                                          active, NB_EL, NB_A, NB_B, e_end, smraw, v[0], v[1]);
             }
 #else
-            (void)e_end;
             const int64_t p1 = (int64_t)e_end * C::N2;
             unsigned char *slot = smraw + (size_t)tid * C::SLOTP;
 #pragma unroll 1
             for (int64_t pid = NB_G0 * C::EPB * C::N2 + tid; pid < p1; pid += blockDim.x)
                 upd_pencil<PREC, N, FUSED, NB_BV == 2>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, (const TJ *)A.dinv,
-                                                       av, pid, prtr, prho, slot);
+                                                       av, pid, v[0], v[1], slot);
 #endif
-            prtr = block_sum<TS>(prtr, sh);
-            prho = block_sum<TS>(prho, sh);
-            if (tid == 0) { A.partB[2 * blockIdx.x] = (double)prtr; A.partB[2 * blockIdx.x + 1] = (double)prho; }
-        }
-        grid_barrier(A.bar);
-        {
-            TS tot2[2];
-            all_blocks_sum<TS, 2>(A.partB, gridDim.x, tot2, sh);
-            const TS rtr = tot2[0], rho_new = tot2[1];
+            TS tot[2];
+            NB_GRID_REDUCE(2, v, A.partB, tot);
             if (tid == 0) {
+                const TS rtr = tot[0], rho_new = tot[1];
                 const int it = st.it + 1;
                 const double res = sqrt((double)rtr / (double)st.rtr0);
                 if (blockIdx.x == 0) {
@@ -938,6 +975,7 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
         s->rtr = (double)st.rtr; s->rtr0 = (double)st.rtr0; s->iter = st.it; s->status = st.status; s->done = 1;
         s->pending = 0;
     }
+#undef NB_GRID_REDUCE
 #undef NB_G0
 #undef NB_G1
 #undef NB_EL

@@ -543,6 +543,8 @@ cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int
     A.bar = ws.bar;
     A.scal = ws.scal;
     const bool fused = order == NB_GS_CONSISTENT && !h->cg_csr;
+    cudaError_t e = cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned int), st);   // barrier epoch 0
+    if (e != cudaSuccess) return e;
     if (fused) { NB_DISPATCH_N(h->n, return (mega_launch_t<PREC, NN, 1>(h, A, st))) }
     NB_DISPATCH_N(h->n, return (mega_launch_t<PREC, NN, 0>(h, A, st)))
 }
