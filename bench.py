@@ -65,7 +65,7 @@ class Clocks:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -112,24 +112,30 @@ def barrier_sync(world):
     torch.cuda.synchronize()
 
 
-def max_over_ranks(v, world):
+def _reduce(v, world, op, device):
     if world == 1:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=op)
     return float(t.item())
 
 
-def sum_over_ranks(v, world):
-    if world == 1:
-        return v
-    import torch
+def max_over_ranks(v, world, device="cuda"):
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    return _reduce(v, world, dist.ReduceOp.MAX if world > 1 else None, device)
+
+
+def sum_over_ranks(v, world, device="cuda"):
+    import torch.distributed as dist
+    return _reduce(v, world, dist.ReduceOp.SUM if world > 1 else None, device)
+
+
+def aggregate(dof_iters_local, t_local, world, device="cuda"):
+    """Whole-job throughput: DOF*iterations summed over ranks / the slowest rank's time."""
+    t_max = max_over_ranks(t_local, world, device)
+    return sum_over_ranks(float(dof_iters_local), world, device) / t_max, t_max
 
 
 # ---------------------------------------------------------------------------- CPU oracle legs
@@ -230,9 +236,7 @@ def run_ours(args):
     ck = clocks.stop()
     step_ms = [a.elapsed_time(b2) for a, b2 in ev]
     t_local = sum(step_ms) / 1e3
-    t_max = max_over_ranks(t_local, world)
-    dof_iter = sum_over_ranks(float(NL * sum(iters)), world)
-    value = dof_iter / t_max
+    value, t_max = aggregate(NL * sum(iters), t_local, world)
 
     # per-phase device time of the same solve: the megakernel's block 0 stamps %globaltimer after
     # every grid barrier (nb_cg_report k_ax_ms / k_upd_ms); graph driver: CUDA events per launch

@@ -1,0 +1,68 @@
+"""Command line: one Jacobi-PCG solve on the GPU, JSON report on stdout.
+
+    python -m paper_2503_02134_b200 solve --nel 16 16 16 --p 7 --policy mixed --rtol 1e-8
+    python -m paper_2503_02134_b200 solve --nel 16 16 16 --p 7 --policy fp32 --gs-order per_copy
+
+Exit codes follow SPEC.md's CLI contract (External Interfaces): 0 converged (or a fixed-iteration
+run that finished), 1 usage / setup error, 2 stagnated, 3 numeric breakdown.
+Every step runs in the CUDA library through include/nb.h; there is no CPU path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+
+POLICIES = {"fp64": 0, "fp32": 1, "mixed": 2}
+ORDERS = {"consistent": 0, "per_copy": 1}
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="python -m paper_2503_02134_b200")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    s = sub.add_parser("solve", help="Jacobi-PCG solve of the SEM Poisson problem on a box")
+    s.add_argument("--nel", type=int, nargs=3, default=[16, 16, 16], metavar=("NX", "NY", "NZ"))
+    s.add_argument("--p", type=int, default=7, help="polynomial order (1..15)")
+    s.add_argument("--deform", type=float, default=0.0, help="vertex deformation amplitude / element size")
+    s.add_argument("--seed", type=int, default=0)
+    s.add_argument("--policy", choices=list(POLICIES), default="mixed")
+    s.add_argument("--rtol", type=float, default=1e-8, help="0: run exactly --max-iter iterations")
+    s.add_argument("--max-iter", type=int, default=4000)
+    s.add_argument("--gs-order", choices=list(ORDERS), default="consistent")
+    s.add_argument("--rhs", choices=["uniform", "manufactured"], default="uniform")
+    s.add_argument("--noise", type=float, default=1e-3)
+    s.add_argument("--history", action="store_true", help="include the residual history")
+    try:
+        a = ap.parse_args(argv)
+    except SystemExit as e:
+        return 1 if e.code else 0
+    import paper_2503_02134_b200 as nb
+    try:
+        mesh = nb.Mesh(*a.nel, a.p, deform=a.deform, seed=a.seed)
+    except (nb.NbError, ValueError) as e:
+        print(json.dumps({"error": str(e)}), file=sys.stderr)
+        return 1
+    pol = POLICIES[a.policy]
+    kind = nb.NB_RHS_UNIFORM if a.rhs == "uniform" else nb.NB_RHS_MANUFACTURED
+    b = mesh.rhs(pol, kind, noise=a.noise, seed=a.seed)
+    x, r = mesh.cg(b, pol, max_iter=a.max_iter, rtol=a.rtol, gs_order=ORDERS[a.gs_order])
+    status = {nb.NB_CONVERGED: "converged", nb.NB_MAXITER: "max_iter", nb.NB_STAGNATED: "stagnated",
+              nb.NB_BROKEDOWN: "breakdown"}[r.status]
+    out = {"schema": "nb-run-report/1", "nel": a.nel, "p": a.p, "deform": a.deform, "policy": a.policy,
+           "gs_order": a.gs_order, "rhs": a.rhs, "n_local": mesh.n_local, "iterations": r.iterations,
+           "status": status, "rel_res_final": r.rel_res_final, "rel_res_min": r.rel_res_min,
+           "solve_ms": r.solve_ms, "dof_iter_per_s": mesh.n_local * r.iterations / (r.solve_ms * 1e-3)
+           if r.solve_ms > 0 else None}
+    if a.history:
+        out["history"] = [float(v) for v in r.history]
+    print(json.dumps(out))
+    mesh.close()
+    if r.status == nb.NB_STAGNATED:
+        return 2
+    if r.status == nb.NB_BROKEDOWN:
+        return 3
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

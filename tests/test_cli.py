@@ -1,0 +1,40 @@
+"""CLI exit codes (SPEC.md External Interfaces: 0 converged, 1 usage/config, 2 stagnated, 3 breakdown)."""
+import json
+import subprocess
+import sys
+import os
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run(*args):
+    return subprocess.run([sys.executable, "-m", "paper_2503_02134_b200", *args], cwd=ROOT,
+                          capture_output=True, text=True, timeout=600)
+
+
+def test_usage_error_is_1():
+    assert run("solve", "--policy", "fp16").returncode == 1
+    assert run("nosuchcommand").returncode == 1
+
+
+@pytest.mark.gpu
+def test_converged_is_0():
+    r = run("solve", "--nel", "4", "4", "4", "--p", "7", "--policy", "mixed")
+    assert r.returncode == 0, r.stderr
+    rep = json.loads(r.stdout)
+    assert rep["status"] == "converged" and rep["rel_res_final"] <= 1e-8
+
+
+@pytest.mark.gpu
+def test_bad_order_is_1():
+    assert run("solve", "--nel", "2", "2", "2", "--p", "20").returncode == 1
+
+
+@pytest.mark.gpu
+def test_per_copy_fp32_stagnation_is_2():
+    r = run("solve", "--nel", "8", "8", "8", "--p", "7", "--policy", "fp32", "--gs-order", "per_copy",
+            "--max-iter", "1200")
+    assert r.returncode == 2, r.stdout
+    assert json.loads(r.stdout)["status"] == "stagnated"
