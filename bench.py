@@ -297,6 +297,30 @@ def run_ours(args):
                          "k2_alg_GBps": K2_BYTES[pp] * NL / (rk.k_upd_ms * 1e-3 / n_it) / 1e9}
         ttr["speedup_fp64_over_mixed_time"] = ttr["fp64"]["time_ms"] / ttr["mixed"]["time_ms"]
 
+    # HBM-bound companion point: configs[1]'s working set (~100 MB mixed) fits in the 126 MB L2,
+    # so its phase GB/s are not an HBM measurement.  configs[2] (32^3, p=9, deformed, 32.8M DOF,
+    # ~1.6 GB per mixed iteration) is: fixed 100 iterations, phase times from the same stamps.
+    large = None
+    if rank == 0 and not args.quick and not args.no_large:
+        lm = nb.Mesh(32, 32, 32, 9, deform=0.1, seed=0, device=dev)
+        lnl = lm.n_local
+        large = {"workload": "configs[2]: box 32x32x32 deformed 0.1, p=9, uniform RHS seed 0, 100 fixed iterations"}
+        for name, pp in (("mixed", POLICIES["mixed"]), ("fp64", POLICIES["fp64"])):
+            lb = lm.rhs(pp, nb.NB_RHS_UNIFORM, seed=0)
+            lx = lm.empty(pp)
+            nb.nb_cg(lm.h, lb, lx, pp, 100, 0.0, history=False)
+            flush.zero_()
+            r, _ = nb.nb_cg(lm.h, lb, lx, pp, 100, 0.0, history=False)
+            a_us, b_us = 1e3 * r.k_ax_ms / r.iterations, 1e3 * r.k_upd_ms / r.iterations
+            large[name] = {"us_per_iteration": 1e3 * r.solve_ms / r.iterations,
+                           "dof_iter_per_s": lnl * r.iterations / (r.solve_ms * 1e-3),
+                           "phaseA_us": a_us, "phaseA_GBps": K1_BYTES[pp] * lnl / (a_us * 1e-6) / 1e9,
+                           "phaseA_frac": K1_BYTES[pp] * lnl / (a_us * 1e-6) / 1e9 / load_peaks()[0],
+                           "phaseB_us": b_us, "phaseB_GBps": K2_BYTES[pp] * lnl / (b_us * 1e-6) / 1e9,
+                           "phaseB_frac": K2_BYTES[pp] * lnl / (b_us * 1e-6) / 1e9 / load_peaks()[0]}
+            del lb, lx
+        lm.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, dt, _, it, _ = oracle_sample(args.cpu_iters, args.policy)
@@ -337,7 +361,8 @@ def run_ours(args):
                                   "GBps": gs_bytes / (gs_ms * 1e-3) / 1e9,
                                   "frac": gs_bytes / (gs_ms * 1e-3) / 1e9 / peak}},
                 "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": NL * vs, "d2h_bytes_per_step": NL * vs},
-                "gpu_launches": launches, "clocks": ck, "cpu_baseline": cpu, "policies": ttr}
+                "gpu_launches": launches, "clocks": ck, "cpu_baseline": cpu, "policies": ttr,
+                "hbm_bound_companion": large}
         print(json.dumps(line), flush=True)
     mesh.close()
     if world > 1:
@@ -356,7 +381,8 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=60)
     ap.add_argument("--ref-iters", type=int, default=20)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--quick", action="store_true", help="skip the per-policy time-to-rtol table")
+    ap.add_argument("--quick", action="store_true", help="skip the per-policy table and the large companion")
+    ap.add_argument("--no-large", action="store_true", help="skip the HBM-bound configs[2] companion point")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -24,32 +24,74 @@ template <> struct Pol<NB_MIXED> { using TV = float; using TG = double; using TS
 // shared-memory or global traffic for D.
 // ---------------------------------------------------------------------------
 template <typename T, int N> struct DMat {
-    T d[N * N];   // d[i*N + j] = l_j'(x_i)
+    alignas(16) T d[N * N];    // d[i*N + j] = l_j'(x_i)
+    alignas(16) T dt[N * N];   // transpose: dt[j*N + i] = d[i*N + j] (column pairs adjacent)
 };
+
+#ifndef NB_FFMA2
+#define NB_FFMA2 1
+#endif
+// sm_100a packed fp32 FMA (FFMA2): two independent fma.rn.f32 in one instruction -- bit-identical
+// to two scalar FMAs.  Used for pairs of contraction outputs (o[i], o[i+1]).
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c)
+{
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ unsigned long long fmul2(unsigned long long a, unsigned long long b)
+{
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi)
+{
+    return ((unsigned long long)__float_as_uint(hi) << 32) | (unsigned long long)__float_as_uint(lo);
+}
+__device__ __forceinline__ float lo2(unsigned long long v) { return __uint_as_float((unsigned)(v & 0xffffffffull)); }
+__device__ __forceinline__ float hi2(unsigned long long v) { return __uint_as_float((unsigned)(v >> 32)); }
+
+// o[i] = sum_l M[i][l] v[l] with M given column-pair-adjacent (mt[l*N + i] = M[i][l]):
+// pairs of outputs with FFMA2 for fp32 (even N), scalar FMAs otherwise
+template <typename T, int N>
+__device__ __forceinline__ void contract_pairs(const T *__restrict__ mt, const T (&v)[N], T (&o)[N])
+{
+    if constexpr (sizeof(T) == 4 && N % 2 == 0 && NB_FFMA2) {
+        unsigned long long vv[N];
+#pragma unroll
+        for (int l = 0; l < N; l++) vv[l] = pack2(v[l], v[l]);
+#pragma unroll
+        for (int i = 0; i < N; i += 2) {
+            unsigned long long acc = fmul2(*reinterpret_cast<const unsigned long long *>(mt + i), vv[0]);
+#pragma unroll
+            for (int l = 1; l < N; l++)
+                acc = ffma2(*reinterpret_cast<const unsigned long long *>(mt + l * N + i), vv[l], acc);
+            o[i] = lo2(acc);
+            o[i + 1] = hi2(acc);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            T s = mt[i] * v[0];
+#pragma unroll
+            for (int l = 1; l < N; l++) s = fma(mt[l * N + i], v[l], s);
+            o[i] = s;
+        }
+    }
+}
 
 // o[i] = sum_l D[i][l] v[l]  (local_grad3 direction)
 template <typename T, int N>
 __device__ __forceinline__ void contract(const DMat<T, N> &D, const T (&v)[N], T (&o)[N])
 {
-#pragma unroll
-    for (int i = 0; i < N; i++) {
-        T s = D.d[i * N] * v[0];
-#pragma unroll
-        for (int l = 1; l < N; l++) s = fma(D.d[i * N + l], v[l], s);
-        o[i] = s;
-    }
+    contract_pairs<T, N>(D.dt, v, o);
 }
 // o[i] = sum_l D[l][i] v[l]  (local_grad3_t direction)
 template <typename T, int N>
 __device__ __forceinline__ void contract_t(const DMat<T, N> &D, const T (&v)[N], T (&o)[N])
 {
-#pragma unroll
-    for (int i = 0; i < N; i++) {
-        T s = D.d[i] * v[0];
-#pragma unroll
-        for (int l = 1; l < N; l++) s = fma(D.d[l * N + i], v[l], s);
-        o[i] = s;
-    }
+    contract_pairs<T, N>(D.d, v, o);
 }
 
 // ---------------------------------------------------------------------------
@@ -298,7 +340,11 @@ template <typename T, int N>
 inline DMat<T, N> make_dmat(const double *D)
 {
     DMat<T, N> m;
-    for (int i = 0; i < N * N; i++) m.d[i] = (T)D[i];
+    for (int i = 0; i < N; i++)
+        for (int j = 0; j < N; j++) {
+            m.d[i * N + j] = (T)D[i * N + j];
+            m.dt[j * N + i] = (T)D[i * N + j];
+        }
     return m;
 }
 
