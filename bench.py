@@ -54,41 +54,63 @@ def load_peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler for the timed region (clocks + throttle reasons)."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+    """nvidia-smi sampler (clocks + throttle reasons), started before the timed region and
+    filtered to the samples whose timestamps fall inside it."""
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                          "--format=csv,noheader,nounits", "-lms", "10"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.5)   # let the sampler come up before the timed region
         except Exception:
             self.proc = None
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def stop(self):
         if not self.proc:
             return None
+        if self.t1 is None:
+            self.t1 = time.time()
+        time.sleep(0.05)
         self.proc.terminate()
         try:
             out, _ = self.proc.communicate(timeout=5)
         except Exception:
             self.proc.kill()
             out = ""
-        rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 5]
-        if not rows:
+        import datetime
+        rows = []
+        for r in out.strip().splitlines():
+            f = [x.strip() for x in r.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                continue
+            rows.append((ts, f[1:]))
+        inside = [f for ts, f in rows if self.t0 - 0.01 <= ts <= self.t1 + 0.01] or [f for _, f in rows[-3:]]
+        if not inside:
             return None
-        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        sm = [float(f[0]) for f in inside if f[0].replace(".", "").isdigit()]
+        mx = [float(f[1]) for f in inside if f[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[2 + i] and "Not" not in r[2 + i]})
+        reasons = sorted({names[i] for f in inside for i in range(4) if "Active" in f[2 + i] and "Not" not in f[2 + i]})
         loaded = [s for s in sm if mx and s > 0.3 * max(mx)] or sm
         return {"sm_mhz": statistics.median(loaded) if loaded else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(inside),
+                "samples_total": len(rows)}
 
 
 def dist_init(n_gpus):
@@ -233,6 +255,7 @@ def run_ours(args):
         launches += rep.kernel_launches
         lib_ms.append(rep.solve_ms)
     barrier_sync(world)
+    clocks.mark_end()
     ck = clocks.stop()
     step_ms = [a.elapsed_time(b2) for a, b2 in ev]
     t_local = sum(step_ms) / 1e3
