@@ -68,6 +68,13 @@ template <typename T, int N> struct AxCfg {
     static constexpr int SMEM = SMEM_AB > SMEM_P ? SMEM_AB : SMEM_P;
     // resident blocks per SM the register allocation must allow (launch bound); fp64 pencils
     // need twice the registers
+// Phase-B loads of w (own pencil, neighbour copies): w was written by other blocks in phase A,
+// before the grid barrier whose acquire (ld.acquire.gpu) invalidates this SM's L1
+// (CCTL.IVALL), so L1-cached loads see the new values and x-/y-neighbour copies just loaded by
+// a neighbouring warp hit in L1.  NB_WLD = LD_CG keeps them L2-only.
+#ifndef NB_WLD
+#define NB_WLD LD_DEF
+#endif
 #ifndef NB_MINB_MODE
 #define NB_MINB_MODE 3
 #endif
@@ -465,19 +472,19 @@ __device__ __forceinline__ void gather_pencil(const MeshDev &m, const typename P
     const int64_t sy = (int64_t)ys * (m.nelx * (int64_t)N3) + (int64_t)(ys ? (N - 1 - 2 * a) : 0) * N;
     const int64_t sz = (int64_t)zs * ((int64_t)m.nelx * m.nely * N3) + (int64_t)(zs ? (N - 1 - 2 * b) : 0) * N2;
     if (ys) {
-        ld_pencil<TV, N, LD_CG>(w + base + sy, vy);
-        if (xl) ly = __ldcg(w + base + sy - N3 + (N - 1));
-        if (xr) ry = __ldcg(w + base + sy + N3);
+        ld_pencil<TV, N, NB_WLD>(w + base + sy, vy);
+        if (xl) ly = ldv<NB_WLD>(w + base + sy - N3 + (N - 1));
+        if (xr) ry = ldv<NB_WLD>(w + base + sy + N3);
     }
     if (zs) {
-        ld_pencil<TV, N, LD_CG>(w + base + sz, vz);
-        if (xl) lz = __ldcg(w + base + sz - N3 + (N - 1));
-        if (xr) rz = __ldcg(w + base + sz + N3);
+        ld_pencil<TV, N, NB_WLD>(w + base + sz, vz);
+        if (xl) lz = ldv<NB_WLD>(w + base + sz - N3 + (N - 1));
+        if (xr) rz = ldv<NB_WLD>(w + base + sz + N3);
     }
     if (ys && zs) {
-        ld_pencil<TV, N, LD_CG>(w + base + sy + sz, vyz);
-        if (xl) lyz = __ldcg(w + base + sy + sz - N3 + (N - 1));
-        if (xr) ryz = __ldcg(w + base + sy + sz + N3);
+        ld_pencil<TV, N, NB_WLD>(w + base + sy + sz, vyz);
+        if (xl) lyz = ldv<NB_WLD>(w + base + sy + sz - N3 + (N - 1));
+        if (xr) ryz = ldv<NB_WLD>(w + base + sy + sz + N3);
     }
     // ascending element order: lexicographic (dz, dy, dx); a negative offset comes first
     TG s[N];
@@ -539,15 +546,15 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
         cp_async_commit();
     }
     const ElemPos P = elem_pos(m, e);
-    ld_pencil<TV, N, LD_CG>(w + base, ww);
+    ld_pencil<TV, N, NB_WLD>(w + base, ww);
     if (!STG) {
         ld_pencil<TV, N>(r + base, rr);
         ld_pencil<TJ, N, LD_NC>(dinv + base, dd);
     }
     if (GATHER) {
         constexpr int N3 = N * N * N;
-        const TV ol = P.ex > 0 ? __ldcg(w + base - N3 + (N - 1)) : TV(0);
-        const TV orr = P.ex < m.nelx - 1 ? __ldcg(w + base + N3) : TV(0);
+        const TV ol = P.ex > 0 ? ldv<NB_WLD>(w + base - N3 + (N - 1)) : TV(0);
+        const TV orr = P.ex < m.nelx - 1 ? ldv<NB_WLD>(w + base + N3) : TV(0);
         gather_pencil<PREC, N>(m, w, e, P, a, b, ww, ol, orr);
     }
     if (STG) {
