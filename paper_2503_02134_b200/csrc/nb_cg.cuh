@@ -51,7 +51,25 @@ template <typename T, int N> struct AxCfg {
     static constexpr int BANKS = (sizeof(T) == 4) ? 32 : 16;
     // plane pitch P >= N^2 with P == N (mod BANKS): the stride-N s-pencil reads and the
     // stride-P t-pencil reads of a warp hit distinct banks.
-    static constexpr int P = N2 + (((N - N2) % BANKS) + BANKS) % BANKS;
+#ifndef NB_PADR
+#define NB_PADR 1
+#endif
+    // Shared-memory layout of one element array: index(i, j, k) = i + R j + P k.
+    // fp32, N = 8: row pitch R = 12 so the 16-byte r-pencil accesses of 8 consecutive threads
+    // (48-byte stride) hit 8 distinct 4-bank groups; P = 104 == 8 (mod 32) keeps the s-pencil
+    // reads conflict-free; t-pencils are then assigned transposed (thread (a,b) takes (i=b, j=a)),
+    // which makes them conflict-free too.  Otherwise R = N and P == N (mod banks).
+    // fp64, N = 8: R = 10 (80-byte stride: 5a mod 8 distinct 16-byte bank groups), P = 88 == 8
+    // (mod 16) for the half-warp s-pencil reads, t-pencils transposed.
+    // fp32 N = 10: R = 14, P = 140; fp64 N = 12: R = 14, P = 172, transposed t-pencils.
+    // (bank-conflict model and search: tools/smem_layout.py)
+    static constexpr int LAY = !NB_PADR ? 0
+                             : (N == 8) ? (sizeof(T) == 4 ? 1 : 2)
+                             : (N == 10 && sizeof(T) == 4) ? 3 : (N == 12 && sizeof(T) == 8) ? 4 : 0;
+    static constexpr int R = LAY == 1 ? 12 : LAY == 2 ? 10 : LAY == 3 ? 14 : LAY == 4 ? 14 : N;
+    static constexpr bool TT = LAY == 1 || LAY == 2 || LAY == 4;
+    static constexpr int P = LAY == 1 ? 104 : LAY == 2 ? 88 : LAY == 3 ? 140 : LAY == 4 ? 172
+                           : N2 + (((N - N2) % BANKS) + BANKS) % BANKS;
     static constexpr int ESZ = P * N;                          // one array, one element
     static constexpr int EPB = (N2 >= 256) ? 1 : (256 / N2);   // elements per group
     static constexpr int NT = ((EPB * N2 + 31) / 32) * 32;     // threads per block
@@ -143,9 +161,9 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
     TV *A1 = S0 + C::ESZ;
     TV *A2 = A1 + C::ESZ;
     const int q = a + N * b;
-    const int rp = N * a + C::P * b;   // r-pencil (i, a, b): contiguous
-    const int sp = a + C::P * b;       // s-pencil (a, j, b): stride N
-    const int tp = a + N * b;          // t-pencil (a, b, k): stride P
+    const int rp = C::R * a + C::P * b;   // r-pencil (i, a, b): contiguous
+    const int sp = a + C::P * b;       // s-pencil (a, j, b): stride R
+    const int tp = C::TT ? b + C::R * a : a + C::R * b;   // t-pencil: stride P
     const size_t gbase = (size_t)e * C::N3 + (size_t)N * q;
 
     // ---- 1. operand: u, or (CG) p = z + beta p_old with the deferred x update
@@ -173,10 +191,10 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
     if (active) {
         TV v[N], o[N];
 #pragma unroll
-        for (int j = 0; j < N; j++) v[j] = S0[sp + N * j];
+        for (int j = 0; j < N; j++) v[j] = S0[sp + C::R * j];
         contract<TV, N>(D, v, o);
 #pragma unroll
-        for (int j = 0; j < N; j++) A1[sp + N * j] = o[j];
+        for (int j = 0; j < N; j++) A1[sp + C::R * j] = o[j];
 #pragma unroll
         for (int k = 0; k < N; k++) v[k] = S0[tp + C::P * k];
         contract<TV, N>(D, v, o);
@@ -224,10 +242,10 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
     if (active) {
         TV v[N], o[N];
 #pragma unroll
-        for (int j = 0; j < N; j++) v[j] = A1[sp + N * j];
+        for (int j = 0; j < N; j++) v[j] = A1[sp + C::R * j];
         contract_t<TV, N>(D, v, o);
 #pragma unroll
-        for (int j = 0; j < N; j++) A1[sp + N * j] = o[j];
+        for (int j = 0; j < N; j++) A1[sp + C::R * j] = o[j];
 #pragma unroll
         for (int k = 0; k < N; k++) v[k] = A2[tp + C::P * k];
         contract_t<TV, N>(D, v, o);
@@ -314,10 +332,10 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
     if (active) {
         TV v[N], o[N];
 #pragma unroll
-        for (int j = 0; j < N; j++) v[j] = A1[sp + N * j];
+        for (int j = 0; j < N; j++) v[j] = A1[sp + C::R * j];
         contract_t<TV, N>(D, v, o);
 #pragma unroll
-        for (int j = 0; j < N; j++) A1[sp + N * j] = o[j];
+        for (int j = 0; j < N; j++) A1[sp + C::R * j] = o[j];
 #pragma unroll
         for (int k = 0; k < N; k++) v[k] = A2[tp + C::P * k];
         contract_t<TV, N>(D, v, o);
@@ -400,10 +418,10 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
     if (active) {
         TV v[N], o[N];
 #pragma unroll
-        for (int j = 0; j < N; j++) v[j] = A1[sp + N * j];
+        for (int j = 0; j < N; j++) v[j] = A1[sp + C::R * j];
         contract_t<TV, N>(D, v, o);
 #pragma unroll
-        for (int j = 0; j < N; j++) A1[sp + N * j] = o[j];
+        for (int j = 0; j < N; j++) A1[sp + C::R * j] = o[j];
 #pragma unroll
         for (int k = 0; k < N; k++) v[k] = A2[tp + C::P * k];
         contract_t<TV, N>(D, v, o);
