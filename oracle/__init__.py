@@ -25,7 +25,7 @@ _SRC = os.path.join(_HERE, "nb_oracle.c")
 _LIB = os.path.join(_HERE, "libnb_oracle.so")
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c99", "-Wall"]
 
-FP64, FP32, MIXED = 0, 1, 2
+FP64, FP32, MIXED, FP32_DOT2 = 0, 1, 2, 3
 GS_CONSISTENT, GS_PER_COPY = 0, 1
 RHS_UNIFORM, RHS_MANUFACTURED = 0, 1
 CONVERGED, MAXITER, STAGNATED, BREAKDOWN = 0, 1, 2, 3
@@ -84,6 +84,10 @@ def lib():
         L.or_glsc3_f_tree.argtypes = [P, P, P, C.c_int64]
         L.or_glsc3_f_seq.restype = C.c_float
         L.or_glsc3_f_seq.argtypes = [P, P, P, C.c_int64]
+        L.or_glsc3_f_dot2.restype = C.c_float
+        L.or_glsc3_f_dot2.argtypes = [P, P, P, C.c_int64]
+        L.or_two_sum_f.argtypes = [C.c_float, C.c_float, P, P]
+        L.or_two_prod_f.argtypes = [C.c_float, C.c_float, P, P]
         L.or_cg.argtypes = [P, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                             P, P, P, C.POINTER(_Report)]
         _lib = L
@@ -235,5 +239,17 @@ def glsc3(a, c, b, policy: int = FP64, seqdot: bool = False) -> float:
         c = np.ascontiguousarray(c, dtype=np.float64)
         return float(lib().or_glsc3_mixed(_p(a), _p(c), _p(b), n))
     a, c, b = (np.ascontiguousarray(v, dtype=np.float32) for v in (a, c, b))
-    fn = lib().or_glsc3_f_seq if seqdot else lib().or_glsc3_f_tree
+    fn = lib().or_glsc3_f_dot2 if policy == FP32_DOT2 else (lib().or_glsc3_f_seq if seqdot else lib().or_glsc3_f_tree)
     return float(fn(_p(a), _p(c), _p(b), n))
+
+
+def two_sum_f(a: float, b: float):
+    s, e = C.c_float(), C.c_float()
+    lib().or_two_sum_f(a, b, C.byref(s), C.byref(e))
+    return s.value, e.value
+
+
+def two_prod_f(a: float, b: float):
+    p, e = C.c_float(), C.c_float()
+    lib().or_two_prod_f(a, b, C.byref(p), C.byref(e))
+    return p.value, e.value

@@ -647,6 +647,41 @@ float or_glsc3_f_seq(const float *a, const float *c, const float *b, int64_t n)
     return s;
 }
 
+/* Error-free transformations in binary32 (Sec. 5.2.1; SPEC.md eft module).
+ * two_sum: Knuth's branch-free TwoSum, s = fl(a+b), s + e = a + b exactly.
+ * two_prod: p = fl(a*b), e = fma(a, b, -p), p + e = a*b exactly (fma-class hardware). */
+void or_two_sum_f(float a, float b, float *s, float *e)
+{
+    /* binary32 per operation: -ffp-contract=off, FLT_EVAL_METHOD 0 on x86-64 */
+    const float x = a + b;
+    const float bv = x - a;
+    const float av = x - bv;
+    *s = x;
+    *e = (a - av) + (b - bv);
+}
+void or_two_prod_f(float a, float b, float *p, float *e)
+{
+    const float x = a * b;
+    *p = x;
+    *e = fmaf(a, b, -x);
+}
+
+/* Dot2 (Ogita, Rump, Oishi 2005, Algorithm 5.3) of x_i = a_i c_i (exact: c_i = 2^-k) and b_i,
+ * sequential, in binary32: [p, s] = TwoProduct(x_1, y_1); for i >= 2: [h, r] = TwoProduct(x_i, y_i);
+ * [p, q] = TwoSum(p, h); s = s + (q + r); result fl(p + s). */
+float or_glsc3_f_dot2(const float *a, const float *c, const float *b, int64_t n)
+{
+    if (n <= 0) return 0.0f;
+    float p, s, h, r, q;
+    or_two_prod_f(a[0] * c[0], b[0], &p, &s);
+    for (int64_t i = 1; i < n; i++) {
+        or_two_prod_f(a[i] * c[i], b[i], &h, &r);
+        or_two_sum_f(p, h, &p, &q);
+        s = s + (q + r);
+    }
+    return p + s;
+}
+
 /* ------------------------------------------------------------------ */
 /* C-10 / C-11: PCG and the stagnation rule                             */
 /* ------------------------------------------------------------------ */
@@ -732,6 +767,7 @@ static int cg_f32(const or_mesh *m, int policy, int max_iter, double rtol, int o
 {
     const int64_t NL = m->NL;
     const int mixed = (policy == OR_MIXED);
+    const int dot2 = (policy == OR_FP32_DOT2);   /* fp32 policy with compensated dot products */
     float *x = (float *)malloc(NL * sizeof(float)), *r = (float *)malloc(NL * sizeof(float));
     float *p = (float *)malloc(NL * sizeof(float)), *z = (float *)malloc(NL * sizeof(float));
     float *w = (float *)malloc(NL * sizeof(float));
@@ -741,6 +777,7 @@ static int cg_f32(const or_mesh *m, int policy, int max_iter, double rtol, int o
 
     /* scalar recurrences: double under mixed, float under fp32 */
 #define DOT(a, b) (mixed ? or_glsc3_mixed((a), m->c, (b), NL) \
+                   : dot2 ? (double)or_glsc3_f_dot2((a), m->cf, (b), NL) \
                          : (double)(seqdot ? or_glsc3_f_seq((a), m->cf, (b), NL) : or_glsc3_f_tree((a), m->cf, (b), NL)))
     double rtr0 = DOT(r, r), rtr = rtr0;
     double rho = 0.0, rho_old = 1.0;
@@ -803,7 +840,7 @@ int or_cg(const or_mesh *m, int policy, int max_iter, double rtol, int gs_order,
           int seqdot, int x64, const double *b64, double *x_out, double *hist, or_report *rep)
 {
     if (!m || !b64 || !x_out || !rep || max_iter < 0 || rtol < 0.0) return 1;
-    if (policy < OR_FP64 || policy > OR_MIXED) return 1;
+    if (policy < OR_FP64 || policy > OR_FP32_DOT2) return 1;
     double *res = (double *)calloc((size_t)max_iter + 1, sizeof(double));
     int rc;
     if (policy == OR_FP64) rc = cg_fp64(m, max_iter, rtol, gs_order, stag_window, b64, x_out, res, rep);

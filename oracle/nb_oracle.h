@@ -20,7 +20,9 @@
 extern "C" {
 #endif
 
-enum { OR_FP64 = 0, OR_FP32 = 1, OR_MIXED = 2 };
+/* OR_FP32_DOT2: the fp32 policy with every glsc3 computed by the
+ * compensated Dot2 in binary32. */
+enum { OR_FP64 = 0, OR_FP32 = 1, OR_MIXED = 2, OR_FP32_DOT2 = 3 };
 enum { OR_GS_CONSISTENT = 0, OR_GS_PER_COPY = 1 };
 enum { OR_RHS_UNIFORM = 0, OR_RHS_MANUFACTURED = 1 };
 enum { OR_CONVERGED = 0, OR_MAXITER = 1, OR_STAGNATED = 2, OR_BREAKDOWN = 3 };
@@ -70,6 +72,10 @@ double or_glsc3_d(const double *a, const double *c, const double *b, int64_t n);
 double or_glsc3_mixed(const float *a, const double *c, const float *b, int64_t n);
 float or_glsc3_f_tree(const float *a, const float *c, const float *b, int64_t n);
 float or_glsc3_f_seq(const float *a, const float *c, const float *b, int64_t n);
+/* error-free transformations and the compensated Dot2 (binary32) */
+void or_two_sum_f(float a, float b, float *s, float *e);
+void or_two_prod_f(float a, float b, float *p, float *e);
+float or_glsc3_f_dot2(const float *a, const float *c, const float *b, int64_t n);
 
 /*
  * C-10 PCG.  b64: fp64 RHS (cast once to the policy precision).  x_out: n_local doubles
