@@ -17,9 +17,9 @@ import torch  # noqa: E402
 
 import paper_2503_02134_b200 as nb  # noqa: E402
 
-SV = {0: 8, 1: 4, 2: 4}
-SJ = {0: 8, 1: 4, 2: 8}
-POL = {"fp64": nb.NB_FP64, "fp32": nb.NB_FP32, "mixed": nb.NB_MIXED}
+SV = {0: 8, 1: 4, 2: 4, 3: 4}
+SJ = {0: 8, 1: 4, 2: 8, 3: 4}
+POL = {"fp64": nb.NB_FP64, "fp32": nb.NB_FP32, "mixed": nb.NB_MIXED, "fp32_dot2": nb.NB_FP32_DOT2}
 
 
 def parse(c):
@@ -36,7 +36,15 @@ def main():
     ap.add_argument("--policies", nargs="+", default=["fp64", "fp32", "mixed"])
     ap.add_argument("--iters", type=int, default=200)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--standalone", action="store_true", help="also time nb_ax (local) and nb_dssum")
+    ap.add_argument("--oracle-max-dof", type=float, default=0, help="time the CPU oracle (5 iterations) "
+                    "on points with at most this many local DOF")
+    ap.add_argument("--configs4", action="store_true", help="BASELINE configs[4]: cubes 10..50, p 7/9/11, "
+                    "undeformed and deformed")
     a = ap.parse_args()
+    if a.configs4:
+        a.cases = [f"{s}x{s}x{s}p{p}{d}" for p in (7, 9, 11) for s in (10, 13, 16, 20, 25, 32, 40, 50)
+                   for d in ("", "d")]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     for c in a.cases:
         nel, p, d = parse(c)
@@ -59,7 +67,34 @@ def main():
             kg = 1e3 * best.k_gs_ms / it
             b1 = (12 * SV[pol]) * NL
             b2 = (4 * SV[pol] + SJ[pol]) * NL
-            print(json.dumps({"case": c, "policy": name, "n_local": NL, "iters": it, "solve_ms": best.solve_ms,
+            extra = {}
+            if a.standalone:
+                st = torch.cuda.current_stream()
+                wv = m.empty(pol)
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                for what in ("ax", "dssum"):
+                    fn = (lambda: nb.nb_ax(m.h, pol, b, wv, nb.NB_AX_LOCAL)) if what == "ax" else \
+                         (lambda: nb.nb_dssum(m.h, pol, nb.NB_GS_CONSISTENT, wv))
+                    fn()
+                    ev0.record(st)
+                    for _ in range(10):
+                        fn()
+                    ev1.record(st)
+                    ev1.synchronize()
+                    us = 1e3 * ev0.elapsed_time(ev1) / 10
+                    byts = (8 * SV[pol]) * NL if what == "ax" else \
+                        m.info.n_shared_copies * (2 * SV[pol] + 4) + (m.info.n_shared_global + 1) * 4
+                    extra[what + "_us"] = us
+                    extra[what + "_GBps"] = byts / (us * 1e-6) / 1e9
+            if a.oracle_max_dof and NL <= a.oracle_max_dof:
+                import time
+                import oracle
+                o = oracle.Mesh(*nel, p, deform=d)
+                bo = o.rhs(seed=0)
+                t0 = time.perf_counter()
+                o.cg(bo, {"fp64": oracle.FP64, "fp32": oracle.FP32, "mixed": oracle.MIXED, "fp32_dot2": oracle.FP32_DOT2}[name], max_iter=5, rtol=0.0)
+                extra["oracle_dof_iter_per_s"] = NL * 5 / (time.perf_counter() - t0)
+            print(json.dumps({**extra, "case": c, "policy": name, "n_local": NL, "iters": it, "solve_ms": best.solve_ms,
                               "dof_iter_per_s": NL * it / (best.solve_ms * 1e-3),
                               "us_per_iter": 1e3 * best.solve_ms / it, "phaseA_us": k1, "phaseS_us": kg,
                               "phaseB_us": k2, "A_GBps": b1 / (k1 * 1e-6) / 1e9 if k1 else None,
