@@ -48,7 +48,11 @@ typedef struct nb_handle nb_handle;
  *   NB_MIXED: float data and float Ax arithmetic; gather-scatter accumulated in
  *             double and rounded once to float; Jacobi z = (float)((double)r * dinv64);
  *             glsc3 products and accumulation and the CG scalars in double. */
-typedef enum { NB_FP64 = 0, NB_FP32 = 1, NB_MIXED = 2 } nb_policy;
+/*   NB_FP32_DOT2: the NB_FP32 policy with every glsc3 (pap, rtr, rho) computed by the
+ *             compensated Dot2 (TwoProduct/TwoSum error-free transformations in binary32,
+ *             block and grid partials combined as expansions of size two) -- PAPER.md:434,
+ *             Sec. 5.2.1; SURVEY.md §8(f) NEXT-1.  For nb_rhs / nb_ax / nb_dssum it is NB_FP32. */
+typedef enum { NB_FP64 = 0, NB_FP32 = 1, NB_MIXED = 2, NB_FP32_DOT2 = 3 } nb_policy;
 
 /* Gather-scatter summation order:
  *   NB_GS_CONSISTENT: one sum per shared global node, copies ascending, written to all copies.

@@ -19,13 +19,13 @@ import numpy as np
 
 from ._build import LIB, build as _build_lib
 
-NB_FP64, NB_FP32, NB_MIXED = 0, 1, 2
+NB_FP64, NB_FP32, NB_MIXED, NB_FP32_DOT2 = 0, 1, 2, 3
 NB_GS_CONSISTENT, NB_GS_PER_COPY = 0, 1
 NB_RHS_UNIFORM, NB_RHS_MANUFACTURED = 0, 1
 NB_AX_LOCAL = 1
 NB_CONVERGED, NB_MAXITER, NB_STAGNATED, NB_BROKEDOWN = 0, 1, 2, 3
 NB_OK, NB_EINVAL, NB_ENOMEM, NB_ECUDA, NB_EGEOM, NB_EBREAKDOWN, NB_ESTATE = range(7)
-POLICY_NAMES = {NB_FP64: "fp64", NB_FP32: "fp32", NB_MIXED: "mixed"}
+POLICY_NAMES = {NB_FP64: "fp64", NB_FP32: "fp32", NB_MIXED: "mixed", NB_FP32_DOT2: "fp32_dot2"}
 
 EXPORTED = ["nb_setup", "nb_destroy", "nb_query", "nb_rhs", "nb_ax", "nb_dssum", "nb_cg", "nb_cg_host",
             "nb_export_maps", "nb_export_geom", "nb_export_basis", "nb_last_error", "nb_version"]

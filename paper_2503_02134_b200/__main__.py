@@ -13,7 +13,7 @@ import argparse
 import json
 import sys
 
-POLICIES = {"fp64": 0, "fp32": 1, "mixed": 2}
+POLICIES = {"fp64": 0, "fp32": 1, "mixed": 2, "fp32_dot2": 3}
 ORDERS = {"consistent": 0, "per_copy": 1}
 
 

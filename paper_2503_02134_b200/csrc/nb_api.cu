@@ -138,8 +138,10 @@ int ensure_f32(nb_handle *h)
 }
 
 // policy dispatch of the per-policy kernel templates
-#define NB_POL(prec, F, ...) \
-    ((prec) == NB_FP64 ? F<NB_FP64>(__VA_ARGS__) : (prec) == NB_FP32 ? F<NB_FP32>(__VA_ARGS__) : F<NB_MIXED>(__VA_ARGS__))
+#define NB_POL(prec, F, ...)                                                                       \
+    ((prec) == NB_FP64 ? F<NB_FP64>(__VA_ARGS__)                                                   \
+     : (prec) == NB_FP32 ? F<NB_FP32>(__VA_ARGS__)                                                 \
+     : (prec) == NB_MIXED ? F<NB_MIXED>(__VA_ARGS__) : F<NB_FP32_DOT2>(__VA_ARGS__))
 
 int ensure_ws(nb_handle *h, int prec, int32_t max_iter)
 {
@@ -157,7 +159,10 @@ int ensure_ws(nb_handle *h, int prec, int32_t max_iter)
         if (gg > maxblk) maxblk = gg;
         const int nchunk = (maxblk + 255) / 256;
         ws.mega_G = NB_POL(prec, nb::grid_mega, h);
-        const int nslots = 2 * maxblk > 4 * ws.mega_G ? 2 * maxblk : 4 * ws.mega_G;
+        // megakernel partials: 4 accumulators per block (pap, shared pap, rtr, rho), 2 doubles
+        // each for the Dot2 expansions (nb_mega_tma.cuh: launch_cg_mega)
+        const int mslots = (prec == NB_FP32_DOT2 ? 8 : 4) * ws.mega_G;
+        const int nslots = 2 * maxblk > mslots ? 2 * maxblk : mslots;
         NB_CU(cudaMalloc(&ws.red.part, sizeof(double) * nslots), "cudaMalloc part");
         NB_CU(cudaMalloc(&ws.bar, sizeof(unsigned int) * 2), "cudaMalloc bar");
         NB_CU(cudaMemset(ws.bar, 0, sizeof(unsigned int) * 2), "memset bar");
@@ -387,7 +392,8 @@ int nb_query(const nb_handle *h, nb_info *o)
 int nb_rhs(nb_handle *h, nb_rhs_kind kind, double noise_amp, uint64_t seed, nb_policy prec, void *b, void *stream)
 {
     if (!h) return fail(NB_EINVAL, "NULL handle");
-    if (prec < NB_FP64 || prec > NB_MIXED) return fail(NB_EINVAL, "bad policy");
+    if (prec < NB_FP64 || prec > NB_FP32_DOT2) return fail(NB_EINVAL, "bad policy");
+    if (prec == NB_FP32_DOT2) prec = NB_FP32;   // same vectors and arithmetic outside the dots
     if (kind != NB_RHS_UNIFORM && kind != NB_RHS_MANUFACTURED) return fail(NB_EINVAL, "bad rhs kind");
     NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
     int rc = check_dev_ptr(h, b, "b");
@@ -399,7 +405,8 @@ int nb_rhs(nb_handle *h, nb_rhs_kind kind, double noise_amp, uint64_t seed, nb_p
 int nb_ax(nb_handle *h, nb_policy prec, const void *u, void *w, uint32_t flags, void *stream)
 {
     if (!h) return fail(NB_EINVAL, "NULL handle");
-    if (prec < NB_FP64 || prec > NB_MIXED) return fail(NB_EINVAL, "bad policy");
+    if (prec < NB_FP64 || prec > NB_FP32_DOT2) return fail(NB_EINVAL, "bad policy");
+    if (prec == NB_FP32_DOT2) prec = NB_FP32;
     if (flags & ~NB_AX_LOCAL) return fail(NB_EINVAL, "unknown flags");
     NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
     int rc = check_dev_ptr(h, u, "u");
@@ -416,7 +423,8 @@ int nb_ax(nb_handle *h, nb_policy prec, const void *u, void *w, uint32_t flags, 
 int nb_dssum(nb_handle *h, nb_policy prec, nb_gs_order order, void *u, void *stream)
 {
     if (!h) return fail(NB_EINVAL, "NULL handle");
-    if (prec < NB_FP64 || prec > NB_MIXED) return fail(NB_EINVAL, "bad policy");
+    if (prec < NB_FP64 || prec > NB_FP32_DOT2) return fail(NB_EINVAL, "bad policy");
+    if (prec == NB_FP32_DOT2) prec = NB_FP32;
     if (order != NB_GS_CONSISTENT && order != NB_GS_PER_COPY) return fail(NB_EINVAL, "bad gs order");
     NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
     int rc = check_dev_ptr(h, u, "u");
@@ -555,7 +563,10 @@ static int cg_impl(nb_handle *h, const nb_cg_opts *o, const void *b, bool b_host
 static int cg_args(nb_handle *h, const nb_cg_opts *o)
 {
     if (!h || !o) return fail(NB_EINVAL, "NULL argument");
-    if (o->policy < NB_FP64 || o->policy > NB_MIXED) return fail(NB_EINVAL, "bad policy");
+    if (o->policy < NB_FP64 || o->policy > NB_FP32_DOT2) return fail(NB_EINVAL, "bad policy");
+    // the graph driver's last-block grid reduction carries one plain value per block
+    if (o->policy == NB_FP32_DOT2 && h->cg_graph)
+        return fail(NB_EINVAL, "the fp32+Dot2 policy runs on the megakernel driver only (unset NB_CG_DRIVER)");
     if (o->gs_order != NB_GS_CONSISTENT && o->gs_order != NB_GS_PER_COPY) return fail(NB_EINVAL, "bad gs order");
     if (o->max_iter < 0 || !(o->rtol >= 0.0)) return fail(NB_EINVAL, "bad max_iter/rtol");
     NB_CU(cudaSetDevice(h->device), "cudaSetDevice");

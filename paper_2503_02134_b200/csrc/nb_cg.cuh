@@ -73,17 +73,7 @@ template <typename T, int N> struct AxCfg {
     static constexpr int ESZ = P * N;                          // one array, one element
     static constexpr int EPB = (N2 >= 256) ? 1 : (256 / N2);   // elements per group
     static constexpr int NT = ((EPB * N2 + 31) / 32) * 32;     // threads per block
-    static constexpr int SMEM_A = 3 * EPB * ESZ * (int)sizeof(T);
-    // phase B staging per element: r (T), dinv (at most 8 B), 16-byte aligned; then the
-    // x-partner exchange (2 T per pencil)
-    static constexpr int OFF_D = ((N3 * (int)sizeof(T) + 15) / 16) * 16;
-    static constexpr int SLOT = ((OFF_D + N3 * 8 + 15) / 16) * 16;
-    static constexpr int SMEM_B = EPB * SLOT + 2 * EPB * N2 * (int)sizeof(T);
-    // phase B (streamed pencils, NB_BV 2): per-thread staging slot for r and dinv
-    static constexpr int SLOTP = ((N * (int)sizeof(T) + 15) / 16) * 16 + ((N * 8 + 15) / 16) * 16;
-    static constexpr int SMEM_P = NT * SLOTP;
-    static constexpr int SMEM_AB = SMEM_A > SMEM_B ? SMEM_A : SMEM_B;
-    static constexpr int SMEM = SMEM_AB > SMEM_P ? SMEM_AB : SMEM_P;
+    static constexpr int SMEM = 3 * EPB * ESZ * (int)sizeof(T);
     // resident blocks per SM the register allocation must allow (launch bound); fp64 pencils
     // need twice the registers
 // Phase-B loads of w (own pencil, neighbour copies): w was written by other blocks in phase A,
@@ -126,27 +116,21 @@ __device__ __forceinline__ void st_chunk(T *__restrict__ p, const T (&d)[V])
 // pap only.  Returns this thread's pap partial.  Contains 4 __syncthreads; consecutive calls
 // need no barrier in between (phase 1 of the next group touches only the caller's own
 // r-pencil slots, which only the caller read in phase 5).
-// Variants kept for A/B measurement (tools/var_run.sh); defaults are the measured best:
-// NB_AXV32 / NB_AXV64 (phase-A step 3 for 4- / 8-byte data): 0: w_r^T in registers, pap =
-//   sum w p (p from shared); 1: energy-form pap, w_r^T via shared; 2: register-lean, the
-//   geometric factors streamed chunk by chunk through a non-unrolled loop.
-// NB_BV  0: phase B streams pencils per thread (no block barriers); 1: element groups with a
-//           shared-memory x-partner exchange and cp.async staging of r / dinv; 2: streamed
-//           pencils with r / dinv staged through a per-thread shared slot (cp.async).
+// Phase-A step 3 variants (measured per data size, tools/var_run.sh): NB_AXV32 / NB_AXV64 for
+// 4- / 8-byte data.  0: w_r^T kept in registers, pap = sum w p (p from shared); 2: register-lean
+// (fp64 needs 255 registers otherwise): the geometric factors streamed chunk by chunk through a
+// non-unrolled loop, w_r^T via shared memory, pap in its energy form.
 #ifndef NB_AXV32
 #define NB_AXV32 0
 #endif
 #ifndef NB_AXV64
 #define NB_AXV64 2
 #endif
-#ifndef NB_BV
-#define NB_BV 0
-#endif
 #ifndef NB_PHASE_ATTR
 #define NB_PHASE_ATTR __forceinline__
 #endif
 template <int PREC, int N, int MODE>
-__device__ NB_PHASE_ATTR typename Pol<PREC>::TS
+__device__ NB_PHASE_ATTR Acc<PREC>
 ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typename Pol<PREC>::TV *__restrict__ in,
          typename Pol<PREC>::TV *__restrict__ pv, typename Pol<PREC>::TV *__restrict__ xv,
          const typename Pol<PREC>::TV *__restrict__ g, typename Pol<PREC>::TV *__restrict__ w, bool apply_mask,
@@ -202,7 +186,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
     }
     __syncthreads();
-    TS acc = 0;
+    Acc<PREC> acc;
     if constexpr (AXV == 0) {
     // ---- 3. ur in registers; geometric factors (C-7); r-part of local_grad3_t
     TV wrt[N];
@@ -275,99 +259,14 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
                 ld_pencil<TV, N>(S0 + rp, pp);
 #pragma unroll
                 for (int i = 0; i < N; i++)
-                    if (!sjk && axis_mult(i, N, P.ex, m.nelx) == 1) acc += (TS)out[i] * (TS)pp[i];
+                    if (!sjk && axis_mult(i, N, P.ex, m.nelx) == 1) acc.add((TS)out[i], (TS)pp[i]);
             }
         }
         if (MODE == 1) {
             TV pp[N];
             ld_pencil<TV, N>(S0 + rp, pp);
 #pragma unroll
-            for (int i = 0; i < N; i++) acc += (TS)out[i] * (TS)pp[i];
-        }
-        st_pencil<TV, N>(w + gbase, out);
-    }
-    } else if constexpr (AXV == 1) {
-    // ---- 3. ur in registers; geometric factors (C-7); r-part of local_grad3_t.
-    // CG (MODE 1): pap = p^T A_L p accumulated here in its energy form
-    // sum_nodes (ur, us, ut) . G (ur, us, ut) = sum (ur wr + us ws + ut wt) -- identical to
-    // sum_l p_l (A_L p)_l = glsc3(w, c, p) for continuous p vanishing on the Dirichlet nodes,
-    // a sum of non-negative terms (G is SPD), and needs neither p nor w afterwards.
-    if (active) {
-        TV wr[N];
-        {
-            TV v[N];
-            ld_pencil<TV, N>(S0 + rp, v);
-            contract<TV, N>(D, v, wr);   // ur (overwritten by wr below)
-        }
-        const TV *ge = g + (size_t)e * 6 * C::N3 + (size_t)N * q;
-#pragma unroll
-        for (int c = 0; c < N / V; c++) {
-            TV g1[V], g2[V], g3[V], g4[V], g5[V], g6[V], us[V], ut[V], ws[V], wt[V];
-            ld_chunk_h<TV, V, LD_CS>(ge + 0 * C::N3 + c * V, g1);
-            ld_chunk_h<TV, V, LD_CS>(ge + 1 * C::N3 + c * V, g2);
-            ld_chunk_h<TV, V, LD_CS>(ge + 2 * C::N3 + c * V, g3);
-            ld_chunk_h<TV, V, LD_CS>(ge + 3 * C::N3 + c * V, g4);
-            ld_chunk_h<TV, V, LD_CS>(ge + 4 * C::N3 + c * V, g5);
-            ld_chunk_h<TV, V, LD_CS>(ge + 5 * C::N3 + c * V, g6);
-            ld_chunk<TV, V>(A1 + rp + c * V, us);
-            ld_chunk<TV, V>(A2 + rp + c * V, ut);
-#pragma unroll
-            for (int t = 0; t < V; t++) {
-                const TV r_ = wr[c * V + t];
-                const TV wr_ = fma(g3[t], ut[t], fma(g2[t], us[t], g1[t] * r_));
-                ws[t] = fma(g5[t], ut[t], fma(g4[t], us[t], g2[t] * r_));
-                wt[t] = fma(g6[t], ut[t], fma(g5[t], us[t], g3[t] * r_));
-                if (MODE == 1) acc += ((TS)r_ * (TS)wr_ + (TS)us[t] * (TS)ws[t]) + (TS)ut[t] * (TS)wt[t];
-                wr[c * V + t] = wr_;
-            }
-            st_chunk<TV, V>(A1 + rp + c * V, ws);
-            st_chunk<TV, V>(A2 + rp + c * V, wt);
-        }
-        TV o[N];
-        contract_t<TV, N>(D, wr, o);
-        st_pencil<TV, N>(S0 + rp, o);    // own r-pencil slots: only this thread reads them again
-    }
-    __syncthreads();
-    // ---- 4. s- and t-parts of local_grad3_t, in place on the owner's pencils
-    if (active) {
-        TV v[N], o[N];
-#pragma unroll
-        for (int j = 0; j < N; j++) v[j] = A1[sp + C::R * j];
-        contract_t<TV, N>(D, v, o);
-#pragma unroll
-        for (int j = 0; j < N; j++) A1[sp + C::R * j] = o[j];
-#pragma unroll
-        for (int k = 0; k < N; k++) v[k] = A2[tp + C::P * k];
-        contract_t<TV, N>(D, v, o);
-#pragma unroll
-        for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
-    }
-    __syncthreads();
-    // ---- 5. w = (w_r + w_s) + w_t, Dirichlet mask, store
-    if (active) {
-        TV out[N];
-        {
-            TV t0[N], t1[N], t2[N];
-            ld_pencil<TV, N>(S0 + rp, t0);
-            ld_pencil<TV, N>(A1 + rp, t1);
-            ld_pencil<TV, N>(A2 + rp, t2);
-#pragma unroll
-            for (int i = 0; i < N; i++) out[i] = (t0[i] + t1[i]) + t2[i];
-        }
-        if (MODE != 0 || apply_mask) {
-            const ElemPos P = elem_pos(m, e);
-            const bool mjk = axis_bnd(a, N, P.ey, m.nely) || axis_bnd(b, N, P.ez, m.nelz);
-#pragma unroll
-            for (int i = 0; i < N; i++)
-                if (mjk || axis_bnd(i, N, P.ex, m.nelx)) out[i] = TV(0);
-            if (MODE == 2) {   // unshared nodes only (c = 1); the CSR phase adds the shared ones
-                const bool sjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz) > 1;
-                TV pp[N];
-                ld_pencil<TV, N>(pv + gbase, pp);   // written by this thread in step 1
-#pragma unroll
-                for (int i = 0; i < N; i++)
-                    if (!sjk && axis_mult(i, N, P.ex, m.nelx) == 1) acc += (TS)out[i] * (TS)pp[i];
-            }
+            for (int i = 0; i < N; i++) acc.add((TS)out[i], (TS)pp[i]);
         }
         st_pencil<TV, N>(w + gbase, out);
     }
@@ -400,7 +299,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
                 wr[t] = fma(g3[t], ut[t], fma(g2[t], us[t], g1[t] * ur[t]));
                 ws[t] = fma(g5[t], ut[t], fma(g4[t], us[t], g2[t] * ur[t]));
                 wt[t] = fma(g6[t], ut[t], fma(g5[t], us[t], g3[t] * ur[t]));
-                if (MODE == 1) acc += ((TS)ur[t] * (TS)wr[t] + (TS)us[t] * (TS)ws[t]) + (TS)ut[t] * (TS)wt[t];
+                if (MODE == 1) acc.add_sum(((TS)ur[t] * (TS)wr[t] + (TS)us[t] * (TS)ws[t]) + (TS)ut[t] * (TS)wt[t]);
             }
             st_chunk<TV, V>(S0 + rp + c * V, wr);
             st_chunk<TV, V>(A1 + rp + c * V, ws);
@@ -452,7 +351,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
                 ld_pencil<TV, N>(pv + gbase, pp);   // written by this thread in step 1
 #pragma unroll
                 for (int i = 0; i < N; i++)
-                    if (!sjk && axis_mult(i, N, P.ex, m.nelx) == 1) acc += (TS)out[i] * (TS)pp[i];
+                    if (!sjk && axis_mult(i, N, P.ex, m.nelx) == 1) acc.add((TS)out[i], (TS)pp[i]);
             }
         }
         st_pencil<TV, N>(w + gbase, out);
@@ -538,47 +437,31 @@ __device__ __forceinline__ void gather_pencil(const MeshDev &m, const typename P
         if (yz || (i == 0 && xl) || (i == N - 1 && xr)) ww[i] = (TV)s[i];
 }
 
-// STG: r and dinv are staged through this thread's private shared-memory slot `stg` with
-// cp.async (LDGSTS), so they are in flight during the gather without occupying registers.
-template <int PREC, int N, int GATHER, bool STG = false>
+template <int PREC, int N, int GATHER>
 __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ w,
                                            typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
                                            const typename Pol<PREC>::TJ *__restrict__ dinv,
-                                           typename Pol<PREC>::TV alpha, int64_t pid, typename Pol<PREC>::TS &rtr,
-                                           typename Pol<PREC>::TS &rho, unsigned char *stg = nullptr)
+                                           typename Pol<PREC>::TV alpha, int64_t pid, Acc<PREC> &rtr, Acc<PREC> &rho)
 {
     using TV = typename Pol<PREC>::TV;
     using TJ = typename Pol<PREC>::TJ;
     using TS = typename Pol<PREC>::TS;
     constexpr int N2 = N * N;
-    constexpr int OFFD = ((N * (int)sizeof(TV) + 15) / 16) * 16;
     const int e = (int)(pid / N2);
     const int q = (int)(pid - (int64_t)e * N2);
     const int a = q % N, b = q / N;
     const size_t base = (size_t)pid * N;
     TV ww[N], rr[N], zz[N];
     TJ dd[N];
-    if (STG) {
-        cp_pencil_async<TV, N>(reinterpret_cast<TV *>(stg), r + base);
-        cp_pencil_async<TJ, N>(reinterpret_cast<TJ *>(stg + OFFD), dinv + base);
-        cp_async_commit();
-    }
     const ElemPos P = elem_pos(m, e);
     ld_pencil<TV, N, NB_WLD>(w + base, ww);
-    if (!STG) {
-        ld_pencil<TV, N>(r + base, rr);
-        ld_pencil<TJ, N, LD_NC>(dinv + base, dd);
-    }
+    ld_pencil<TV, N>(r + base, rr);
+    ld_pencil<TJ, N, LD_NC>(dinv + base, dd);
     if (GATHER) {
         constexpr int N3 = N * N * N;
         const TV ol = P.ex > 0 ? ldv<NB_WLD>(w + base - N3 + (N - 1)) : TV(0);
         const TV orr = P.ex < m.nelx - 1 ? ldv<NB_WLD>(w + base + N3) : TV(0);
         gather_pencil<PREC, N>(m, w, e, P, a, b, ww, ol, orr);
-    }
-    if (STG) {
-        cp_async_wait_all();
-        ld_pencil<TV, N>(reinterpret_cast<const TV *>(stg), rr);
-        ld_pencil<TJ, N>(reinterpret_cast<const TJ *>(stg + OFFD), dd);
     }
     const int mjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz);
 #pragma unroll
@@ -587,79 +470,11 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
         zz[i] = (TV)((TJ)rr[i] * dd[i]);                     // solveM
         const TS c = (TS)1 / (TS)(mjk * axis_mult(i, N, P.ex, m.nelx));
         const TS rs = (TS)rr[i];
-        rtr += (rs * c) * rs;                                // glsc3(r, c, r)
-        rho += (rs * c) * (TS)zz[i];                         // glsc3(r, c, z)
+        rtr.add(rs * c, rs);                                 // glsc3(r, c, r)
+        rho.add(rs * c, (TS)zz[i]);                          // glsc3(r, c, z)
     }
     st_pencil<TV, N>(r + base, rr);
     st_pencil<TV, N>(z + base, zz);
-}
-
-// Phase B for one group of EPB elements with the phase-A thread mapping (all threads of the
-// block call it).  The x-partners of the own pencil come from the neighbouring element's
-// thread through shared memory when that element is in the same group (xch: EPB*N^2*2 TV).
-template <int PREC, int N, int GATHER>
-__device__ NB_PHASE_ATTR void upd_group(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ w,
-                                        typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
-                                        const typename Pol<PREC>::TJ *__restrict__ dinv,
-                                        typename Pol<PREC>::TV alpha, int e, bool active, int el, int a, int b,
-                                        int e_end, unsigned char *__restrict__ smem,
-                                        typename Pol<PREC>::TS &rtr, typename Pol<PREC>::TS &rho)
-{
-    using TV = typename Pol<PREC>::TV;
-    using TJ = typename Pol<PREC>::TJ;
-    using TS = typename Pol<PREC>::TS;
-    using C = AxCfg<TV, N>;
-    constexpr int N2 = N * N, N3 = N * N * N;
-    const int q = a + N * b;
-    const size_t base = ((size_t)e * N2 + q) * N;
-    // shared staging of this element slot: r [N^3] TV | dinv [N^3] TJ; then the x-partner exchange
-    TV *sr = reinterpret_cast<TV *>(smem + (size_t)(el < C::EPB ? el : 0) * C::SLOT);
-    TJ *sd = reinterpret_cast<TJ *>(reinterpret_cast<unsigned char *>(sr) + C::OFF_D);
-    TV *xch = reinterpret_cast<TV *>(smem + (size_t)C::EPB * C::SLOT);
-    TV ww[N];
-    ElemPos P;
-    if (active) {
-        // r and dinv go to shared memory asynchronously: not held in registers during the gather
-        cp_pencil_async<TV, N>(sr + q * N, r + base);
-        cp_pencil_async<TJ, N>(sd + q * N, dinv + base);
-        cp_async_commit();
-        ld_pencil<TV, N, LD_CG>(w + base, ww);
-        P = elem_pos(m, e);
-    }
-    if (GATHER) {
-        if (active) {
-            xch[2 * (el * N2 + q)] = ww[0];
-            xch[2 * (el * N2 + q) + 1] = ww[N - 1];
-        }
-        __syncthreads();
-        if (active) {
-            TV ol = 0, orr = 0;
-            if (P.ex > 0) ol = el > 0 ? xch[2 * ((el - 1) * N2 + q) + 1] : __ldcg(w + base - N3 + (N - 1));
-            if (P.ex < m.nelx - 1)
-                orr = (el + 1 < C::EPB && e + 1 < e_end) ? xch[2 * ((el + 1) * N2 + q)] : __ldcg(w + base + N3);
-            gather_pencil<PREC, N>(m, w, e, P, a, b, ww, ol, orr);
-        }
-        __syncthreads();
-    }
-    if (active) {
-        cp_async_wait_all();   // own copies only: no barrier needed
-        TV rr[N], zz[N];
-        TJ dd[N];
-        ld_pencil<TV, N>(sr + q * N, rr);
-        ld_pencil<TJ, N>(sd + q * N, dd);
-        const int mjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz);
-#pragma unroll
-        for (int i = 0; i < N; i++) {
-            rr[i] = fma(-alpha, ww[i], rr[i]);                   // add2s2(r, w, -alpha)
-            zz[i] = (TV)((TJ)rr[i] * dd[i]);                     // solveM
-            const TS c = (TS)1 / (TS)(mjk * axis_mult(i, N, P.ex, m.nelx));
-            const TS rs = (TS)rr[i];
-            rtr += (rs * c) * rs;                                // glsc3(r, c, r)
-            rho += (rs * c) * (TS)zz[i];                         // glsc3(r, c, z)
-        }
-        st_pencil<TV, N>(r + base, rr);
-        st_pencil<TV, N>(z + base, zz);
-    }
 }
 
 // CG prologue for one pencil: r = b, x = 0, p = 0, z = M^-1 r; rtr0 and rho_1 partials.
@@ -668,7 +483,7 @@ __device__ __forceinline__ void init_pencil(const MeshDev &m, const typename Pol
                                             typename Pol<PREC>::TV *__restrict__ x, typename Pol<PREC>::TV *__restrict__ pv,
                                             typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
                                             const typename Pol<PREC>::TJ *__restrict__ dinv, int64_t pid,
-                                            typename Pol<PREC>::TS &rtr, typename Pol<PREC>::TS &rho)
+                                            Acc<PREC> &rtr, Acc<PREC> &rho)
 {
     using TV = typename Pol<PREC>::TV;
     using TJ = typename Pol<PREC>::TJ;
@@ -690,8 +505,8 @@ __device__ __forceinline__ void init_pencil(const MeshDev &m, const typename Pol
         zz[i] = (TV)((TJ)rr[i] * dd[i]);
         const TS c = (TS)1 / (TS)(mjk * axis_mult(i, N, P.ex, m.nelx));
         const TS rs = (TS)rr[i];
-        rtr += (rs * c) * rs;
-        rho += (rs * c) * (TS)zz[i];
+        rtr.add(rs * c, rs);
+        rho.add(rs * c, (TS)zz[i]);
     }
     st_pencil<TV, N>(r + base, rr);
     st_pencil<TV, N>(z + base, zz);
@@ -810,6 +625,52 @@ __device__ __forceinline__ void all_blocks_reduce(const double *part, int G, TS 
     for (int k = 0; k < K; k++) out[k] = bc[k];
 }
 
+// Acc versions (dot-product accumulators, plain or Dot2 expansions): block tree, then every
+// block merges all blocks' stored partials in a fixed order; TOT = merged values (TS)
+template <int PREC, int K>
+__device__ __forceinline__ void block_reduce_acc(Acc<PREC> (&v)[K], Acc<PREC> *sh)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int k = 0; k < K; k++)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k].merge(v[k].shfl_down(o));
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; k++) sh[wid * K + k] = v[k];
+    }
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            Acc<PREC> t = lane < nw ? sh[lane * K + k] : Acc<PREC>();
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t.merge(t.shfl_down(o));
+            v[k] = t;
+        }
+    }
+}
+template <int PREC, int K>
+__device__ __forceinline__ void all_blocks_reduce_acc(const double *part, int G, typename Pol<PREC>::TS (&out)[K],
+                                                      Acc<PREC> *sh)
+{
+    using TS = typename Pol<PREC>::TS;
+    __shared__ TS bc[K];
+    Acc<PREC> s[K];
+    for (int i = threadIdx.x; i < G; i += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < K; k++) s[k].merge(Acc<PREC>::load(part + ((size_t)i * K + k) * Acc<PREC>::W));
+    }
+    block_reduce_acc<PREC, K>(s, sh);   // caller: sh free (a __syncthreads since its last use)
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; k++) bc[k] = s[k].value();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; k++) out[k] = bc[k];
+}
+
 // every block: sum part[i*K + k] over all G blocks in a fixed order (same result everywhere);
 // K values per block are summed in one pass (one L2 round trip)
 template <typename TS, int K>
@@ -836,7 +697,8 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
     using TS = typename Pol<PREC>::TS;
     using C = AxCfg<TV, N>;
     extern __shared__ __align__(16) unsigned char smraw[];
-    __shared__ TS sh[64];
+    __shared__ __align__(8) unsigned char acc_raw[64 * sizeof(Acc<PREC>)];   // no constructors in smem
+    Acc<PREC> *const acc_sh = reinterpret_cast<Acc<PREC> *>(acc_raw);
     // Solver state lives in shared memory, not registers: it is live across both phases,
     // and every register it held would be taken from the phases' pencils (occupancy).
     struct State {
@@ -856,22 +718,22 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
     // block partials -> grid barrier (thread 0) -> every block sums all partials in fixed order
 #define NB_GRID_REDUCE(K, VALS, PART, TOT)                                             \
     do {                                                                                \
-        block_reduce<TS, K>(VALS, sh);                                                  \
+        block_reduce_acc<PREC, K>(VALS, acc_sh);                                        \
         if (tid == 0) {                                                                 \
             _Pragma("unroll") for (int k_ = 0; k_ < K; k_++)                            \
-                (PART)[(size_t)blockIdx.x * K + k_] = (double)VALS[k_];                 \
+                VALS[k_].store((PART) + ((size_t)blockIdx.x * K + k_) * Acc<PREC>::W);  \
             tgt += gridDim.x;                                                           \
             grid_arrive_wait(A.bar, tgt);                                               \
         }                                                                               \
         __syncthreads();                                                                \
-        all_blocks_reduce<TS, K>(PART, gridDim.x, TOT, sh);                             \
+        all_blocks_reduce_acc<PREC, K>(PART, gridDim.x, TOT, acc_sh);                   \
     } while (0)
 
     // ---- prologue: r = b, x = p = 0, z = M^-1 r; rtr0, rho_1
     {
         const int64_t p0 = min((int64_t)A.m.E, NB_G0 * C::EPB) * C::N2;
         const int64_t p1 = min((int64_t)A.m.E, NB_G1 * C::EPB) * C::N2;
-        TS v[2] = {0, 0};
+        Acc<PREC> v[2];
 #pragma unroll 1
         for (int64_t pid = p0 + tid; pid < p1; pid += blockDim.x)
             init_pencil<PREC, N>(A.m, (const TV *)A.b, (TV *)A.x, (TV *)A.p, (TV *)A.r, (TV *)A.z,
@@ -896,16 +758,16 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
         // ---- phase A: p update, deferred x update, w = mask A_L p, pap partial
         TS pap;
         {
-            TS v[1] = {0};
+            Acc<PREC> v[1];
             const TV bv = (TV)st.beta, av = st.pending ? (TV)st.alpha : TV(0);
             const int64_t g1 = NB_G1;
 #pragma unroll 1
             for (int64_t gr = NB_G0; gr < g1; gr++) {
                 const int e = (int)(gr * C::EPB) + NB_EL;
                 const bool active = NB_EL < C::EPB && e < A.m.E;
-                v[0] += ax_group<PREC, N, FUSED ? 1 : 2>(A.m, D, (const TV *)A.z, (TV *)A.p, (TV *)A.x,
+                v[0].merge(ax_group<PREC, N, FUSED ? 1 : 2>(A.m, D, (const TV *)A.z, (TV *)A.p, (TV *)A.x,
                                                          (const TV *)A.g, (TV *)A.w, true, bv, av, e, active, NB_A,
-                                                         NB_B, NB_S0);
+                                                         NB_B, NB_S0));
             }
             TS tot[1];
             NB_GRID_REDUCE(1, v, A.partA, tot);
@@ -915,14 +777,14 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
         if (!FUSED) {
             // ---- CSR gather-scatter phase: per-copy (or consistent) QQ^T, shared pap partial
             const int64_t s0 = split(A.nseg, gridDim.x, blockIdx.x), s1 = split(A.nseg, gridDim.x, blockIdx.x + 1);
-            TS v[1] = {0};
+            Acc<PREC> v[1];
             for (int64_t s = s0 + tid; s < s1; s += blockDim.x) {
                 if (A.order == NB_GS_CONSISTENT)
-                    v[0] += gs_segment<PREC, NB_GS_CONSISTENT, 1, TV, typename Pol<PREC>::TG, LD_CG>(
-                        (int32_t)s, A.gs_off, A.gs_idx, (TV *)A.w, (const TV *)A.p);
+                    v[0].merge(gs_segment<PREC, NB_GS_CONSISTENT, 1, TV, typename Pol<PREC>::TG, LD_CG>(
+                        (int32_t)s, A.gs_off, A.gs_idx, (TV *)A.w, (const TV *)A.p));
                 else
-                    v[0] += gs_segment<PREC, NB_GS_PER_COPY, 1, TV, typename Pol<PREC>::TG, LD_CG>(
-                        (int32_t)s, A.gs_off, A.gs_idx, (TV *)A.w, (const TV *)A.p);
+                    v[0].merge(gs_segment<PREC, NB_GS_PER_COPY, 1, TV, typename Pol<PREC>::TG, LD_CG>(
+                        (int32_t)s, A.gs_off, A.gs_idx, (TV *)A.w, (const TV *)A.p));
             }
             TS tot[1];
             NB_GRID_REDUCE(1, v, A.partS, tot);
@@ -944,26 +806,15 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
         if (st.done) break;
         // ---- phase B: (gather) r -= alpha w, z = M^-1 r, rtr and rho partials
         {
-            TS v[2] = {0, 0};
+            Acc<PREC> v[2];
             const TV av = (TV)st.alpha;
             const int64_t g1 = NB_G1;
             const int e_end = (int)min((int64_t)A.m.E, g1 * C::EPB);
-#if NB_BV == 1
-#pragma unroll 1
-            for (int64_t gr = NB_G0; gr < g1; gr++) {
-                const int e = (int)(gr * C::EPB) + NB_EL;
-                const bool active = NB_EL < C::EPB && e < e_end;
-                upd_group<PREC, N, FUSED>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, (const TJ *)A.dinv, av, e,
-                                          active, NB_EL, NB_A, NB_B, e_end, smraw, v[0], v[1]);
-            }
-#else
             const int64_t p1 = (int64_t)e_end * C::N2;
-            unsigned char *slot = smraw + (size_t)tid * C::SLOTP;
 #pragma unroll 1
             for (int64_t pid = NB_G0 * C::EPB * C::N2 + tid; pid < p1; pid += blockDim.x)
-                upd_pencil<PREC, N, FUSED, NB_BV == 2>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, (const TJ *)A.dinv,
-                                                       av, pid, v[0], v[1], slot);
-#endif
+                upd_pencil<PREC, N, FUSED>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, (const TJ *)A.dinv, av, pid,
+                                           v[0], v[1]);
             TS tot[2];
             NB_GRID_REDUCE(2, v, A.partB, tot);
             if (tid == 0) {
@@ -1041,7 +892,8 @@ k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
     for (int64_t gr = g0; gr < g1; gr++) {
         const int e = (int)(gr * C::EPB) + el;
         const bool active = el < C::EPB && e < m.E;
-        acc += ax_group<PREC, N, MODE>(m, D, in, pv, xv, g, w, apply_mask != 0, beta, alpha, e, active, a, b, S0);
+        acc += ax_group<PREC, N, MODE>(m, D, in, pv, xv, g, w, apply_mask != 0, beta, alpha, e, active, a, b, S0)
+                   .value();
     }
     if (MODE == 0) return;
     __shared__ TS red[32];
@@ -1082,15 +934,15 @@ k_upd(const MeshDev m, const typename Pol<PREC>::TV *__restrict__ w, typename Po
         return;
     }
     const TV alpha = (TV)(TS)scal->alpha;
-    TS rtr = 0, rho = 0;
+    Acc<PREC> artr, arho;
     const int64_t np = (int64_t)m.E * N * N;
     const int64_t p0 = split(np, gridDim.x, blockIdx.x), p1 = split(np, gridDim.x, blockIdx.x + 1);
     for (int64_t pid = p0 + threadIdx.x; pid < p1; pid += UPD_NT)
-        upd_pencil<PREC, N, GATHER>(m, w, r, z, dinv, alpha, pid, rtr, rho);
+        upd_pencil<PREC, N, GATHER>(m, w, r, z, dinv, alpha, pid, artr, arho);
     __shared__ TS red[32];
     TS v[2];
-    v[0] = block_sum<TS>(rtr, red);
-    v[1] = block_sum<TS>(rho, red);
+    v[0] = block_sum<TS>(artr.value(), red);
+    v[1] = block_sum<TS>(arho.value(), red);
     TS tot[2];
     if (grid_reduce<TS, 2>(v, rw, tot) && threadIdx.x == 0) {
         const TS trtr = tot[0], trho = tot[1];
@@ -1126,15 +978,15 @@ k_init(const MeshDev m, const typename Pol<PREC>::TV *__restrict__ bvec, typenam
        Scal *__restrict__ scal, const RedWs rw, double *__restrict__ hist)
 {
     using TS = typename Pol<PREC>::TS;
-    TS rtr = 0, rho = 0;
+    Acc<PREC> artr, arho;
     const int64_t np = (int64_t)m.E * N * N;
     const int64_t p0 = split(np, gridDim.x, blockIdx.x), p1 = split(np, gridDim.x, blockIdx.x + 1);
     for (int64_t pid = p0 + threadIdx.x; pid < p1; pid += UPD_NT)
-        init_pencil<PREC, N>(m, bvec, x, pv, r, z, dinv, pid, rtr, rho);
+        init_pencil<PREC, N>(m, bvec, x, pv, r, z, dinv, pid, artr, arho);
     __shared__ TS red[32];
     TS v[2];
-    v[0] = block_sum<TS>(rtr, red);
-    v[1] = block_sum<TS>(rho, red);
+    v[0] = block_sum<TS>(artr.value(), red);
+    v[1] = block_sum<TS>(arho.value(), red);
     TS tot[2];
     if (grid_reduce<TS, 2>(v, rw, tot) && threadIdx.x == 0) {
         const TS trtr = tot[0], trho = tot[1];
@@ -1239,7 +1091,7 @@ cudaError_t launch_cg_init(const nb_handle *h, Workspace &ws, const void *b, cud
 {
     using TV = typename Pol<PREC>::TV;
     using TJ = typename Pol<PREC>::TJ;
-    const TJ *dinv = (const TJ *)(PREC == NB_FP32 ? (const void *)h->dinv32 : (const void *)h->dinv64);
+    const TJ *dinv = (const TJ *)(sizeof(TJ) == 4 ? (const void *)h->dinv32 : (const void *)h->dinv64);
     const int grid = grid_k2<PREC>(h);
     NB_DISPATCH_N(h->n, (k_init<PREC, NN><<<grid, UPD_NT, 0, st>>>(h->md(), (const TV *)b, (TV *)ws.x, (TV *)ws.p,
                                                                    (TV *)ws.r, (TV *)ws.z, dinv, ws.scal, ws.red,
@@ -1263,7 +1115,7 @@ cudaError_t launch_cg_k2(const nb_handle *h, Workspace &ws, bool gather, cudaStr
 {
     using TV = typename Pol<PREC>::TV;
     using TJ = typename Pol<PREC>::TJ;
-    const TJ *dinv = (const TJ *)(PREC == NB_FP32 ? (const void *)h->dinv32 : (const void *)h->dinv64);
+    const TJ *dinv = (const TJ *)(sizeof(TJ) == 4 ? (const void *)h->dinv32 : (const void *)h->dinv64);
     const int grid = grid_k2<PREC>(h);
     const int uc = use_cond ? 1 : 0;
     if (gather) {

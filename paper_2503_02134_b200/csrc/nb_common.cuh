@@ -16,6 +16,85 @@ template <int PREC> struct Pol;
 template <> struct Pol<NB_FP64> { using TV = double; using TG = double; using TS = double; using TJ = double; };
 template <> struct Pol<NB_FP32> { using TV = float;  using TG = float;  using TS = float;  using TJ = float; };
 template <> struct Pol<NB_MIXED> { using TV = float; using TG = double; using TS = double; using TJ = double; };
+template <> struct Pol<NB_FP32_DOT2> { using TV = float; using TG = float; using TS = float; using TJ = float; };
+
+// ---------------------------------------------------------------------------
+// dot-product accumulators (glsc3 partial sums).  Plain: TS accumulation.  Dot2 (NB_FP32_DOT2):
+// Ogita-Rump-Oishi compensated accumulation in binary32 -- (p, s) with TwoProduct via FMA and
+// TwoSum; partials merged as expansions of size two (SPEC.md eft module).
+// ---------------------------------------------------------------------------
+template <int PREC> struct Acc {
+    using TS = typename Pol<PREC>::TS;
+    static constexpr int W = 1;   // doubles per stored partial
+    TS v;
+    __device__ __forceinline__ Acc() : v(0) {}
+    __device__ __forceinline__ void add(TS a, TS b) { v += a * b; }
+    __device__ __forceinline__ void add_sum(TS a) { v += a; }
+    __device__ __forceinline__ void merge(const Acc &o) { v += o.v; }
+    __device__ __forceinline__ TS value() const { return v; }
+    __device__ __forceinline__ Acc shfl_down(int o) const
+    {
+        Acc r;
+        r.v = __shfl_down_sync(0xffffffffu, v, o);
+        return r;
+    }
+    __device__ __forceinline__ void store(double *d) const { d[0] = (double)v; }
+    __device__ __forceinline__ static Acc load(const double *s)
+    {
+        Acc r;
+        r.v = (TS)__ldcg(s);
+        return r;
+    }
+};
+__device__ __forceinline__ void two_sum_f(float a, float b, float &s, float &e)
+{
+    s = __fadd_rn(a, b);
+    const float bv = __fsub_rn(s, a);
+    const float av = __fsub_rn(s, bv);
+    e = __fadd_rn(__fsub_rn(a, av), __fsub_rn(b, bv));
+}
+template <> struct Acc<NB_FP32_DOT2> {
+    using TS = float;
+    static constexpr int W = 2;
+    float p, s;
+    __device__ __forceinline__ Acc() : p(0.f), s(0.f) {}
+    __device__ __forceinline__ void add(float a, float b)
+    {
+        const float h = __fmul_rn(a, b);
+        const float r = __fmaf_rn(a, b, -h);   // TwoProduct: h + r = a b exactly
+        float q;
+        two_sum_f(p, h, p, q);                // TwoSum: p + q = p_old + h exactly
+        s = __fadd_rn(s, __fadd_rn(q, r));
+    }
+    __device__ __forceinline__ void add_sum(float a)
+    {
+        float q;
+        two_sum_f(p, a, p, q);
+        s = __fadd_rn(s, q);
+    }
+    __device__ __forceinline__ void merge(const Acc &o)
+    {
+        float q;
+        two_sum_f(p, o.p, p, q);
+        s = __fadd_rn(__fadd_rn(s, o.s), q);
+    }
+    __device__ __forceinline__ float value() const { return __fadd_rn(p, s); }
+    __device__ __forceinline__ Acc shfl_down(int o) const
+    {
+        Acc r;
+        r.p = __shfl_down_sync(0xffffffffu, p, o);
+        r.s = __shfl_down_sync(0xffffffffu, s, o);
+        return r;
+    }
+    __device__ __forceinline__ void store(double *d) const { d[0] = (double)p; d[1] = (double)s; }
+    __device__ __forceinline__ static Acc load(const double *src)
+    {
+        Acc r;
+        r.p = (float)__ldcg(src);
+        r.s = (float)__ldcg(src + 1);
+        return r;
+    }
+};
 
 // ---------------------------------------------------------------------------
 // GLL derivative matrix passed by value in kernel-parameter space

@@ -26,7 +26,7 @@ k_gs(const int32_t nseg, const int32_t *__restrict__ off, const int32_t *__restr
     if (MODE == 1 && scal->done) return;
     TS acc = 0;
     const int32_t s = blockIdx.x * GS_NT + threadIdx.x;
-    if (s < nseg) acc = gs_segment<PREC, ORDER, MODE, TVX, TGX, LD_DEF>(s, off, idx, w, pv);
+    if (s < nseg) acc = gs_segment<PREC, ORDER, MODE, TVX, TGX, LD_DEF>(s, off, idx, w, pv).value();
     if (MODE == 1) {
         __shared__ TS red[32];
         TS vv[1] = {block_sum<TS>(acc, red)};

@@ -14,12 +14,12 @@
 namespace nb {
 
 template <int PREC, int ORDER, int PAP, typename TVX, typename TGX, int H>
-__device__ __forceinline__ typename Pol<PREC>::TS gs_segment(int32_t s, const int32_t *__restrict__ off,
-                                                             const int32_t *__restrict__ idx, TVX *__restrict__ w,
-                                                             const TVX *__restrict__ pv)
+__device__ __forceinline__ Acc<PREC> gs_segment(int32_t s, const int32_t *__restrict__ off,
+                                                const int32_t *__restrict__ idx, TVX *__restrict__ w,
+                                                const TVX *__restrict__ pv)
 {
     using TS = typename Pol<PREC>::TS;
-    TS acc = 0;
+    Acc<PREC> acc;
     const int32_t a0 = __ldg(off + s);
     const int32_t cnt = __ldg(off + s + 1) - a0;
     int32_t id[8];
@@ -39,7 +39,7 @@ __device__ __forceinline__ typename Pol<PREC>::TS gs_segment(int32_t s, const in
 #pragma unroll
         for (int c = 0; c < 8; c++)
             if (c < cnt) w[id[c]] = tv;
-        if (PAP) acc += (TS)tv * (TS)ldv<H>(pv + id[0]);   // sum_copies c w p = sigma p (p continuous)
+        if (PAP) acc.add((TS)tv, (TS)ldv<H>(pv + id[0]));   // sum_copies c w p = sigma p (p continuous)
     } else {
         const TS cinv = (TS)1 / (TS)cnt;
 #pragma unroll
@@ -51,7 +51,7 @@ __device__ __forceinline__ typename Pol<PREC>::TS gs_segment(int32_t s, const in
                     if (r < cnt && r != c) t += (TGX)v[r];
                 const TVX tv = (TVX)t;
                 w[id[c]] = tv;
-                if (PAP) acc += ((TS)tv * cinv) * (TS)ldv<H>(pv + id[c]);
+                if (PAP) acc.add((TS)tv * cinv, (TS)ldv<H>(pv + id[c]));
             }
         }
     }

@@ -81,7 +81,7 @@ struct nb_handle {
     cudaStream_t cap_stream = nullptr;   // private stream used for graph capture / setup
     int cg_csr = 0;             // 1: consistent-order CG also through the CSR dssum kernel (A/B)
     int cg_graph = 0;           // 1: per-phase kernels in a CUDA graph instead of the megakernel
-    nb::Workspace ws[3];
+    nb::Workspace ws[4];   // one per nb_policy
     nb::MeshDev md() const {
         nb::MeshDev m;
         m.nelx = nelx; m.nely = nely; m.nelz = nelz; m.p = p; m.n = n;

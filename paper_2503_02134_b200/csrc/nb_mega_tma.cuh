@@ -294,14 +294,14 @@ k_cg_mega_tma(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<t
     {
         const int64_t p0 = min((int64_t)A.m.E, g0 * T::EPB) * T::N2;
         const int64_t p1 = min((int64_t)A.m.E, g1 * T::EPB) * T::N2;
-        TS rtr = 0, rho = 0;
+        Acc<PREC> artr, arho;
 #pragma unroll 1
         for (int64_t pid = p0 + tid; pid < p1; pid += blockDim.x)
             init_pencil<PREC, N>(A.m, (const TV *)A.b, (TV *)A.x, (TV *)A.p, (TV *)A.r, (TV *)A.z,
-                                 (const TJ *)A.dinv, pid, rtr, rho);
+                                 (const TJ *)A.dinv, pid, artr, arho);
         fence_proxy_async();   // these writes are read by bulk copies after the barrier
-        rtr = block_sum<TS>(rtr, sh);
-        rho = block_sum<TS>(rho, sh);
+        const TS rtr = block_sum<TS>(artr.value(), sh);
+        const TS rho = block_sum<TS>(arho.value(), sh);
         if (tid == 0) { A.partB[2 * blockIdx.x] = (double)rtr; A.partB[2 * blockIdx.x + 1] = (double)rho; }
     }
     grid_barrier(A.bar);
@@ -356,10 +356,10 @@ k_cg_mega_tma(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<t
             for (int64_t s = s0 + tid; s < s1; s += blockDim.x) {
                 if (A.order == NB_GS_CONSISTENT)
                     acc2 += gs_segment<PREC, NB_GS_CONSISTENT, 1, TV, typename Pol<PREC>::TG, LD_CG>(
-                        (int32_t)s, A.gs_off, A.gs_idx, (TV *)A.w, (const TV *)A.p);
+                        (int32_t)s, A.gs_off, A.gs_idx, (TV *)A.w, (const TV *)A.p).value();
                 else
                     acc2 += gs_segment<PREC, NB_GS_PER_COPY, 1, TV, typename Pol<PREC>::TG, LD_CG>(
-                        (int32_t)s, A.gs_off, A.gs_idx, (TV *)A.w, (const TV *)A.p);
+                        (int32_t)s, A.gs_off, A.gs_idx, (TV *)A.w, (const TV *)A.p).value();
             }
             fence_proxy_async();   // w is read by bulk copies after the barrier
             acc2 = block_sum<TS>(acc2, sh);
@@ -467,7 +467,7 @@ struct MegaSel {
 template <int PREC, int N>
 constexpr bool use_tma()
 {
-    return NB_WITH_TMA && TmaCfg<PREC, N>::OK;
+    return NB_WITH_TMA && PREC != NB_FP32_DOT2 && TmaCfg<PREC, N>::OK;
 }
 
 static bool env_no_tma()
@@ -535,11 +535,13 @@ cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int
     A.b = b;
     A.x = ws.x; A.p = ws.p; A.r = ws.r; A.z = ws.z; A.w = ws.w;
     A.g = (sizeof(typename Pol<PREC>::TV) == 8) ? (const void *)h->g64 : (const void *)h->g32;
-    A.dinv = PREC == NB_FP32 ? (const void *)h->dinv32 : (const void *)h->dinv64;
+    A.dinv = sizeof(typename Pol<PREC>::TJ) == 4 ? (const void *)h->dinv32 : (const void *)h->dinv64;
     A.gs_off = h->gs_off; A.gs_idx = h->gs_idx; A.nseg = (int32_t)h->nseg;
     A.order = order; A.max_iter = max_iter; A.rtol = rtol;
     A.hist = ws.hist; A.tim = tim;
-    A.partA = ws.red.part; A.partS = ws.red.part + ws.mega_G; A.partB = ws.red.part + 2 * ws.mega_G;
+    // per-block partials: W doubles per accumulator (2 for the Dot2 expansions)
+    const size_t W = (size_t)Acc<PREC>::W;
+    A.partA = ws.red.part; A.partS = ws.red.part + W * ws.mega_G; A.partB = ws.red.part + 2 * W * ws.mega_G;
     A.bar = ws.bar;
     A.scal = ws.scal;
     const bool fused = order == NB_GS_CONSISTENT && !h->cg_csr;
