@@ -27,6 +27,7 @@ CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-st
 
 FP64, FP32, MIXED, FP32_DOT2 = 0, 1, 2, 3
 GS_CONSISTENT, GS_PER_COPY = 0, 1
+PC_JACOBI, PC_IDENTITY, PC_JACOBI_F32 = 0, 1, 2   # or_cg precond
 RHS_UNIFORM, RHS_MANUFACTURED = 0, 1
 CONVERGED, MAXITER, STAGNATED, BREAKDOWN = 0, 1, 2, 3
 
@@ -89,7 +90,7 @@ def lib():
         L.or_two_sum_f.argtypes = [C.c_float, C.c_float, P, P]
         L.or_two_prod_f.argtypes = [C.c_float, C.c_float, P, P]
         L.or_cg.argtypes = [P, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
-                            P, P, P, C.POINTER(_Report)]
+                            C.c_int, P, P, P, C.POINTER(_Report)]
         _lib = L
     return _lib
 
@@ -215,13 +216,13 @@ class Mesh:
 
     def cg(self, b64: np.ndarray, policy: int = FP64, max_iter: int = 100, rtol: float = 0.0,
            gs_order: int = GS_CONSISTENT, stag_window: int = 200, seqdot: bool = False,
-           x64: bool = False):
+           x64: bool = False, precond: int = 0):
         b64 = np.ascontiguousarray(b64, dtype=np.float64)
         x = np.zeros(self.n_local)
         hist = np.zeros(max_iter + 1)
         rep = _Report()
         rc = lib().or_cg(self._h, policy, max_iter, rtol, gs_order, stag_window, int(seqdot),
-                         int(x64), _p(b64), _p(x), _p(hist), C.byref(rep))
+                         int(x64), int(precond), _p(b64), _p(x), _p(hist), C.byref(rep))
         if rc:
             raise ValueError("or_cg: bad arguments")
         r = Report(rep.iterations, rep.status, rep.rtr0, rep.rtr_final, rep.rel_res_final,

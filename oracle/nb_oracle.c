@@ -725,7 +725,7 @@ static double true_residual(const or_mesh *m, const double *b64, const double *x
     return bb > 0.0 ? sqrt(rr / bb) : 0.0;
 }
 
-static int cg_fp64(const or_mesh *m, int max_iter, double rtol, int order, int W, const double *b64,
+static int cg_fp64(const or_mesh *m, int max_iter, double rtol, int order, int W, int pc, const double *b64,
                    double *x, double *res, or_report *rep)
 {
     const int64_t NL = m->NL;
@@ -738,7 +738,8 @@ static int cg_fp64(const or_mesh *m, int max_iter, double rtol, int order, int W
     if (rtr0 == 0.0) { status = OR_CONVERGED; res[0] = 0.0; }
     else {
         for (k = 1; k <= max_iter; k++) {
-            for (int64_t l = 0; l < NL; l++) z[l] = r[l] * m->dinv[l];                /* solveM */
+            if (pc == OR_PC_IDENTITY) for (int64_t l = 0; l < NL; l++) z[l] = r[l];  /* solveM: none */
+            else for (int64_t l = 0; l < NL; l++) z[l] = r[l] * m->dinv[l];          /* solveM */
             rho = or_glsc3_d(r, m->c, z, NL);                                        /* glsc3 */
             double beta = (k == 1) ? 0.0 : rho / rho_old;
             rho_old = rho;
@@ -763,7 +764,7 @@ static int cg_fp64(const or_mesh *m, int max_iter, double rtol, int order, int W
 
 /* fp32 and mixed policies (C-10 table). */
 static int cg_f32(const or_mesh *m, int policy, int max_iter, double rtol, int order, int W, int seqdot,
-                  int x64, const double *b64, double *x_out, double *res, or_report *rep)
+                  int x64, int pc, const double *b64, double *x_out, double *res, or_report *rep)
 {
     const int64_t NL = m->NL;
     const int mixed = (policy == OR_MIXED);
@@ -787,8 +788,10 @@ static int cg_f32(const or_mesh *m, int policy, int max_iter, double rtol, int o
     if (rtr0 == 0.0) { status = OR_CONVERGED; res[0] = 0.0; }
     else {
         for (k = 1; k <= max_iter; k++) {
-            /* solveM: mixed z = (float)((double)r * dinv64); fp32 z = r * dinv32 */
-            if (mixed) for (int64_t l = 0; l < NL; l++) z[l] = (float)((double)r[l] * m->dinv[l]);
+            /* solveM: mixed z = (float)((double)r * dinv64); fp32 (and the Neko-style fp32 copy
+               under mixed) z = r * dinv32; identity z = r */
+            if (pc == OR_PC_IDENTITY) for (int64_t l = 0; l < NL; l++) z[l] = r[l];
+            else if (mixed && pc == OR_PC_JACOBI) for (int64_t l = 0; l < NL; l++) z[l] = (float)((double)r[l] * m->dinv[l]);
             else for (int64_t l = 0; l < NL; l++) z[l] = r[l] * m->dinvf[l];
             float beta_f;
             if (mixed) {
@@ -837,14 +840,17 @@ static int cg_f32(const or_mesh *m, int policy, int max_iter, double rtol, int o
 }
 
 int or_cg(const or_mesh *m, int policy, int max_iter, double rtol, int gs_order, int stag_window,
-          int seqdot, int x64, const double *b64, double *x_out, double *hist, or_report *rep)
+          int seqdot, int x64, int precond, const double *b64, double *x_out, double *hist, or_report *rep)
 {
     if (!m || !b64 || !x_out || !rep || max_iter < 0 || rtol < 0.0) return 1;
     if (policy < OR_FP64 || policy > OR_FP32_DOT2) return 1;
+    if (precond < OR_PC_JACOBI || precond > OR_PC_JACOBI_F32) return 1;
+    if (policy == OR_FP64 && precond == OR_PC_JACOBI_F32) return 1;
+    if (x64 && policy != OR_MIXED) return 1;
     double *res = (double *)calloc((size_t)max_iter + 1, sizeof(double));
     int rc;
-    if (policy == OR_FP64) rc = cg_fp64(m, max_iter, rtol, gs_order, stag_window, b64, x_out, res, rep);
-    else rc = cg_f32(m, policy, max_iter, rtol, gs_order, stag_window, seqdot, x64, b64, x_out, res, rep);
+    if (policy == OR_FP64) rc = cg_fp64(m, max_iter, rtol, gs_order, stag_window, precond, b64, x_out, res, rep);
+    else rc = cg_f32(m, policy, max_iter, rtol, gs_order, stag_window, seqdot, x64, precond, b64, x_out, res, rep);
     if (hist) for (int i = 0; i <= rep->iterations; i++) hist[i] = res[i];
     rep->true_res = true_residual(m, b64, x_out);
     free(res);

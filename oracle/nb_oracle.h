@@ -81,10 +81,16 @@ float or_glsc3_f_dot2(const float *a, const float *c, const float *b, int64_t n)
  * C-10 PCG.  b64: fp64 RHS (cast once to the policy precision).  x_out: n_local doubles
  * (the policy-precision solution widened).  hist: nullable, len max_iter+1 (hist[0] = 1).
  * seqdot: fp32 policy uses Nekbone's sequential float dot instead of the pairwise tree.
- * x64: mixed policy keeps x in fp64 (C-15 variant).  Returns 0, or 1 on bad arguments.
+ * x64: mixed policy keeps x in fp64 (C-15 variant).
+ * precond: OR_PC_JACOBI = the policy's Jacobi (C-10 table);
+ *   OR_PC_IDENTITY = none, z = r ("CG with the identity ... preconditioner");
+ *   OR_PC_JACOBI_F32 = Neko's single-precision copy of the Jacobi diagonal, z = r * (float)dinv in
+ *   binary32 -- for fp32/dot2 the same as OR_PC_JACOBI; rejected for fp64.
+ * Returns 0, or 1 on bad arguments.
  */
+enum { OR_PC_JACOBI = 0, OR_PC_IDENTITY = 1, OR_PC_JACOBI_F32 = 2 };
 int or_cg(const or_mesh *m, int policy, int max_iter, double rtol, int gs_order, int stag_window,
-          int seqdot, int x64, const double *b64, double *x_out, double *hist, or_report *rep);
+          int seqdot, int x64, int precond, const double *b64, double *x_out, double *hist, or_report *rep);
 
 #ifdef __cplusplus
 }
