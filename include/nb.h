@@ -88,6 +88,15 @@ typedef struct {
     int32_t p, nelx, nely, nelz;
 } nb_info;
 
+/* Preconditioner of nb_cg:
+ *   NB_PC_JACOBI    : the policy's Jacobi z = M^-1 r (C-10 table: fp64 diagonal for NB_FP64 and
+ *                     NB_MIXED, its one-time float copy for NB_FP32 / NB_FP32_DOT2).
+ *   NB_PC_IDENTITY  : none, z = r -- "CG with the identity ... preconditioner".
+ *   NB_PC_JACOBI_F32: Neko's "single precision copy of the preconditioner":
+ *                     z = r * (float)dinv in binary32.  Same as NB_PC_JACOBI for NB_FP32 /
+ *                     NB_FP32_DOT2; NB_EINVAL for NB_FP64. */
+typedef enum { NB_PC_JACOBI = 0, NB_PC_IDENTITY = 1, NB_PC_JACOBI_F32 = 2 } nb_precond;
+
 typedef struct {
     nb_policy policy;
     int32_t max_iter;          /* >= 0 */
@@ -96,6 +105,9 @@ typedef struct {
     int32_t stag_window;       /* C-11 window W (default 200 when <= 0) */
     int32_t time_kernels;      /* 1: record per-kernel CUDA-event durations into the report */
     double *rel_res_history;   /* host, length max_iter+1, nullable: [0] = 1, [k] = sqrt(rtr_k/rtr0) */
+    nb_precond precond;        /* 0 = NB_PC_JACOBI (zero-initialised options keep the default) */
+    int32_t x_fp64;            /* NB_MIXED only (else NB_EINVAL): x += alpha p accumulated in double
+                                  with the double alpha, and x returned as n_local DOUBLES (C-15 variant) */
 } nb_cg_opts;
 
 typedef struct {
@@ -132,7 +144,9 @@ int nb_ax(nb_handle *h, nb_policy prec, const void *u, void *w, uint32_t flags, 
 int nb_dssum(nb_handle *h, nb_policy prec, nb_gs_order order, void *u, void *stream);
 
 /* Jacobi-PCG (Table 2 order) from x0 = 0.  b, x: device vectors in the
- * policy precision; b must be continuous and masked (e.g. from nb_rhs).  Blocks until done.
+ * policy precision (x: double when o->x_fp64); b must be continuous and masked (e.g. from
+ * nb_rhs).  Blocks until done.  The graph driver (env NB_CG_DRIVER=graph) supports the default
+ * options only (policies 0-2, NB_PC_JACOBI, x_fp64 = 0): NB_EINVAL otherwise.
  * Returns NB_OK for converged / max_iter / stagnated runs, NB_EBREAKDOWN on breakdown
  * (report filled in either case). */
 int nb_cg(nb_handle *h, const nb_cg_opts *o, const void *b, void *x, nb_cg_report *rep, void *stream);

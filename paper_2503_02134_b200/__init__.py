@@ -21,6 +21,7 @@ from ._build import LIB, build as _build_lib
 
 NB_FP64, NB_FP32, NB_MIXED, NB_FP32_DOT2 = 0, 1, 2, 3
 NB_GS_CONSISTENT, NB_GS_PER_COPY = 0, 1
+NB_PC_JACOBI, NB_PC_IDENTITY, NB_PC_JACOBI_F32 = 0, 1, 2
 NB_RHS_UNIFORM, NB_RHS_MANUFACTURED = 0, 1
 NB_AX_LOCAL = 1
 NB_CONVERGED, NB_MAXITER, NB_STAGNATED, NB_BROKEDOWN = 0, 1, 2, 3
@@ -45,7 +46,8 @@ class nb_info(C.Structure):
 
 class nb_cg_opts(C.Structure):
     _fields_ = [("policy", C.c_int), ("max_iter", C.c_int32), ("rtol", C.c_double), ("gs_order", C.c_int),
-                ("stag_window", C.c_int32), ("time_kernels", C.c_int32), ("rel_res_history", C.c_void_p)]
+                ("stag_window", C.c_int32), ("time_kernels", C.c_int32), ("rel_res_history", C.c_void_p),
+                ("precond", C.c_int), ("x_fp64", C.c_int32)]
 
 
 class nb_cg_report(C.Structure):
@@ -150,41 +152,47 @@ def nb_dssum(h, prec: int, order: int, u, stream=None):
     _check(lib().nb_dssum(h, prec, order, _dptr(u, policy_dtype(prec)), _stream(stream)))
 
 
-def _opts(policy, max_iter, rtol, gs_order, stag_window, time_kernels, hist):
+def _opts(policy, max_iter, rtol, gs_order, stag_window, time_kernels, hist, precond=NB_PC_JACOBI, x64=False):
     o = nb_cg_opts()
     o.policy, o.max_iter, o.rtol, o.gs_order = policy, max_iter, rtol, gs_order
     o.stag_window, o.time_kernels = stag_window, int(time_kernels)
+    o.precond, o.x_fp64 = precond, int(x64)
     o.rel_res_history = hist.ctypes.data if hist is not None else None
     return o
 
 
 def nb_cg(h, b, x, policy: int = NB_MIXED, max_iter: int = 1000, rtol: float = 1e-8,
           gs_order: int = NB_GS_CONSISTENT, stag_window: int = 200, time_kernels: bool = False,
-          history: bool = True, stream=None, allow_breakdown: bool = True):
-    """Jacobi-PCG from x0 = 0; returns (report, rel_res_history)."""
+          history: bool = True, stream=None, allow_breakdown: bool = True, precond: int = NB_PC_JACOBI,
+          x64: bool = False):
+    """PCG from x0 = 0; returns (report, rel_res_history).  x is float64 when x64."""
+    import torch
     dt = policy_dtype(policy)
     hist = np.zeros(max_iter + 1) if history else None
-    o = _opts(policy, max_iter, rtol, gs_order, stag_window, time_kernels, hist)
+    o = _opts(policy, max_iter, rtol, gs_order, stag_window, time_kernels, hist, precond, x64)
     rep = nb_cg_report()
-    rc = lib().nb_cg(h, C.byref(o), _dptr(b, dt), _dptr(x, dt), C.byref(rep), _stream(stream))
+    rc = lib().nb_cg(h, C.byref(o), _dptr(b, dt), _dptr(x, torch.float64 if x64 else dt), C.byref(rep),
+                     _stream(stream))
     if rc != NB_OK and not (allow_breakdown and rc == NB_EBREAKDOWN):
         _check(rc)
     return rep, (hist[: rep.iterations + 1] if hist is not None else None)
 
 
 def nb_cg_host(h, b_host, x_host, policy: int = NB_MIXED, max_iter: int = 1000, rtol: float = 1e-8,
-               gs_order: int = NB_GS_CONSISTENT, stag_window: int = 200, history: bool = False, stream=None):
+               gs_order: int = NB_GS_CONSISTENT, stag_window: int = 200, history: bool = False, stream=None,
+               precond: int = NB_PC_JACOBI, x64: bool = False):
     """Same solve with host buffers (numpy arrays or pinned CPU tensors); copies inside the call."""
-    def hp(a):
+    def hp(a, pol):
         if isinstance(a, np.ndarray):
-            assert a.flags["C_CONTIGUOUS"] and a.dtype == policy_np_dtype(policy)
+            assert a.flags["C_CONTIGUOUS"] and a.dtype == policy_np_dtype(pol)
             return C.c_void_p(a.ctypes.data)
-        assert a.device.type == "cpu" and a.is_contiguous() and a.dtype == policy_dtype(policy)
+        assert a.device.type == "cpu" and a.is_contiguous() and a.dtype == policy_dtype(pol)
         return C.c_void_p(a.data_ptr())
     hist = np.zeros(max_iter + 1) if history else None
-    o = _opts(policy, max_iter, rtol, gs_order, stag_window, False, hist)
+    o = _opts(policy, max_iter, rtol, gs_order, stag_window, False, hist, precond, x64)
     rep = nb_cg_report()
-    rc = lib().nb_cg_host(h, C.byref(o), hp(b_host), hp(x_host), C.byref(rep), _stream(stream))
+    rc = lib().nb_cg_host(h, C.byref(o), hp(b_host, policy), hp(x_host, NB_FP64 if x64 else policy), C.byref(rep),
+                          _stream(stream))
     if rc not in (NB_OK, NB_EBREAKDOWN):
         _check(rc)
     return rep, (hist[: rep.iterations + 1] if hist is not None else None)
@@ -284,9 +292,10 @@ class Mesh:
         return v
 
     def cg(self, b, policy=NB_MIXED, max_iter=1000, rtol=1e-8, gs_order=NB_GS_CONSISTENT, stag_window=200,
-           time_kernels=False):
-        x = self.empty(policy)
-        rep, hist = nb_cg(self.h, b, x, policy, max_iter, rtol, gs_order, stag_window, time_kernels)
+           time_kernels=False, precond=NB_PC_JACOBI, x64=False):
+        x = self.empty(NB_FP64 if x64 else policy)
+        rep, hist = nb_cg(self.h, b, x, policy, max_iter, rtol, gs_order, stag_window, time_kernels,
+                          precond=precond, x64=x64)
         r = CgResult(rep.iterations, rep.status, rep.rtr0, rep.rel_res_final, rep.rel_res_min, rep.solve_ms,
                      rep.kernel_launches, rep.k_ax_ms, rep.k_gs_ms, rep.k_upd_ms, hist)
         return x, r

@@ -15,6 +15,7 @@ import sys
 
 POLICIES = {"fp64": 0, "fp32": 1, "mixed": 2, "fp32_dot2": 3}
 ORDERS = {"consistent": 0, "per_copy": 1}
+PRECONDS = {"jacobi": 0, "identity": 1, "jacobi_f32": 2}
 
 
 def main(argv=None) -> int:
@@ -31,6 +32,8 @@ def main(argv=None) -> int:
     s.add_argument("--gs-order", choices=list(ORDERS), default="consistent")
     s.add_argument("--rhs", choices=["uniform", "manufactured"], default="uniform")
     s.add_argument("--noise", type=float, default=1e-3)
+    s.add_argument("--precond", choices=list(PRECONDS), default="jacobi")
+    s.add_argument("--x64", action="store_true", help="mixed policy: accumulate x in fp64")
     s.add_argument("--history", action="store_true", help="include the residual history")
     try:
         a = ap.parse_args(argv)
@@ -45,11 +48,16 @@ def main(argv=None) -> int:
     pol = POLICIES[a.policy]
     kind = nb.NB_RHS_UNIFORM if a.rhs == "uniform" else nb.NB_RHS_MANUFACTURED
     b = mesh.rhs(pol, kind, noise=a.noise, seed=a.seed)
-    x, r = mesh.cg(b, pol, max_iter=a.max_iter, rtol=a.rtol, gs_order=ORDERS[a.gs_order])
+    try:
+        x, r = mesh.cg(b, pol, max_iter=a.max_iter, rtol=a.rtol, gs_order=ORDERS[a.gs_order],
+                       precond=PRECONDS[a.precond], x64=a.x64)
+    except nb.NbError as e:
+        print(json.dumps({"error": str(e)}), file=sys.stderr)
+        return 1
     status = {nb.NB_CONVERGED: "converged", nb.NB_MAXITER: "max_iter", nb.NB_STAGNATED: "stagnated",
               nb.NB_BROKEDOWN: "breakdown"}[r.status]
     out = {"schema": "nb-run-report/1", "nel": a.nel, "p": a.p, "deform": a.deform, "policy": a.policy,
-           "gs_order": a.gs_order, "rhs": a.rhs, "n_local": mesh.n_local, "iterations": r.iterations,
+           "gs_order": a.gs_order, "precond": a.precond, "x64": a.x64, "rhs": a.rhs, "n_local": mesh.n_local, "iterations": r.iterations,
            "status": status, "rel_res_final": r.rel_res_final, "rel_res_min": r.rel_res_min,
            "solve_ms": r.solve_ms, "dof_iter_per_s": mesh.n_local * r.iterations / (r.solve_ms * 1e-3)
            if r.solve_ms > 0 else None}

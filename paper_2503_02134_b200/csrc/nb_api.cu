@@ -199,7 +199,7 @@ void free_ws(nb::Workspace &ws)
         if (ws.exec[o]) cudaGraphExecDestroy(ws.exec[o]);
         if (ws.graph[o]) cudaGraphDestroy(ws.graph[o]);
     }
-    cudaFree(ws.r); cudaFree(ws.p); cudaFree(ws.w); cudaFree(ws.x); cudaFree(ws.z);
+    cudaFree(ws.r); cudaFree(ws.p); cudaFree(ws.w); cudaFree(ws.x); cudaFree(ws.z); cudaFree(ws.xd);
     cudaFree(ws.red.part); cudaFree(ws.red.part2); cudaFree(ws.red.cnt);
     cudaFree(ws.scal); cudaFree(ws.hist); cudaFree(ws.tim); cudaFree(ws.bar);
     if (ws.scal_host) cudaFreeHost(ws.scal_host);
@@ -442,6 +442,7 @@ static int cg_impl(nb_handle *h, const nb_cg_opts *o, const void *b, bool b_host
     if (prec != NB_FP64 && (rc = ensure_f32(h))) return rc;
     if ((rc = ensure_ws(h, prec, o->max_iter))) return rc;
     nb::Workspace &ws = h->ws[prec];
+    if (o->x_fp64 && !ws.xd) NB_CU(cudaMalloc(&ws.xd, sizeof(double) * h->NL), "cudaMalloc xd");
     const size_t vbytes = vsize(prec) * h->NL;
     const bool mega = !h->cg_graph;
     if (!mega && !o->time_kernels && (rc = build_graph(h, prec, order))) return rc;
@@ -468,7 +469,9 @@ static int cg_impl(nb_handle *h, const nb_cg_opts *o, const void *b, bool b_host
     const int per_it = fused ? 2 : 3;
     double kms[3] = {0.0, 0.0, 0.0};
     if (mega) {
-        NB_CU(NB_POL(prec, nb::launch_cg_mega, h, ws, bdev, order, o->max_iter, o->rtol, ws.tim, st), "cg megakernel");
+        NB_CU(NB_POL(prec, nb::launch_cg_mega, h, ws, bdev, order, o->max_iter, o->rtol, (int)o->precond, (int)o->x_fp64,
+                     ws.tim, st),
+              "cg megakernel");
         launches = 1;
     } else {
         NB_CU(NB_POL(prec, nb::launch_cg_init, h, ws, bdev, st), "cg init");
@@ -511,7 +514,12 @@ static int cg_impl(nb_handle *h, const nb_cg_opts *o, const void *b, bool b_host
         NB_CU(NB_POL(prec, nb::launch_cg_fin, h, ws, st), "cg fin");
     }
     NB_CU(cudaMemcpyAsync(ws.scal_host, ws.scal, sizeof(nb::Scal), cudaMemcpyDeviceToHost, st), "copy scal back");
-    NB_CU(cudaMemcpyAsync(x, ws.x, vbytes, x_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st), "copy x");
+    if (o->x_fp64)
+        NB_CU(cudaMemcpyAsync(x, ws.xd, sizeof(double) * h->NL, x_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                              st),
+              "copy x");
+    else
+        NB_CU(cudaMemcpyAsync(x, ws.x, vbytes, x_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st), "copy x");
     NB_CU(cudaEventRecord(t1, st), "event record");
     NB_CU(cudaStreamSynchronize(st), "solve sync");
     float ms = 0.f;
@@ -564,9 +572,15 @@ static int cg_args(nb_handle *h, const nb_cg_opts *o)
 {
     if (!h || !o) return fail(NB_EINVAL, "NULL argument");
     if (o->policy < NB_FP64 || o->policy > NB_FP32_DOT2) return fail(NB_EINVAL, "bad policy");
-    // the graph driver's last-block grid reduction carries one plain value per block
-    if (o->policy == NB_FP32_DOT2 && h->cg_graph)
-        return fail(NB_EINVAL, "the fp32+Dot2 policy runs on the megakernel driver only (unset NB_CG_DRIVER)");
+    if (o->precond < NB_PC_JACOBI || o->precond > NB_PC_JACOBI_F32) return fail(NB_EINVAL, "bad precond");
+    if (o->precond == NB_PC_JACOBI_F32 && o->policy == NB_FP64)
+        return fail(NB_EINVAL, "NB_PC_JACOBI_F32 is a single-precision variant (not for NB_FP64)");
+    if (o->x_fp64 != 0 && o->x_fp64 != 1) return fail(NB_EINVAL, "x_fp64 must be 0 or 1");
+    if (o->x_fp64 && o->policy != NB_MIXED) return fail(NB_EINVAL, "x_fp64 applies to NB_MIXED only");
+    // the graph driver's last-block grid reduction carries one plain value per block, and its
+    // kernels implement the default options only
+    if (h->cg_graph && (o->policy == NB_FP32_DOT2 || o->precond != NB_PC_JACOBI || o->x_fp64))
+        return fail(NB_EINVAL, "the graph driver supports policies 0-2 with the default options only (unset NB_CG_DRIVER)");
     if (o->gs_order != NB_GS_CONSISTENT && o->gs_order != NB_GS_PER_COPY) return fail(NB_EINVAL, "bad gs order");
     if (o->max_iter < 0 || !(o->rtol >= 0.0)) return fail(NB_EINVAL, "bad max_iter/rtol");
     NB_CU(cudaSetDevice(h->device), "cudaSetDevice");

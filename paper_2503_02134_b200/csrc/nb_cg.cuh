@@ -135,7 +135,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
          typename Pol<PREC>::TV *__restrict__ pv, typename Pol<PREC>::TV *__restrict__ xv,
          const typename Pol<PREC>::TV *__restrict__ g, typename Pol<PREC>::TV *__restrict__ w, bool apply_mask,
          typename Pol<PREC>::TV beta, typename Pol<PREC>::TV alpha, int e, bool active, int a, int b,
-         typename Pol<PREC>::TV *__restrict__ S0)
+         typename Pol<PREC>::TV *__restrict__ S0, double *__restrict__ xd = nullptr, double alpha_d = 0.0)
 {
     using TV = typename Pol<PREC>::TV;
     using TS = typename Pol<PREC>::TS;
@@ -155,6 +155,20 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         TV u[N];
         if (MODE == 0) {
             ld_pencil<TV, N>(in + gbase, u);
+        } else if (PREC == NB_MIXED && xd) {
+            // x_fp64 variant (C-15): x += alpha p in double with the double alpha
+            TV zz[N], po[N];
+            double xx[N];
+            ld_pencil<TV, N, LD_CS>(in + gbase, zz);
+            ld_pencil<TV, N>(pv + gbase, po);
+            ld_pencil<double, N, LD_CS>(xd + gbase, xx);
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                u[i] = fma(beta, po[i], zz[i]);                 // add2s1
+                xx[i] = fma(alpha_d, (double)po[i], xx[i]);     // add2s2(x, p_old, alpha_prev)
+            }
+            st_pencil<TV, N>(pv + gbase, u);
+            st_pencil<double, N, LD_CS>(xd + gbase, xx);
         } else {
             TV zz[N], po[N], xx[N];
             ld_pencil<TV, N, LD_CS>(in + gbase, zz);
@@ -437,11 +451,38 @@ __device__ __forceinline__ void gather_pencil(const MeshDev &m, const typename P
         if (yz || (i == 0 && xl) || (i == N - 1 && xr)) ww[i] = (TV)s[i];
 }
 
+// z = M^-1 r of the preconditioner variant (nb.h nb_precond, uniform runtime pc): the dinv
+// pencil as TJ -- the policy's diagonal, or under mixed the fp32 copy (NB_PC_JACOBI_F32) widened
+// exactly; the identity loads nothing (d = 1, so z = r exactly, and z aliases r).
+template <typename TJ, int N>
+__device__ __forceinline__ void ld_dinv(const void *__restrict__ dinv, size_t base, int pc, TJ (&dd)[N])
+{
+    if (pc == NB_PC_IDENTITY) {
+#pragma unroll
+        for (int i = 0; i < N; i++) dd[i] = TJ(1);
+    } else if (sizeof(TJ) == 8 && pc == NB_PC_JACOBI_F32) {
+        float f[N];
+        ld_pencil<float, N, LD_NC>((const float *)dinv + base, f);
+#pragma unroll
+        for (int i = 0; i < N; i++) dd[i] = (TJ)f[i];
+    } else {
+        ld_pencil<TJ, N, LD_NC>((const TJ *)dinv + base, dd);
+    }
+}
+template <int PREC>
+__device__ __forceinline__ typename Pol<PREC>::TV solve_m(typename Pol<PREC>::TV r, typename Pol<PREC>::TJ d, int pc)
+{
+    using TV = typename Pol<PREC>::TV;
+    if (PREC == NB_MIXED && pc == NB_PC_JACOBI_F32) return (TV)((float)r * (float)d);   // Neko's fp32 copy
+    return (TV)((typename Pol<PREC>::TJ)r * d);
+}
+
 template <int PREC, int N, int GATHER>
 __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ w,
                                            typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
-                                           const typename Pol<PREC>::TJ *__restrict__ dinv,
-                                           typename Pol<PREC>::TV alpha, int64_t pid, Acc<PREC> &rtr, Acc<PREC> &rho)
+                                           const void *__restrict__ dinv,
+                                           typename Pol<PREC>::TV alpha, int64_t pid, Acc<PREC> &rtr, Acc<PREC> &rho,
+                                           int pc = NB_PC_JACOBI)
 {
     using TV = typename Pol<PREC>::TV;
     using TJ = typename Pol<PREC>::TJ;
@@ -456,7 +497,7 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
     const ElemPos P = elem_pos(m, e);
     ld_pencil<TV, N, NB_WLD>(w + base, ww);
     ld_pencil<TV, N>(r + base, rr);
-    ld_pencil<TJ, N, LD_NC>(dinv + base, dd);
+    ld_dinv<TJ, N>(dinv, base, pc, dd);
     if (GATHER) {
         constexpr int N3 = N * N * N;
         const TV ol = P.ex > 0 ? ldv<NB_WLD>(w + base - N3 + (N - 1)) : TV(0);
@@ -467,14 +508,14 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
 #pragma unroll
     for (int i = 0; i < N; i++) {
         rr[i] = fma(-alpha, ww[i], rr[i]);                   // add2s2(r, w, -alpha)
-        zz[i] = (TV)((TJ)rr[i] * dd[i]);                     // solveM
+        zz[i] = solve_m<PREC>(rr[i], dd[i], pc);              // solveM
         const TS c = (TS)1 / (TS)(mjk * axis_mult(i, N, P.ex, m.nelx));
         const TS rs = (TS)rr[i];
         rtr.add(rs * c, rs);                                 // glsc3(r, c, r)
         rho.add(rs * c, (TS)zz[i]);                          // glsc3(r, c, z)
     }
     st_pencil<TV, N>(r + base, rr);
-    st_pencil<TV, N>(z + base, zz);
+    if (pc != NB_PC_IDENTITY) st_pencil<TV, N>(z + base, zz);
 }
 
 // CG prologue for one pencil: r = b, x = 0, p = 0, z = M^-1 r; rtr0 and rho_1 partials.
@@ -482,12 +523,12 @@ template <int PREC, int N>
 __device__ __forceinline__ void init_pencil(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ bvec,
                                             typename Pol<PREC>::TV *__restrict__ x, typename Pol<PREC>::TV *__restrict__ pv,
                                             typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
-                                            const typename Pol<PREC>::TJ *__restrict__ dinv, int64_t pid,
-                                            Acc<PREC> &rtr, Acc<PREC> &rho)
+                                            const void *__restrict__ dinv, int64_t pid,
+                                            Acc<PREC> &rtr, Acc<PREC> &rho, bool x64 = false, int pc = NB_PC_JACOBI)
 {
     using TV = typename Pol<PREC>::TV;
-    using TJ = typename Pol<PREC>::TJ;
     using TS = typename Pol<PREC>::TS;
+    using TD = typename Pol<PREC>::TJ;
     constexpr int N2 = N * N;
     const int e = (int)(pid / N2);
     const int q = (int)(pid - (int64_t)e * N2);
@@ -495,22 +536,29 @@ __device__ __forceinline__ void init_pencil(const MeshDev &m, const typename Pol
     const size_t base = (size_t)pid * N;
     const ElemPos P = elem_pos(m, e);
     TV rr[N], zz[N], zero[N];
-    TJ dd[N];
+    TD dd[N];
     ld_pencil<TV, N>(bvec + base, rr);
-    ld_pencil<TJ, N, LD_NC>(dinv + base, dd);
+    ld_dinv<TD, N>(dinv, base, pc, dd);
     const int mjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz);
 #pragma unroll
     for (int i = 0; i < N; i++) {
         zero[i] = TV(0);
-        zz[i] = (TV)((TJ)rr[i] * dd[i]);
+        zz[i] = solve_m<PREC>(rr[i], dd[i], pc);
         const TS c = (TS)1 / (TS)(mjk * axis_mult(i, N, P.ex, m.nelx));
         const TS rs = (TS)rr[i];
         rtr.add(rs * c, rs);
         rho.add(rs * c, (TS)zz[i]);
     }
     st_pencil<TV, N>(r + base, rr);
-    st_pencil<TV, N>(z + base, zz);
-    st_pencil<TV, N>(x + base, zero);
+    if (pc != NB_PC_IDENTITY) st_pencil<TV, N>(z + base, zz);
+    if (PREC == NB_MIXED && x64) {
+        double zd[N];
+#pragma unroll
+        for (int i = 0; i < N; i++) zd[i] = 0.0;
+        st_pencil<double, N>((double *)x + base, zd);
+    } else {
+        st_pencil<TV, N>(x + base, zero);
+    }
     st_pencil<TV, N>(pv + base, zero);
 }
 
@@ -532,7 +580,9 @@ struct MegaArgs {
     double rtol;
     double *hist;           // [max_iter + 1]
     unsigned long long *tim;  // nullable: [3 * (max_iter + 1)] globaltimer stamps (block 0)
-    double *partA, *partS, *partB;   // per-block partials, [G], [G], [2G]
+    double *partA, *partS, *partB;   // per-block partials, [G], [G], [2G] (x Acc::W)
+    int32_t pc;             // nb_precond (z aliases r for the identity)
+    int32_t x64;            // NB_MIXED: x is double (x_fp64 option)
     unsigned int *bar;      // [2] grid barrier: arrival count, generation
     Scal *scal;             // result scalars (written by block 0)
 };
@@ -688,7 +738,9 @@ __device__ __forceinline__ TS all_blocks_sum1(const double *part, int G, TS *sh)
     return o[0];
 }
 
-template <int PREC, int N, int FUSED>
+// VAR = 0: the default options (Jacobi, x in the policy precision) folded at compile time;
+// VAR = 1: the NEXT-3 variants (nb_cg_opts.precond / .x_fp64) as uniform runtime selects.
+template <int PREC, int N, int FUSED, int VAR>
 __global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT, AxCfg<typename Pol<PREC>::TV, N>::MINB)
 k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D)
 {
@@ -736,8 +788,8 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
         Acc<PREC> v[2];
 #pragma unroll 1
         for (int64_t pid = p0 + tid; pid < p1; pid += blockDim.x)
-            init_pencil<PREC, N>(A.m, (const TV *)A.b, (TV *)A.x, (TV *)A.p, (TV *)A.r, (TV *)A.z,
-                                 (const TJ *)A.dinv, pid, v[0], v[1]);
+            init_pencil<PREC, N>(A.m, (const TV *)A.b, (TV *)A.x, (TV *)A.p, (TV *)A.r, (TV *)A.z, A.dinv, pid, v[0],
+                                 v[1], VAR && A.x64 != 0, VAR ? A.pc : NB_PC_JACOBI);
         TS tot[2];
         NB_GRID_REDUCE(2, v, A.partB, tot);
         if (t0 && A.tim) A.tim[0] = globaltimer();
@@ -760,6 +812,8 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
         {
             Acc<PREC> v[1];
             const TV bv = (TV)st.beta, av = st.pending ? (TV)st.alpha : TV(0);
+            double *const xd = (VAR && PREC == NB_MIXED && A.x64) ? (double *)A.x : nullptr;
+            const double ad = st.pending ? (double)st.alpha : 0.0;
             const int64_t g1 = NB_G1;
 #pragma unroll 1
             for (int64_t gr = NB_G0; gr < g1; gr++) {
@@ -767,7 +821,7 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
                 const bool active = NB_EL < C::EPB && e < A.m.E;
                 v[0].merge(ax_group<PREC, N, FUSED ? 1 : 2>(A.m, D, (const TV *)A.z, (TV *)A.p, (TV *)A.x,
                                                          (const TV *)A.g, (TV *)A.w, true, bv, av, e, active, NB_A,
-                                                         NB_B, NB_S0));
+                                                         NB_B, NB_S0, xd, ad));
             }
             TS tot[1];
             NB_GRID_REDUCE(1, v, A.partA, tot);
@@ -811,10 +865,10 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
             const int64_t g1 = NB_G1;
             const int e_end = (int)min((int64_t)A.m.E, g1 * C::EPB);
             const int64_t p1 = (int64_t)e_end * C::N2;
+            const int pc = VAR ? A.pc : NB_PC_JACOBI;
 #pragma unroll 1
             for (int64_t pid = NB_G0 * C::EPB * C::N2 + tid; pid < p1; pid += blockDim.x)
-                upd_pencil<PREC, N, FUSED>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, (const TJ *)A.dinv, av, pid,
-                                           v[0], v[1]);
+                upd_pencil<PREC, N, FUSED>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, A.dinv, av, pid, v[0], v[1], pc);
             TS tot[2];
             NB_GRID_REDUCE(2, v, A.partB, tot);
             if (tid == 0) {
@@ -841,9 +895,15 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
         const TV av = (TV)st.alpha;
         const int64_t l0 = min((int64_t)A.m.E, NB_G0 * C::EPB) * C::N3;
         const int64_t l1 = min((int64_t)A.m.E, NB_G1 * C::EPB) * C::N3;
-        TV *x = (TV *)A.x;
         const TV *pv = (const TV *)A.p;
-        for (int64_t l = l0 + tid; l < l1; l += blockDim.x) x[l] = fma(av, pv[l], x[l]);
+        if (VAR && PREC == NB_MIXED && A.x64) {
+            double *x = (double *)A.x;
+            const double ad = (double)st.alpha;
+            for (int64_t l = l0 + tid; l < l1; l += blockDim.x) x[l] = fma(ad, (double)pv[l], x[l]);
+        } else {
+            TV *x = (TV *)A.x;
+            for (int64_t l = l0 + tid; l < l1; l += blockDim.x) x[l] = fma(av, pv[l], x[l]);
+        }
     }
     if (t0) {
         Scal *s = A.scal;
@@ -1142,16 +1202,24 @@ cudaError_t launch_cg_fin(const nb_handle *h, Workspace &ws, cudaStream_t st)
 }
 
 #define NB_INSTANTIATE_CG(P)                                                                                  \
+    extern template int grid_mega_var<P, 1>(const nb_handle *);                                               \
+    extern template cudaError_t launch_cg_mega_var<P, 1>(const nb_handle *, const MegaArgs &, bool, cudaStream_t); \
     template cudaError_t launch_ax_local<P>(const nb_handle *, const void *, void *, bool, cudaStream_t);      \
     template int grid_k1<P>(const nb_handle *);                                                               \
     template int grid_k2<P>(const nb_handle *);                                                               \
     template int grid_mega<P>(const nb_handle *);                                                             \
+    template int grid_mega_var<P, 0>(const nb_handle *);                                                      \
     template cudaError_t launch_cg_init<P>(const nb_handle *, Workspace &, const void *, cudaStream_t);        \
     template cudaError_t launch_cg_k1<P>(const nb_handle *, Workspace &, bool, cudaStream_t);                 \
     template cudaError_t launch_cg_k2<P>(const nb_handle *, Workspace &, bool, cudaStream_t,                  \
                                          cudaGraphConditionalHandle, bool);                                   \
     template cudaError_t launch_cg_fin<P>(const nb_handle *, Workspace &, cudaStream_t);                      \
     template cudaError_t launch_cg_mega<P>(const nb_handle *, Workspace &, const void *, int, int, double,    \
-                                           unsigned long long *, cudaStream_t);
+                                           int, int, unsigned long long *, cudaStream_t);                     \
+    template cudaError_t launch_cg_mega_var<P, 0>(const nb_handle *, const MegaArgs &, bool, cudaStream_t);
+// the variant (VAR = 1) megakernels: their own translation units (parallel build)
+#define NB_INSTANTIATE_CG_VAR(P)                                                                              \
+    template int grid_mega_var<P, 1>(const nb_handle *);                                                      \
+    template cudaError_t launch_cg_mega_var<P, 1>(const nb_handle *, const MegaArgs &, bool, cudaStream_t);
 
 }  // namespace nb

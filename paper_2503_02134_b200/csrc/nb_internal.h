@@ -44,6 +44,7 @@ struct MeshDev {
 struct Workspace {          // per-policy CG workspace (lazily allocated)
     bool ready = false;
     void *r = nullptr, *p = nullptr, *w = nullptr, *x = nullptr, *z = nullptr;
+    double *xd = nullptr;       // x accumulated in double (x_fp64 option), lazily allocated
     RedWs red = {nullptr, nullptr, nullptr};
     Scal *scal = nullptr;       // device scalars
     Scal *scal_host = nullptr;  // pinned mirror
@@ -125,7 +126,12 @@ template <int PREC> cudaError_t launch_cg_k2(const nb_handle *h, Workspace &ws, 
 template <int PREC> cudaError_t launch_cg_fin(const nb_handle *h, Workspace &ws, cudaStream_t st);
 // the whole solve as one persistent cooperative kernel (grid size: grid_mega)
 template <int PREC> int grid_mega(const nb_handle *h);
+struct MegaArgs;
+template <int PREC, int VAR> int grid_mega_var(const nb_handle *h);
+template <int PREC, int VAR>
+cudaError_t launch_cg_mega_var(const nb_handle *h, const MegaArgs &A, bool fused, cudaStream_t st);
 template <int PREC> cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int order,
-                                              int max_iter, double rtol, unsigned long long *tim, cudaStream_t st);
+                                              int max_iter, double rtol, int precond, int x64,
+                                              unsigned long long *tim, cudaStream_t st);
 
 }  // namespace nb

@@ -448,26 +448,26 @@ k_cg_mega_tma(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<t
 
 // ---- megakernel launchers: the TMA-staged variant where its bulk copies apply (even N and
 // the 2-stage ring fits in shared memory), the register-staged one otherwise ----
-template <int PREC, int N, int FUSED, bool TMA>
+template <int PREC, int N, int FUSED, bool TMA, int VAR>
 struct MegaSel {
     static const void *fn()
     {
         if constexpr (TMA) return (const void *)k_cg_mega_tma<PREC, N, FUSED>;
-        else return (const void *)k_cg_mega<PREC, N, FUSED>;
+        else return (const void *)k_cg_mega<PREC, N, FUSED, VAR>;
     }
     static int nt() { return TMA ? TmaCfg<PREC, N>::NT : AxCfg<typename Pol<PREC>::TV, N>::NT; }
     static int smem() { return TMA ? TmaCfg<PREC, N>::SMEM : AxCfg<typename Pol<PREC>::TV, N>::SMEM; }
 };
 
 // The TMA-staged variant measured slower than the register-streamed one on B200 (DESIGN.md
-// §6): compiled only with -DNB_WITH_TMA=1 and then selected by NB_MEGA_TMA=1.
+// §6): compiled only with -DNB_WITH_TMA=1 and then selected by NB_MEGA_TMA=1 (default options).
 #ifndef NB_WITH_TMA
 #define NB_WITH_TMA 0
 #endif
-template <int PREC, int N>
+template <int PREC, int N, int VAR>
 constexpr bool use_tma()
 {
-    return NB_WITH_TMA && PREC != NB_FP32_DOT2 && TmaCfg<PREC, N>::OK;
+    return NB_WITH_TMA && VAR == 0 && PREC != NB_FP32_DOT2 && TmaCfg<PREC, N>::OK;
 }
 
 static bool env_no_tma()
@@ -480,10 +480,10 @@ static bool env_no_tma()
     return v == 1;
 }
 
-template <int PREC, int N, int FUSED, bool TMA>
+template <int PREC, int N, int FUSED, bool TMA, int VAR>
 static int mega_grid_t(const nb_handle *h)
 {
-    using Sel = MegaSel<PREC, N, FUSED, TMA>;
+    using Sel = MegaSel<PREC, N, FUSED, TMA, VAR>;
     static int occ = -1;
     if (occ < 0) {
         cudaFuncSetAttribute(Sel::fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, Sel::smem());
@@ -494,48 +494,67 @@ static int mega_grid_t(const nb_handle *h)
     return h->sm_count * occ;
 }
 
-template <int PREC, int N, int FUSED>
+template <int PREC, int N, int FUSED, int VAR>
 static int mega_grid_sel(const nb_handle *h)
 {
-    if (use_tma<PREC, N>() && !env_no_tma()) return mega_grid_t<PREC, N, FUSED, use_tma<PREC, N>()>(h);
-    return mega_grid_t<PREC, N, FUSED, false>(h);
+    if (use_tma<PREC, N, VAR>() && !env_no_tma()) return mega_grid_t<PREC, N, FUSED, use_tma<PREC, N, VAR>(), VAR>(h);
+    return mega_grid_t<PREC, N, FUSED, false, VAR>(h);
 }
 
+template <int PREC, int VAR>
+int grid_mega_var(const nb_handle *h)
+{
+    NB_DISPATCH_N(h->n, return (mega_grid_sel<PREC, NN, 1, VAR>(h) > mega_grid_sel<PREC, NN, 0, VAR>(h)
+                                    ? mega_grid_sel<PREC, NN, 1, VAR>(h)
+                                    : mega_grid_sel<PREC, NN, 0, VAR>(h)))
+}
+
+// grid size of every megakernel of the policy (sizes the per-block partials)
 template <int PREC>
 int grid_mega(const nb_handle *h)
 {
-    NB_DISPATCH_N(h->n, return (mega_grid_sel<PREC, NN, 1>(h) > mega_grid_sel<PREC, NN, 0>(h)
-                                    ? mega_grid_sel<PREC, NN, 1>(h)
-                                    : mega_grid_sel<PREC, NN, 0>(h)))
+    const int g0 = grid_mega_var<PREC, 0>(h), g1 = grid_mega_var<PREC, 1>(h);
+    return g0 > g1 ? g0 : g1;
 }
 
-template <int PREC, int N, int FUSED>
+template <int PREC, int N, int FUSED, int VAR>
 static cudaError_t mega_launch_t(const nb_handle *h, const MegaArgs &args, cudaStream_t st)
 {
     using TV = typename Pol<PREC>::TV;
-    const bool tma = use_tma<PREC, N>() && !env_no_tma();
+    const bool tma = use_tma<PREC, N, VAR>() && !env_no_tma();
     DMat<TV, N> D = make_dmat<TV, N>(h->D);
     void *params[2] = {(void *)&args, (void *)&D};
     if (tma) {
-        using Sel = MegaSel<PREC, N, FUSED, use_tma<PREC, N>()>;
-        const int grid = mega_grid_t<PREC, N, FUSED, use_tma<PREC, N>()>(h);
+        using Sel = MegaSel<PREC, N, FUSED, use_tma<PREC, N, VAR>(), VAR>;
+        const int grid = mega_grid_t<PREC, N, FUSED, use_tma<PREC, N, VAR>(), VAR>(h);
         return cudaLaunchCooperativeKernel(Sel::fn(), dim3(grid), dim3(Sel::nt()), params, (size_t)Sel::smem(), st);
     }
-    using Sel = MegaSel<PREC, N, FUSED, false>;
-    const int grid = mega_grid_t<PREC, N, FUSED, false>(h);
+    using Sel = MegaSel<PREC, N, FUSED, false, VAR>;
+    const int grid = mega_grid_t<PREC, N, FUSED, false, VAR>(h);
     return cudaLaunchCooperativeKernel(Sel::fn(), dim3(grid), dim3(Sel::nt()), params, (size_t)Sel::smem(), st);
+}
+
+template <int PREC, int VAR>
+cudaError_t launch_cg_mega_var(const nb_handle *h, const MegaArgs &A, bool fused, cudaStream_t st)
+{
+    if (fused) { NB_DISPATCH_N(h->n, return (mega_launch_t<PREC, NN, 1, VAR>(h, A, st))) }
+    NB_DISPATCH_N(h->n, return (mega_launch_t<PREC, NN, 0, VAR>(h, A, st)))
 }
 
 template <int PREC>
 cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int order, int max_iter, double rtol,
-                           unsigned long long *tim, cudaStream_t st)
+                           int precond, int x64, unsigned long long *tim, cudaStream_t st)
 {
     MegaArgs A;
     A.m = h->md();
     A.b = b;
-    A.x = ws.x; A.p = ws.p; A.r = ws.r; A.z = ws.z; A.w = ws.w;
+    A.pc = precond;
+    A.x64 = (PREC == NB_MIXED && x64) ? 1 : 0;
+    A.x = A.x64 ? (void *)ws.xd : ws.x; A.p = ws.p; A.r = ws.r; A.w = ws.w;
+    A.z = precond == NB_PC_IDENTITY ? ws.r : ws.z;   // identity: z aliases r (never stored)
     A.g = (sizeof(typename Pol<PREC>::TV) == 8) ? (const void *)h->g64 : (const void *)h->g32;
-    A.dinv = sizeof(typename Pol<PREC>::TJ) == 4 ? (const void *)h->dinv32 : (const void *)h->dinv64;
+    A.dinv = (sizeof(typename Pol<PREC>::TJ) == 4 || precond == NB_PC_JACOBI_F32) ? (const void *)h->dinv32
+                                                                                  : (const void *)h->dinv64;
     A.gs_off = h->gs_off; A.gs_idx = h->gs_idx; A.nseg = (int32_t)h->nseg;
     A.order = order; A.max_iter = max_iter; A.rtol = rtol;
     A.hist = ws.hist; A.tim = tim;
@@ -547,8 +566,8 @@ cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int
     const bool fused = order == NB_GS_CONSISTENT && !h->cg_csr;
     cudaError_t e = cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned int), st);   // barrier epoch 0
     if (e != cudaSuccess) return e;
-    if (fused) { NB_DISPATCH_N(h->n, return (mega_launch_t<PREC, NN, 1>(h, A, st))) }
-    NB_DISPATCH_N(h->n, return (mega_launch_t<PREC, NN, 0>(h, A, st)))
+    const bool var = precond != NB_PC_JACOBI || A.x64;
+    return var ? launch_cg_mega_var<PREC, 1>(h, A, fused, st) : launch_cg_mega_var<PREC, 0>(h, A, fused, st);
 }
 
 }  // namespace nb

@@ -6,4 +6,3 @@ for v in head nb; do
   NB_LIBPATH=$lib python tools/sweep.py --cases 16x16x16p7 32x32x32p7 32x32x32p9d --policies fp64 fp32 mixed --iters 200 --reps 3 > gpurun_out/var_${v}_$rep.log 2>&1
 done
 done
-python tools/sweep.py --cases 16x16x16p7 32x32x32p7 --policies fp32_dot2 --iters 200 --reps 3 > gpurun_out/var_dot2.log 2>&1
