@@ -10,8 +10,13 @@ dots and Jacobi).  One step = one complete nb_cg solve (all SURVEY.md §8(a) per
 rows a5..a12; setup a1..a4 is done once before timing, like Nekbone's solve time).
 value = local DOF x iterations / solve time, summed over ranks / max-over-ranks time.
 
-Multi-GPU: the single-GPU solve is replicated (independent problems per rank, no
-data-path collective) -> "scaling": "weak"; DESIGN.md §7 explains why.
+Multi-GPU (--mode replicas, default): the single-GPU solve is replicated (independent problems
+per rank, no data-path collective) -> "scaling": "weak".  --mode slab: ONE box of 16x16x(16 N)
+elements split into N z-slabs, one per rank/GPU (configs[1] per GPU, weak scaling), solved by
+the multi-rank megakernel that reads the neighbour slabs' interface layers over NVLink peer
+memory (CUDA IPC) and reduces the dot products across ranks in-kernel (SURVEY.md §8(e));
+with one GPU, --mode slab --slabs K runs K slabs of one box in one launch (the emulation the
+multi-rank path is tested with).  DESIGN.md §7.
 --impl reference times the oracle (plain C, one core) on bounded samples of the same
 workload (the tier's reference arm).
 """
@@ -224,17 +229,36 @@ def run_ours(args):
     dev = local if world > 1 else 0
     torch.cuda.set_device(dev)
     pol = POLICIES[args.policy]
-    nel, p = WORKLOAD["nel"], WORKLOAD["p"]
-    mesh = nb.Mesh(*nel, p, deform=0.0, seed=0, device=dev)
-    NL = mesh.n_local
+    nel, p = list(WORKLOAD["nel"]), WORKLOAD["p"]
+    slab = args.mode == "slab"
+    group = []
+    if slab:
+        args.quick = True        # the per-policy table / companion run on rank 0 alone
+        if world > 1:
+            nel[2] = WORKLOAD["nel"][2] * world          # configs[1] per GPU, stacked along z
+            mesh = nb.Mesh(*nel, p, deform=0.0, seed=0, device=dev, slab=nb.slab_bounds(nel[2], world, rank))
+            nb.peer_attach_dist(mesh, pol)
+        else:
+            K = args.slabs
+            group = [nb.Mesh(*nel, p, deform=0.0, seed=0, device=dev, slab=nb.slab_bounds(nel[2], K, r))
+                     for r in range(K)]
+            mesh = group[0]
+    else:
+        mesh = nb.Mesh(*nel, p, deform=0.0, seed=0, device=dev)
+    NL = sum(m.n_local for m in group) if group else mesh.n_local
     info = mesh.info
     b = mesh.rhs(pol, nb.NB_RHS_UNIFORM, seed=0)
     x = mesh.empty(pol)
+    gb = [m.rhs(pol, nb.NB_RHS_UNIFORM, seed=0) for m in group]
+    gx = [m.empty(pol) for m in group]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
     max_iter = 4000
     st = torch.cuda.current_stream()
 
     def solve(time_kernels=False):
+        if group:
+            reps, _ = nb.nb_cg_group([m.h for m in group], gb, gx, pol, max_iter, WORKLOAD["rtol"], history=False)
+            return reps[0]
         rep, _ = nb.nb_cg(mesh.h, b, x, pol, max_iter, WORKLOAD["rtol"], time_kernels=time_kernels, history=False)
         return rep
 
@@ -286,18 +310,22 @@ def run_ours(args):
         pass
 
     # e2e: the public host-buffer call, pinned host b/x, copies inside the timed region
-    bh = b.cpu().pin_memory()
-    xh = torch.empty_like(bh).pin_memory()
-    e2e_t, e2e_it = 0.0, 0
-    for s in range(args.steps):
-        flush.zero_()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        rep, _ = nb.nb_cg_host(mesh.h, bh, xh, pol, max_iter, WORKLOAD["rtol"])
-        e2e_t += time.perf_counter() - t0
-        e2e_it += rep.iterations
-    e2e_t = max_over_ranks(e2e_t, world)
-    e2e_val = sum_over_ranks(float(NL * e2e_it), world) / e2e_t
+    e2e = None
+    if not group:
+        bh = b.cpu().pin_memory()
+        xh = torch.empty_like(bh).pin_memory()
+        e2e_t, e2e_it = 0.0, 0
+        barrier_sync(world)
+        for s in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rep, _ = nb.nb_cg_host(mesh.h, bh, xh, pol, max_iter, WORKLOAD["rtol"])
+            e2e_t += time.perf_counter() - t0
+            e2e_it += rep.iterations
+        e2e_t = max_over_ranks(e2e_t, world)
+        e2e_val = sum_over_ranks(float(NL * e2e_it), world) / e2e_t
+        e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": NL * SV[pol], "d2h_bytes_per_step": NL * SV[pol]}
 
     # time-to-1e-8 for every policy (reported next to the headline; not the timed region)
     ttr = {}
@@ -361,7 +389,10 @@ def run_ours(args):
                 "data": "synthetic",
                 "config": dict(WORKLOAD, policy=args.policy, iterations=iters[0], status=sorted(statuses),
                                n_local=NL, l2="256 MiB write between steps (outside the step events)",
-                               parallelism="replicas" if world > 1 else "single GPU"),
+                               parallelism=(f"z-slabs over {world} GPUs (NVLink peer memory)" if slab and world > 1
+                                            else f"{len(group)} z-slabs in one launch on one GPU" if group
+                                            else "replicas" if world > 1 else "single GPU"),
+                               **({"nel": nel} if slab else {})),
                 "time_to_rtol_ms": ms_per_step,
                 "step_ms": {"events_around_call": step_ms, "library_device_ms": lib_ms},
                 "roofline": {"bound": "hbm",
@@ -383,11 +414,12 @@ def run_ours(args):
                     "dssum_csr": {"avg_us": 1e3 * gs_ms, "alg_bytes": gs_bytes,
                                   "GBps": gs_bytes / (gs_ms * 1e-3) / 1e9,
                                   "frac": gs_bytes / (gs_ms * 1e-3) / 1e9 / peak}},
-                "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": NL * vs, "d2h_bytes_per_step": NL * vs},
+                "e2e": e2e,
                 "gpu_launches": launches, "clocks": ck, "cpu_baseline": cpu, "policies": ttr,
                 "hbm_bound_companion": large}
         print(json.dumps(line), flush=True)
-    mesh.close()
+    for m in group or [mesh]:
+        m.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
@@ -406,6 +438,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip the per-policy table and the large companion")
     ap.add_argument("--no-large", action="store_true", help="skip the HBM-bound configs[2] companion point")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "slab"],
+                    help="N>1: independent replicas, or one box split in z-slabs over the GPUs")
+    ap.add_argument("--slabs", type=int, default=2, help="--mode slab on one GPU: slabs in the launch")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

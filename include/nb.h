@@ -84,8 +84,10 @@ enum { NB_CONVERGED = 0, NB_MAXITER = 1, NB_STAGNATED = 2, NB_BROKEDOWN = 3 };
 enum { NB_AX_LOCAL = 1u };   /* w = A_L u only: no gather-scatter, no mask */
 
 typedef struct {
-    int64_t E, n_local, n_global, n_unmasked, n_shared_global, n_shared_copies;
-    int32_t p, nelx, nely, nelz;
+    int64_t E, n_local, n_global, n_unmasked, n_shared_global, n_shared_copies;  /* E, n_local, n_shared_*:
+                                            this handle's slab; n_global, n_unmasked: the whole box */
+    int32_t p, nelx, nely, nelz;           /* nelz: the whole box */
+    int32_t ez0, nelz_local;               /* the slab's first z layer and layer count (box: 0, nelz) */
 } nb_info;
 
 /* Preconditioner of nb_cg:
@@ -129,6 +131,17 @@ typedef struct {
 int nb_setup(int32_t nelx, int32_t nely, int32_t nelz, int32_t p, double deform_amp, uint64_t seed,
              int32_t device, nb_handle **out);
 int nb_destroy(nb_handle *h);                 /* NULL is a no-op; frees all device memory */
+
+/* A z-slab of the same box for multi-GPU runs: the elements with
+ * ez0 <= ez < ez1 (element e = ex + nelx*(ey + nely*(ez - ez0)) locally, vectors hold only them).
+ * Global numbering, mask, multiplicity c and geometry are those of the whole box; the Jacobi
+ * diagonal and the manufactured RHS include the neighbour slabs' contributions (computed
+ * redundantly on a one-ghost-layer twin, bit-identical to the whole box).  nb_ax / nb_dssum act
+ * on the slab alone; nb_cg on a slab needs its neighbours: nb_cg_group (slabs on one device, one
+ * launch) or nb_peer_attach (one slab per process/GPU).  nb_setup = nb_setup_slab(.., 0, nelz, ..).
+ * Errors as nb_setup, plus NB_EINVAL unless 0 <= ez0 < ez1 <= nelz. */
+int nb_setup_slab(int32_t nelx, int32_t nely, int32_t nelz, int32_t ez0, int32_t ez1, int32_t p,
+                  double deform_amp, uint64_t seed, int32_t device, nb_handle **out);
 int nb_query(const nb_handle *h, nb_info *out);
 
 /* Fill device vector b (policy precision of `prec`) with a right-hand side. Async. */
@@ -154,6 +167,31 @@ int nb_cg(nb_handle *h, const nb_cg_opts *o, const void *b, void *x, nb_cg_repor
 /* Same solve with HOST buffers (pinned or pageable): copies b in and x out on `stream`. */
 int nb_cg_host(nb_handle *h, const nb_cg_opts *o, const void *b_host, void *x_host,
                nb_cg_report *rep, void *stream);
+
+/* ---- multi-rank z-slab solves (slabs from nb_setup_slab) ----
+ * The z-slabs of one box are solved together: Ax stays slab-local; the phase-B gather reads
+ * the neighbour slabs' w of the interface layers directly (peer memory over NVLink, or plain
+ * device memory for slabs on one GPU), and the three dot products are reduced per rank, the
+ * rank partials pushed into every rank's control block and merged in rank order (every rank
+ * takes bit-identical scalar decisions).  Consistent GS order, fused megakernel only
+ * (NB_EINVAL otherwise); the per-slab reports carry the same iterations/status/residuals. */
+
+/* Slabs of one box that share a GPU (1 <= nslab <= 4, bottom to top, tiling the box): one
+ * cooperative launch over all of them.  b[r], x[r]: slab r's device vectors; reps: nslab reports.
+ * This is also how the multi-rank path is verified on one GPU. */
+int nb_cg_group(nb_handle *const *hs, int32_t nslab, const nb_cg_opts *o, const void *const *b,
+                void *const *x, nb_cg_report *reps, void *stream);
+
+/* One slab per process/GPU: each rank exports an NB_PEER_BLOB_BYTES blob (CUDA IPC handles of
+ * its policy workspace's w and control block), the blobs are exchanged (e.g. all_gather over
+ * torch.distributed), and every rank attaches with all nrank blobs in rank order (rank r holds
+ * the r-th slab from the bottom).  Afterwards nb_cg / nb_cg_host on this handle and policy run the
+ * multi-rank solve; every rank must call them with the same options.  All ranks must attach before
+ * any rank solves.  Errors: NB_EINVAL (bad blobs, slabs not tiling the box), NB_ECUDA (IPC). */
+#define NB_PEER_BLOB_BYTES 256
+int nb_peer_export(nb_handle *h, nb_policy policy, void *blob);
+int nb_peer_attach(nb_handle *h, nb_policy policy, int32_t nrank, int32_t rank, const void *blobs);
+int nb_peer_detach(nb_handle *h, nb_policy policy);
 
 /* Host copies of the integer maps (caller-allocated host arrays, each nullable):
  * gid[n_local], mask[n_local], gs_off[n_shared_global+1], gs_idx[n_shared_copies]. */

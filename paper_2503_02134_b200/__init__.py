@@ -28,8 +28,11 @@ NB_CONVERGED, NB_MAXITER, NB_STAGNATED, NB_BROKEDOWN = 0, 1, 2, 3
 NB_OK, NB_EINVAL, NB_ENOMEM, NB_ECUDA, NB_EGEOM, NB_EBREAKDOWN, NB_ESTATE = range(7)
 POLICY_NAMES = {NB_FP64: "fp64", NB_FP32: "fp32", NB_MIXED: "mixed", NB_FP32_DOT2: "fp32_dot2"}
 
-EXPORTED = ["nb_setup", "nb_destroy", "nb_query", "nb_rhs", "nb_ax", "nb_dssum", "nb_cg", "nb_cg_host",
-            "nb_export_maps", "nb_export_geom", "nb_export_basis", "nb_last_error", "nb_version"]
+EXPORTED = ["nb_setup", "nb_setup_slab", "nb_destroy", "nb_query", "nb_rhs", "nb_ax", "nb_dssum", "nb_cg",
+            "nb_cg_host", "nb_cg_group", "nb_peer_export", "nb_peer_attach", "nb_peer_detach", "nb_export_maps",
+            "nb_export_geom", "nb_export_basis", "nb_last_error", "nb_version"]
+NB_PEER_BLOB_BYTES = 256
+NB_MAX_LOCAL_SLABS = 4
 
 
 class NbError(RuntimeError):
@@ -41,7 +44,8 @@ class NbError(RuntimeError):
 class nb_info(C.Structure):
     _fields_ = [("E", C.c_int64), ("n_local", C.c_int64), ("n_global", C.c_int64), ("n_unmasked", C.c_int64),
                 ("n_shared_global", C.c_int64), ("n_shared_copies", C.c_int64), ("p", C.c_int32),
-                ("nelx", C.c_int32), ("nely", C.c_int32), ("nelz", C.c_int32)]
+                ("nelx", C.c_int32), ("nely", C.c_int32), ("nelz", C.c_int32), ("ez0", C.c_int32),
+                ("nelz_local", C.c_int32)]
 
 
 class nb_cg_opts(C.Structure):
@@ -72,6 +76,14 @@ def lib(auto_build: bool = True):
     L = C.CDLL(LIB)
     P, I, U64, D = C.c_void_p, C.c_int, C.c_uint64, C.c_double
     L.nb_setup.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, D, U64, C.c_int32, C.POINTER(P)]
+    if hasattr(L, "nb_setup_slab"):   # (older builds used in A/B runs lack the slab entry points)
+        L.nb_setup_slab.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, D, U64,
+                                    C.c_int32, C.POINTER(P)]
+        L.nb_cg_group.argtypes = [C.POINTER(P), C.c_int32, C.POINTER(nb_cg_opts), C.POINTER(P), C.POINTER(P),
+                                  C.POINTER(nb_cg_report), P]
+        L.nb_peer_export.argtypes = [P, I, P]
+        L.nb_peer_attach.argtypes = [P, I, C.c_int32, C.c_int32, P]
+        L.nb_peer_detach.argtypes = [P, I]
     L.nb_destroy.argtypes = [P]
     L.nb_query.argtypes = [P, C.POINTER(nb_info)]
     L.nb_rhs.argtypes = [P, I, D, U64, I, P, P]
@@ -129,8 +141,81 @@ def nb_setup(nelx: int, nely: int, nelz: int, p: int, deform_amp: float = 0.0, s
     return h
 
 
+def nb_setup_slab(nelx: int, nely: int, nelz: int, ez0: int, ez1: int, p: int, deform_amp: float = 0.0, seed: int = 0,
+                  device: int = 0):
+    h = C.c_void_p()
+    _check(lib().nb_setup_slab(nelx, nely, nelz, ez0, ez1, p, deform_amp, seed, device, C.byref(h)))
+    return h
+
+
 def nb_destroy(h):
     _check(lib().nb_destroy(h))
+
+
+def slab_bounds(nelz: int, nrank: int, rank: int):
+    """z-layers [ez0, ez1) of rank `rank` when nelz layers are split over nrank slabs as evenly
+    as possible (the first nelz % nrank slabs hold one extra layer)."""
+    if not 1 <= nrank <= nelz or not 0 <= rank < nrank:
+        raise ValueError("need 1 <= nrank <= nelz and 0 <= rank < nrank")
+    q, r = divmod(nelz, nrank)
+    ez0 = rank * q + min(rank, r)
+    return ez0, ez0 + q + (1 if rank < r else 0)
+
+
+def nb_cg_group(hs, bs, xs, policy: int = NB_MIXED, max_iter: int = 1000, rtol: float = 1e-8,
+                stag_window: int = 200, precond: int = NB_PC_JACOBI, x64: bool = False, stream=None,
+                history: bool = True):
+    """One solve over the z-slabs hs (bottom to top) of a box on one GPU: one cooperative launch.
+    Returns (reports, rel_res_history)."""
+    import torch
+    n = len(hs)
+    dt = policy_dtype(policy)
+    hist = np.zeros(max_iter + 1) if history else None
+    o = _opts(policy, max_iter, rtol, NB_GS_CONSISTENT, stag_window, False, hist, precond, x64)
+    reps = (nb_cg_report * n)()
+    H = (C.c_void_p * n)(*[h.value if isinstance(h, C.c_void_p) else h for h in hs])
+    B = (C.c_void_p * n)(*[_dptr(b, dt).value for b in bs])
+    X = (C.c_void_p * n)(*[_dptr(x, torch.float64 if x64 else dt).value for x in xs])
+    rc = lib().nb_cg_group(H, n, C.byref(o), B, X, reps, _stream(stream))
+    if rc not in (NB_OK, NB_EBREAKDOWN):
+        _check(rc)
+    return list(reps), (hist[: reps[0].iterations + 1] if hist is not None else None)
+
+
+def nb_peer_export(h, policy: int) -> bytes:
+    buf = (C.c_ubyte * NB_PEER_BLOB_BYTES)()
+    _check(lib().nb_peer_export(h, policy, buf))
+    return bytes(buf)
+
+
+def nb_peer_attach(h, policy: int, nrank: int, rank: int, blobs: bytes):
+    if len(blobs) != nrank * NB_PEER_BLOB_BYTES:
+        raise ValueError("need nrank blobs of NB_PEER_BLOB_BYTES")
+    buf = (C.c_ubyte * len(blobs)).from_buffer_copy(blobs)
+    _check(lib().nb_peer_attach(h, policy, nrank, rank, buf))
+
+
+def nb_peer_detach(h, policy: int):
+    _check(lib().nb_peer_detach(h, policy))
+
+
+def exchange_blobs(blob: bytes, group=None) -> bytes:
+    """All ranks' peer blobs concatenated in rank order (all_gather over torch.distributed, any
+    backend; host bytes only)."""
+    import torch.distributed as dist
+    if len(blob) != NB_PEER_BLOB_BYTES:
+        raise ValueError("blob must be NB_PEER_BLOB_BYTES long")
+    blobs = [None] * dist.get_world_size(group)
+    dist.all_gather_object(blobs, bytes(blob), group=group)
+    return b"".join(blobs)
+
+
+def peer_attach_dist(mesh, policy: int, group=None):
+    """Attach this rank's slab (rank r = the r-th slab from the bottom) to its peers."""
+    import torch.distributed as dist
+    blobs = exchange_blobs(nb_peer_export(mesh.h, policy), group)
+    nb_peer_attach(mesh.h, policy, len(blobs) // NB_PEER_BLOB_BYTES, dist.get_rank(group), blobs)
+    dist.barrier(group)   # every rank attached (flags zeroed) before any rank solves
 
 
 def nb_query(h) -> nb_info:
@@ -251,8 +336,13 @@ class CgResult:
 class Mesh:
     """Owning wrapper of an nb_handle (frees device memory on close/deletion)."""
 
-    def __init__(self, nelx, nely, nelz, p, deform=0.0, seed=0, device=0):
-        self.h = nb_setup(nelx, nely, nelz, p, deform, seed, device)
+    def __init__(self, nelx, nely, nelz, p, deform=0.0, seed=0, device=0, slab=None):
+        """slab=(ez0, ez1): hold only the z-layers ez0 <= ez < ez1 of the box (multi-rank solves)."""
+        if slab is None:
+            self.h = nb_setup(nelx, nely, nelz, p, deform, seed, device)
+        else:
+            self.h = nb_setup_slab(nelx, nely, nelz, slab[0], slab[1], p, deform, seed, device)
+        self.slab = slab
         info = nb_query(self.h)
         self.info = info
         self.n_local = info.n_local
@@ -299,3 +389,14 @@ class Mesh:
         r = CgResult(rep.iterations, rep.status, rep.rtr0, rep.rel_res_final, rep.rel_res_min, rep.solve_ms,
                      rep.kernel_launches, rep.k_ax_ms, rep.k_gs_ms, rep.k_upd_ms, hist)
         return x, r
+
+
+def cg_group(meshes, bs, policy=NB_MIXED, max_iter=1000, rtol=1e-8, stag_window=200, precond=NB_PC_JACOBI,
+             x64=False):
+    """Solve over the z-slab Meshes of one box sharing a GPU (bottom to top): one launch.
+    Returns ([x per slab], [CgResult per slab])."""
+    xs = [m.empty(NB_FP64 if x64 else policy) for m in meshes]
+    reps, hist = nb_cg_group([m.h for m in meshes], bs, xs, policy, max_iter, rtol, stag_window, precond, x64)
+    res = [CgResult(r.iterations, r.status, r.rtr0, r.rel_res_final, r.rel_res_min, r.solve_ms, r.kernel_launches,
+                    r.k_ax_ms, r.k_gs_ms, r.k_upd_ms, hist) for r in reps]
+    return xs, res

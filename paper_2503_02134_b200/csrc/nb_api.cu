@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <unistd.h>
+
 #include "nb.h"
 #include "nb_internal.h"
 
@@ -169,6 +171,8 @@ int ensure_ws(nb_handle *h, int prec, int32_t max_iter)
         NB_CU(cudaMalloc(&ws.red.part2, sizeof(double) * 2 * nchunk), "cudaMalloc part2");
         NB_CU(cudaMalloc(&ws.red.cnt, sizeof(uint32_t) * (1 + nchunk)), "cudaMalloc cnt");
         NB_CU(cudaMemset(ws.red.cnt, 0, sizeof(uint32_t) * (1 + nchunk)), "memset cnt");
+        NB_CU(cudaMalloc(&ws.ctl, nb::NB_CTL_BYTES), "cudaMalloc ctl");
+        NB_CU(cudaMemset(ws.ctl, 0, nb::NB_CTL_BYTES), "memset ctl");
         NB_CU(cudaMalloc(&ws.scal, sizeof(nb::Scal)), "cudaMalloc scal");
         NB_CU(cudaMallocHost(&ws.scal_host, sizeof(nb::Scal)), "cudaMallocHost scal");
         NB_CU(cudaMemset(ws.scal, 0, sizeof(nb::Scal)), "memset scal");
@@ -199,7 +203,8 @@ void free_ws(nb::Workspace &ws)
         if (ws.exec[o]) cudaGraphExecDestroy(ws.exec[o]);
         if (ws.graph[o]) cudaGraphDestroy(ws.graph[o]);
     }
-    cudaFree(ws.r); cudaFree(ws.p); cudaFree(ws.w); cudaFree(ws.x); cudaFree(ws.z); cudaFree(ws.xd);
+    for (int i = 0; i < ws.peer.nopened; i++) cudaIpcCloseMemHandle(ws.peer.opened[i]);
+    cudaFree(ws.r); cudaFree(ws.p); cudaFree(ws.w); cudaFree(ws.x); cudaFree(ws.z); cudaFree(ws.xd); cudaFree(ws.ctl);
     cudaFree(ws.red.part); cudaFree(ws.red.part2); cudaFree(ws.red.cnt);
     cudaFree(ws.scal); cudaFree(ws.hist); cudaFree(ws.tim); cudaFree(ws.bar);
     if (ws.scal_host) cudaFreeHost(ws.scal_host);
@@ -300,78 +305,130 @@ extern "C" {
 const char *nb_last_error(void) { return g_err.c_str(); }
 const char *nb_version(void) { return "nb-b200 0.1 (sm_100a)"; }
 
-int nb_setup(int32_t nelx, int32_t nely, int32_t nelz, int32_t p, double deform_amp, uint64_t seed, int32_t device,
-             nb_handle **out)
+// Build the data of one handle's slab [ez0, ez0 + nelzl) of the box (every field of h set by
+// make_handle): geometry, GS segments and (when `jacobi`) the Jacobi diagonal.
+static int setup_box(nb_handle *h, bool jacobi)
 {
-    if (!out) return fail(NB_EINVAL, "out is NULL");
-    *out = nullptr;
-    if (p < 1 || p > 15) return fail(NB_EINVAL, "p must be in [1,15]");
-    if (nelx < 1 || nely < 1 || nelz < 1) return fail(NB_EINVAL, "element counts must be >= 1");
-    if (!(deform_amp >= 0.0) || deform_amp > 0.25) return fail(NB_EINVAL, "deform_amp must be in [0, 0.25]");
-    const int n = p + 1;
-    const int64_t E = (int64_t)nelx * nely * nelz;
-    const int64_t NL = E * n * n * n;
-    if (NL >= 2147483647LL) return fail(NB_EINVAL, "n_local must be < 2^31 (int32 GS indices)");
-    int ndev = 0;
-    NB_CU(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
-    if (device < 0 || device >= ndev) return fail(NB_EINVAL, "bad device ordinal");
-    NB_CU(cudaSetDevice(device), "cudaSetDevice");
-
-    nb_handle *h = new (std::nothrow) nb_handle();
-    if (!h) return fail(NB_ENOMEM, "host allocation failed");
-    h->device = device;
-    h->nelx = nelx; h->nely = nely; h->nelz = nelz; h->p = p; h->n = n;
-    h->E = E; h->NL = NL;
-    h->NX = (int64_t)nelx * p + 1; h->NY = (int64_t)nely * p + 1; h->NZ = (int64_t)nelz * p + 1;
-    h->NG = h->NX * h->NY * h->NZ;
-    h->n_unmasked = ((int64_t)nelx * p - 1) * ((int64_t)nely * p - 1) * ((int64_t)nelz * p - 1);
-    h->deform = deform_amp;
-    h->seed = seed;
-    if (!gll_basis(p, h->nodes, h->weights, h->D)) { delete h; return fail(NB_EINVAL, "GLL Newton failed"); }
-    cudaDeviceProp prop;
-    int rc = NB_OK;
-    auto bail = [&](int code) { nb_destroy(h); return code; };
-    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "props"));
-    h->sm_count = prop.multiProcessorCount;
-    if (h->NG >= 2147483647LL) return bail(fail(NB_EINVAL, "global node count must be < 2^31"));
-
+    const int64_t NL = h->NL;
     cudaError_t e;
-    if ((e = cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking)) != cudaSuccess) return bail(cuda_fail(e, "stream"));
+    if ((e = cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
     {
         const char *gs = std::getenv("NB_CG_GS");
         h->cg_csr = (gs && std::strcmp(gs, "csr") == 0) ? 1 : 0;
         const char *dr = std::getenv("NB_CG_DRIVER");
         h->cg_graph = (dr && std::strcmp(dr, "graph") == 0) ? 1 : 0;
     }
-    if ((e = cudaMalloc(&h->g64, sizeof(double) * 6 * NL)) != cudaSuccess) return bail(fail(NB_ENOMEM, "cudaMalloc g64"));
-    if ((e = cudaMalloc(&h->B, sizeof(double) * NL)) != cudaSuccess) return bail(fail(NB_ENOMEM, "cudaMalloc B"));
-    if ((e = cudaMalloc(&h->dinv64, sizeof(double) * NL)) != cudaSuccess) return bail(fail(NB_ENOMEM, "cudaMalloc dinv"));
-    if ((e = cudaMalloc(&h->flag, sizeof(int32_t))) != cudaSuccess) return bail(fail(NB_ENOMEM, "cudaMalloc flag"));
+    if ((e = cudaMalloc(&h->g64, sizeof(double) * 6 * NL)) != cudaSuccess) return fail(NB_ENOMEM, "cudaMalloc g64");
+    if ((e = cudaMalloc(&h->B, sizeof(double) * NL)) != cudaSuccess) return fail(NB_ENOMEM, "cudaMalloc B");
+    if ((e = cudaMalloc(&h->dinv64, sizeof(double) * NL)) != cudaSuccess) return fail(NB_ENOMEM, "cudaMalloc dinv");
+    if ((e = cudaMalloc(&h->flag, sizeof(int32_t))) != cudaSuccess) return fail(NB_ENOMEM, "cudaMalloc flag");
     cudaStream_t st = h->cap_stream;
-    if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int32_t), st)) != cudaSuccess) return bail(cuda_fail(e, "memset"));
+    if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int32_t), st)) != cudaSuccess) return cuda_fail(e, "memset");
     double ph[3];
-    nb::deform_phases(seed, ph);
-    if ((e = nb::launch_geometry(h, ph, st)) != cudaSuccess) return bail(cuda_fail(e, "geometry"));
-    if ((e = nb::build_gs(h, st)) != cudaSuccess) return bail(cuda_fail(e, "gs segments"));
+    nb::deform_phases(h->seed, ph);
+    if ((e = nb::launch_geometry(h, ph, st)) != cudaSuccess) return cuda_fail(e, "geometry");
+    if ((e = nb::build_gs(h, st)) != cudaSuccess) return cuda_fail(e, "gs segments");
     double *diag = nullptr;
-    if ((e = cudaMalloc(&diag, sizeof(double) * NL)) != cudaSuccess) return bail(fail(NB_ENOMEM, "cudaMalloc diag"));
-    e = nb::launch_jacobi(h, diag, st);
+    if (jacobi) {
+        if ((e = cudaMalloc(&diag, sizeof(double) * NL)) != cudaSuccess) return fail(NB_ENOMEM, "cudaMalloc diag");
+        e = nb::launch_jacobi(h, diag, st);
+    }
     int32_t flag = 0;
     if (e == cudaSuccess) e = cudaMemcpyAsync(&flag, h->flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFree(diag);
-    if (e != cudaSuccess) return bail(cuda_fail(e, "jacobi"));
-    if (flag & 1) return bail(fail(NB_EGEOM, "non-positive Jacobian"));
-    if (flag & 2) return bail(fail(NB_EGEOM, "non-positive Jacobi diagonal"));
-    (void)rc;
+    if (e != cudaSuccess) return cuda_fail(e, "jacobi");
+    if (flag & 1) return fail(NB_EGEOM, "non-positive Jacobian");
+    if (flag & 2) return fail(NB_EGEOM, "non-positive Jacobi diagonal");
+    return NB_OK;
+}
+
+static nb_handle *make_handle(int32_t nelx, int32_t nely, int32_t nelz, int32_t ez0, int32_t ez1, int32_t p,
+                              double deform_amp, uint64_t seed, int32_t device, int sm_count)
+{
+    nb_handle *h = new (std::nothrow) nb_handle();
+    if (!h) return nullptr;
+    const int n = p + 1;
+    h->device = device;
+    h->nelx = nelx; h->nely = nely; h->nelz = nelz; h->p = p; h->n = n;
+    h->ez0 = ez0; h->nelzl = ez1 - ez0;
+    h->E = (int64_t)nelx * nely * h->nelzl;
+    h->NL = h->E * n * n * n;
+    h->NX = (int64_t)nelx * p + 1; h->NY = (int64_t)nely * p + 1; h->NZ = (int64_t)nelz * p + 1;
+    h->NG = h->NX * h->NY * h->NZ;
+    h->NZl = (int64_t)h->nelzl * p + 1;
+    h->NGl = h->NX * h->NY * h->NZl;
+    h->n_unmasked = ((int64_t)nelx * p - 1) * ((int64_t)nely * p - 1) * ((int64_t)nelz * p - 1);
+    h->deform = deform_amp;
+    h->seed = seed;
+    h->sm_count = sm_count;
+    if (!gll_basis(p, h->nodes, h->weights, h->D)) { delete h; return nullptr; }
+    return h;
+}
+
+int nb_setup_slab(int32_t nelx, int32_t nely, int32_t nelz, int32_t ez0, int32_t ez1, int32_t p, double deform_amp,
+                  uint64_t seed, int32_t device, nb_handle **out)
+{
+    if (!out) return fail(NB_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (p < 1 || p > 15) return fail(NB_EINVAL, "p must be in [1,15]");
+    if (nelx < 1 || nely < 1 || nelz < 1) return fail(NB_EINVAL, "element counts must be >= 1");
+    if (ez0 < 0 || ez1 > nelz || ez0 >= ez1) return fail(NB_EINVAL, "slab must satisfy 0 <= ez0 < ez1 <= nelz");
+    if (!(deform_amp >= 0.0) || deform_amp > 0.25) return fail(NB_EINVAL, "deform_amp must be in [0, 0.25]");
+    const int n = p + 1;
+    // the slab (and its ghost-extended twin) must fit the int32 local indexing
+    const int32_t ghosts = (ez0 > 0) + (ez1 < nelz);
+    if ((int64_t)nelx * nely * (int64_t)(ez1 - ez0 + ghosts) * n * n * n >= 2147483647LL)
+        return fail(NB_EINVAL, "n_local must be < 2^31 (int32 GS indices)");
+    int ndev = 0;
+    NB_CU(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) return fail(NB_EINVAL, "bad device ordinal");
+    NB_CU(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    NB_CU(cudaGetDeviceProperties(&prop, device), "props");
+    const int64_t NX = (int64_t)nelx * p + 1, NY = (int64_t)nely * p + 1, NZ = (int64_t)nelz * p + 1;
+    if (NX * NY * NZ >= 2147483647LL) return fail(NB_EINVAL, "global node count must be < 2^31");
+
+    nb_handle *h = make_handle(nelx, nely, nelz, ez0, ez1, p, deform_amp, seed, device, prop.multiProcessorCount);
+    if (!h) return fail(NB_ENOMEM, "host allocation or GLL Newton failed");
+    const bool whole = ez0 == 0 && ez1 == nelz;
+    int rc;
+    if (whole) {
+        if ((rc = setup_box(h, true))) { nb_destroy(h); return rc; }
+    } else {
+        // The Jacobi diagonal (and the manufactured RHS) of the slab's interface nodes need the
+        // neighbour slabs' element contributions: computed redundantly on a twin slab with one
+        // ghost layer per side (closed-form geometry), so setup needs no communication.  Same
+        // elements, same ascending-element summation order: bit-identical to the whole box.
+        const int32_t x0 = ez0 > 0 ? ez0 - 1 : 0, x1 = ez1 < nelz ? ez1 + 1 : nelz;
+        nb_handle *x = make_handle(nelx, nely, nelz, x0, x1, p, deform_amp, seed, device, prop.multiProcessorCount);
+        if (!x) { delete h; return fail(NB_ENOMEM, "host allocation failed"); }
+        h->ext = x;
+        h->ext_off = (int64_t)(ez0 - x0) * nelx * nely;
+        if ((rc = setup_box(x, true)) || (rc = setup_box(h, false))) { nb_destroy(h); return rc; }
+        const size_t n3 = (size_t)n * n * n;
+        cudaError_t e = cudaMemcpy(h->dinv64, x->dinv64 + h->ext_off * n3, sizeof(double) * h->NL, cudaMemcpyDeviceToDevice);
+        if (e != cudaSuccess) { nb_destroy(h); return cuda_fail(e, "slab dinv"); }
+    }
     *out = h;
     return NB_OK;
+}
+
+int nb_setup(int32_t nelx, int32_t nely, int32_t nelz, int32_t p, double deform_amp, uint64_t seed, int32_t device,
+             nb_handle **out)
+{
+    if (nelz < 1) {
+        if (out) *out = nullptr;
+        return fail(NB_EINVAL, "element counts must be >= 1");
+    }
+    return nb_setup_slab(nelx, nely, nelz, 0, nelz, p, deform_amp, seed, device, out);
 }
 
 int nb_destroy(nb_handle *h)
 {
     if (!h) return NB_OK;
     cudaSetDevice(h->device);
+    if (h->ext) nb_destroy(h->ext);
     for (auto &ws : h->ws) free_ws(ws);
     cudaFree(h->g64); cudaFree(h->g32); cudaFree(h->B); cudaFree(h->dinv64); cudaFree(h->dinv32);
     cudaFree(h->gs_off); cudaFree(h->gs_idx); cudaFree(h->flag);
@@ -386,6 +443,7 @@ int nb_query(const nb_handle *h, nb_info *o)
     o->E = h->E; o->n_local = h->NL; o->n_global = h->NG; o->n_unmasked = h->n_unmasked;
     o->n_shared_global = h->nseg; o->n_shared_copies = h->ncopies;
     o->p = h->p; o->nelx = h->nelx; o->nely = h->nely; o->nelz = h->nelz;
+    o->ez0 = h->ez0; o->nelz_local = h->nelzl;
     return NB_OK;
 }
 
@@ -398,6 +456,21 @@ int nb_rhs(nb_handle *h, nb_rhs_kind kind, double noise_amp, uint64_t seed, nb_p
     NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
     int rc = check_dev_ptr(h, b, "b");
     if (rc) return rc;
+    if (kind == NB_RHS_MANUFACTURED && h->ext) {
+        // QQ^T (B f) on the slab's interface nodes needs the neighbours' B f: computed on the
+        // ghost-extended twin, then the owned elements sliced out (stream-ordered)
+        const size_t es = prec == NB_FP64 ? sizeof(double) : sizeof(float);
+        const size_t n3 = (size_t)h->n * h->n * h->n;
+        cudaStream_t st = (cudaStream_t)stream;
+        void *tmp = nullptr;
+        NB_CU(cudaMallocAsync(&tmp, es * h->ext->NL, st), "rhs tmp");
+        cudaError_t e = nb::launch_rhs(h->ext, kind, noise_amp, seed, prec, tmp, st);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(b, (char *)tmp + es * h->ext_off * n3, es * h->NL, cudaMemcpyDeviceToDevice, st);
+        cudaError_t e2 = cudaFreeAsync(tmp, st);
+        NB_CU(e != cudaSuccess ? e : e2, "slab rhs");
+        return NB_OK;
+    }
     NB_CU(nb::launch_rhs(h, kind, noise_amp, seed, prec, b, (cudaStream_t)stream), "rhs");
     return NB_OK;
 }
@@ -433,139 +506,202 @@ int nb_dssum(nb_handle *h, nb_policy prec, nb_gs_order order, void *u, void *str
     return NB_OK;
 }
 
-static int cg_impl(nb_handle *h, const nb_cg_opts *o, const void *b, bool b_host, void *x, bool x_host,
-                   nb_cg_report *rep, cudaStream_t st)
+// One solve over nh handles: nh = 1 -> the handle's own solve (whole box, or one slab of a
+// multi-rank solve when nb_peer_attach'ed); nh > 1 -> slabs of one box sharing this GPU, one
+// cooperative launch (nb_cg_group).  b, x: per handle.
+static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void *const *b, bool b_host, void *const *x,
+                  bool x_host, nb_cg_report *reps, cudaStream_t st)
 {
     const int prec = o->policy;
     const int order = o->gs_order;
     int rc;
-    if (prec != NB_FP64 && (rc = ensure_f32(h))) return rc;
-    if ((rc = ensure_ws(h, prec, o->max_iter))) return rc;
-    nb::Workspace &ws = h->ws[prec];
-    if (o->x_fp64 && !ws.xd) NB_CU(cudaMalloc(&ws.xd, sizeof(double) * h->NL), "cudaMalloc xd");
-    const size_t vbytes = vsize(prec) * h->NL;
-    const bool mega = !h->cg_graph;
-    if (!mega && !o->time_kernels && (rc = build_graph(h, prec, order))) return rc;
+    for (int r = 0; r < nh; r++) {
+        nb_handle *h = hs[r];
+        if (prec != NB_FP64 && (rc = ensure_f32(h))) return rc;
+        if ((rc = ensure_ws(h, prec, o->max_iter))) return rc;
+        nb::Workspace &ws = h->ws[prec];
+        if (o->x_fp64 && !ws.xd) NB_CU(cudaMalloc(&ws.xd, sizeof(double) * h->NL), "cudaMalloc xd");
+    }
+    nb_handle *h0 = hs[0];
+    nb::Workspace &ws0 = h0->ws[prec];
+    const bool multi = nh > 1 || ws0.peer.nrank > 0;
+    const bool mega = !h0->cg_graph;
+    if (!multi && !mega && !o->time_kernels && (rc = build_graph(h0, prec, order))) return rc;
 
     cudaEvent_t t0, t1;
     NB_CU(cudaEventCreate(&t0), "event");
     NB_CU(cudaEventCreate(&t1), "event");
-    // device scalars
     nb::Scal s0;
     memset(&s0, 0, sizeof(s0));
     s0.rtol = o->rtol;
     s0.max_iter = o->max_iter;
-    *ws.scal_host = s0;
     NB_CU(cudaEventRecord(t0, st), "event record");
-    // host b is staged in w (the only H2D copy of the solve); the prologue reads it
-    const void *bdev = b;
-    if (b_host) {
-        NB_CU(cudaMemcpyAsync(ws.w, b, vbytes, cudaMemcpyHostToDevice, st), "copy b");
-        bdev = ws.w;
+    std::vector<const void *> bdev(nh);
+    for (int r = 0; r < nh; r++) {
+        nb::Workspace &ws = hs[r]->ws[prec];
+        *ws.scal_host = s0;
+        // host b is staged in w (the only H2D copy of the solve); the prologue reads it
+        bdev[r] = b[r];
+        if (b_host) {
+            NB_CU(cudaMemcpyAsync(ws.w, b[r], vsize(prec) * hs[r]->NL, cudaMemcpyHostToDevice, st), "copy b");
+            bdev[r] = ws.w;
+        }
+        NB_CU(cudaMemcpyAsync(ws.scal, ws.scal_host, sizeof(nb::Scal), cudaMemcpyHostToDevice, st), "copy scal");
     }
-    NB_CU(cudaMemcpyAsync(ws.scal, ws.scal_host, sizeof(nb::Scal), cudaMemcpyHostToDevice, st), "copy scal");
     int64_t launches = 0;
-    const bool fused = order == NB_GS_CONSISTENT && !h->cg_csr;
+    const bool fused = order == NB_GS_CONSISTENT && !h0->cg_csr;
     const int per_it = fused ? 2 : 3;
     double kms[3] = {0.0, 0.0, 0.0};
-    if (mega) {
-        NB_CU(NB_POL(prec, nb::launch_cg_mega, h, ws, bdev, order, o->max_iter, o->rtol, (int)o->precond, (int)o->x_fp64,
-                     ws.tim, st),
+    if (multi) {
+        // z-slab solve: one MR megakernel for this GPU's slabs
+        nb::MultiArgs M;
+        memset(&M, 0, sizeof(M));
+        const size_t es = vsize(prec);
+        for (int r = 0; r < nh; r++) {
+            nb_handle *h = hs[r];
+            nb::Workspace &ws = h->ws[prec];
+            NB_POL(prec, nb::fill_mega_args, h, ws, bdev[r], order, o->max_iter, o->rtol, (int)o->precond,
+                   (int)o->x_fp64, ws.tim, M.a[r]);
+            NB_CU(cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned int), st), "memset bar");
+        }
+        if (nh > 1) {
+            // slabs sharing this launch: neighbours' w and control blocks are plain device pointers
+            const size_t n3 = (size_t)h0->n * h0->n * h0->n;
+            for (int r = 0; r < nh; r++) {
+                nb::Workspace &ws = hs[r]->ws[prec];
+                M.a[r].wlo = r > 0 ? (const void *)((const char *)hs[r - 1]->ws[prec].w + es * hs[r - 1]->E * n3) : nullptr;
+                M.a[r].whi = r + 1 < nh ? (const void *)((const char *)hs[r + 1]->ws[prec].w - es * hs[r]->E * n3) : nullptr;
+                M.mr.flag[r] = (unsigned int *)ws.ctl;
+                M.mr.slot[r] = (double *)(ws.ctl + nb::NB_CTL_FLAG_BYTES);
+                NB_CU(cudaMemsetAsync(ws.ctl, 0, nb::NB_CTL_BYTES, st), "memset ctl");
+            }
+            M.mr.nrank = nh; M.mr.rank0 = 0; M.mr.nloc = nh; M.mr.epoch0 = 0;
+        } else {
+            const nb::PeerState &ps = ws0.peer;
+            for (int q = 0; q < ps.nrank; q++) { M.mr.flag[q] = ps.flag[q]; M.mr.slot[q] = ps.slot[q]; }
+            M.mr.nrank = ps.nrank; M.mr.rank0 = ps.rank; M.mr.nloc = 1; M.mr.epoch0 = ps.epoch;
+        }
+        M.mr.Gr = NB_POL(prec, nb::grid_mega_mr, h0) / nh;
+        if (M.mr.Gr < 1) return fail(NB_EINVAL, "too many slabs for one launch");
+        NB_CU(NB_POL(prec, nb::launch_cg_mr, h0, M, st), "cg multi-rank megakernel");
+        launches = 1;
+    } else if (mega) {
+        NB_CU(NB_POL(prec, nb::launch_cg_mega, h0, ws0, bdev[0], order, o->max_iter, o->rtol, (int)o->precond,
+                     (int)o->x_fp64, ws0.tim, st),
               "cg megakernel");
         launches = 1;
     } else {
-        NB_CU(NB_POL(prec, nb::launch_cg_init, h, ws, bdev, st), "cg init");
+        NB_CU(NB_POL(prec, nb::launch_cg_init, h0, ws0, bdev[0], st), "cg init");
         launches = 1;
-    }
-    if (mega) {
-    } else if (!o->time_kernels) {
-        NB_CU(cudaGraphLaunch(ws.exec[order], st), "graph launch");
-    } else {
-        // per-kernel CUDA-event timing: direct launches, check the done flag every 16 iterations
-        std::vector<cudaEvent_t> ev;
-        const int chunk = 16;
-        ev.resize(4 * chunk);
-        for (auto &e : ev) NB_CU(cudaEventCreate(&e), "event");
-        int k = 0;
-        bool done = false;
-        while (!done && k < o->max_iter) {
-            const int m = (o->max_iter - k) < chunk ? (o->max_iter - k) : chunk;
-            for (int c = 0; c < m; c++) {
-                cudaError_t e;
-                iteration(h, prec, order, ws, st, 0, false, e, &ev[4 * c]);
-                NB_CU(e, "iteration");
+        if (!o->time_kernels) {
+            NB_CU(cudaGraphLaunch(ws0.exec[order], st), "graph launch");
+        } else {
+            // per-kernel CUDA-event timing: direct launches, check the done flag every 16 iterations
+            std::vector<cudaEvent_t> ev;
+            const int chunk = 16;
+            ev.resize(4 * chunk);
+            for (auto &e : ev) NB_CU(cudaEventCreate(&e), "event");
+            int k = 0;
+            bool done = false;
+            while (!done && k < o->max_iter) {
+                const int m = (o->max_iter - k) < chunk ? (o->max_iter - k) : chunk;
+                for (int c = 0; c < m; c++) {
+                    cudaError_t e;
+                    iteration(h0, prec, order, ws0, st, 0, false, e, &ev[4 * c]);
+                    NB_CU(e, "iteration");
+                }
+                NB_CU(cudaMemcpyAsync(ws0.scal_host, ws0.scal, sizeof(nb::Scal), cudaMemcpyDeviceToHost, st), "scal");
+                NB_CU(cudaStreamSynchronize(st), "sync");
+                const int before = k;
+                const int it_now = ws0.scal_host->iter;
+                for (int c = 0; c < m; c++) {
+                    if (before + c >= it_now && ws0.scal_host->done) break;   // no-op launches after the end
+                    float a, b2, c3;
+                    cudaEventElapsedTime(&a, ev[4 * c], ev[4 * c + 1]);
+                    cudaEventElapsedTime(&b2, ev[4 * c + 1], ev[4 * c + 2]);
+                    cudaEventElapsedTime(&c3, ev[4 * c + 2], ev[4 * c + 3]);
+                    kms[0] += a; kms[1] += b2; kms[2] += c3;
+                }
+                k += m;
+                done = ws0.scal_host->done != 0;
             }
-            NB_CU(cudaMemcpyAsync(ws.scal_host, ws.scal, sizeof(nb::Scal), cudaMemcpyDeviceToHost, st), "scal");
-            NB_CU(cudaStreamSynchronize(st), "sync");
-            const int before = k;
-            const int it_now = ws.scal_host->iter;
-            for (int c = 0; c < m; c++) {
-                if (before + c >= it_now && ws.scal_host->done) break;   // no-op launches after the end
-                float a, b2, c3;
-                cudaEventElapsedTime(&a, ev[4 * c], ev[4 * c + 1]);
-                cudaEventElapsedTime(&b2, ev[4 * c + 1], ev[4 * c + 2]);
-                cudaEventElapsedTime(&c3, ev[4 * c + 2], ev[4 * c + 3]);
-                kms[0] += a; kms[1] += b2; kms[2] += c3;
-            }
-            k += m;
-            done = ws.scal_host->done != 0;
+            for (auto &e : ev) cudaEventDestroy(e);
+            NB_CU(NB_POL(prec, nb::launch_cg_fin, h0, ws0, st), "cg fin");
         }
-        for (auto &e : ev) cudaEventDestroy(e);
-        NB_CU(NB_POL(prec, nb::launch_cg_fin, h, ws, st), "cg fin");
     }
-    NB_CU(cudaMemcpyAsync(ws.scal_host, ws.scal, sizeof(nb::Scal), cudaMemcpyDeviceToHost, st), "copy scal back");
-    if (o->x_fp64)
-        NB_CU(cudaMemcpyAsync(x, ws.xd, sizeof(double) * h->NL, x_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
-                              st),
-              "copy x");
-    else
-        NB_CU(cudaMemcpyAsync(x, ws.x, vbytes, x_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st), "copy x");
+    for (int r = 0; r < nh; r++) {
+        nb_handle *h = hs[r];
+        nb::Workspace &ws = h->ws[prec];
+        NB_CU(cudaMemcpyAsync(ws.scal_host, ws.scal, sizeof(nb::Scal), cudaMemcpyDeviceToHost, st), "copy scal back");
+        const cudaMemcpyKind kind = x_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+        if (o->x_fp64) NB_CU(cudaMemcpyAsync(x[r], ws.xd, sizeof(double) * h->NL, kind, st), "copy x");
+        else NB_CU(cudaMemcpyAsync(x[r], ws.x, vsize(prec) * h->NL, kind, st), "copy x");
+    }
     NB_CU(cudaEventRecord(t1, st), "event record");
     NB_CU(cudaStreamSynchronize(st), "solve sync");
     float ms = 0.f;
     cudaEventElapsedTime(&ms, t0, t1);
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
-    const nb::Scal s = *ws.scal_host;
-    const int k = s.iter;
-    std::vector<double> res(k + 1, 0.0);
-    NB_CU(cudaMemcpy(res.data(), ws.hist, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost), "copy hist");
-    if (mega) {
-        // phase durations from the block-0 globaltimer stamps taken after each grid barrier
-        std::vector<unsigned long long> tm(3 * (size_t)(k + 1), 0ull);
-        NB_CU(cudaMemcpy(tm.data(), ws.tim, sizeof(unsigned long long) * 3 * (k + 1), cudaMemcpyDeviceToHost),
-              "copy tim");
-        for (int i = 1; i <= k; i++) {
-            const double tA = (double)tm[3 * (i - 1) + 1] - (double)tm[3 * (i - 1)];
-            const double tS = (double)tm[3 * (i - 1) + 2] - (double)tm[3 * (i - 1) + 1];
-            const double tB = (double)tm[3 * i] - (double)tm[3 * (i - 1) + 2];
-            kms[0] += 1e-6 * tA; kms[1] += 1e-6 * tS; kms[2] += 1e-6 * tB;
+    int ret = NB_OK;
+    for (int r = 0; r < nh; r++) {
+        nb_handle *h = hs[r];
+        nb::Workspace &ws = h->ws[prec];
+        const nb::Scal s = *ws.scal_host;
+        if (multi && nh == 1) ws.peer.epoch += (uint32_t)s.epochs;   // flags are never reset
+        const int k = s.iter;
+        std::vector<double> res(k + 1, 0.0);
+        NB_CU(cudaMemcpy(res.data(), ws.hist, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost), "copy hist");
+        double km[3] = {kms[0], kms[1], kms[2]};
+        int64_t nl = launches;
+        if (mega || multi) {
+            // phase durations from the block-0 globaltimer stamps taken after each grid barrier
+            std::vector<unsigned long long> tm(3 * (size_t)(k + 1), 0ull);
+            NB_CU(cudaMemcpy(tm.data(), ws.tim, sizeof(unsigned long long) * 3 * (k + 1), cudaMemcpyDeviceToHost),
+                  "copy tim");
+            for (int i = 1; i <= k; i++) {
+                const double tA = (double)tm[3 * (i - 1) + 1] - (double)tm[3 * (i - 1)];
+                const double tS = (double)tm[3 * (i - 1) + 2] - (double)tm[3 * (i - 1) + 1];
+                const double tB = (double)tm[3 * i] - (double)tm[3 * (i - 1) + 2];
+                km[0] += 1e-6 * tA; km[1] += 1e-6 * tS; km[2] += 1e-6 * tB;
+            }
+        } else {
+            // kernels that did work: init, per_it per completed iteration (+ the partial iteration of a
+            // breakdown), the deferred-x kernel
+            nl += (int64_t)per_it * k + (s.status == NB_BROKEDOWN ? per_it - 1 : 0) + 1;
         }
-    } else {
-        // kernels that did work: init, per_it per completed iteration (+ the partial iteration of a
-        // breakdown), the deferred-x kernel
-        launches += (int64_t)per_it * k + (s.status == NB_BROKEDOWN ? per_it - 1 : 0) + 1;
+        int status = s.status;
+        if (status == NB_MAXITER && o->rtol > 0.0) status = classify(res, k, o->stag_window > 0 ? o->stag_window : 200);
+        if (o->rel_res_history && r == 0) memcpy(o->rel_res_history, res.data(), sizeof(double) * (k + 1));
+        if (reps) {
+            nb_cg_report *rep = reps + r;
+            rep->iterations = k;
+            rep->status = status;
+            rep->rtr0 = s.rtr0;
+            rep->rtr_final = s.rtr;
+            rep->rel_res_final = res[k];
+            double mn = res[0];
+            for (int i = 1; i <= k; i++) mn = res[i] < mn ? res[i] : mn;
+            rep->rel_res_min = mn;
+            rep->solve_ms = ms;
+            rep->kernel_launches = nl;
+            rep->k_ax_ms = km[0];
+            rep->k_gs_ms = km[1];
+            rep->k_upd_ms = km[2];
+        }
+        if (status == NB_BROKEDOWN) ret = NB_EBREAKDOWN;
     }
-    int status = s.status;
-    if (status == NB_MAXITER && o->rtol > 0.0) status = classify(res, k, o->stag_window > 0 ? o->stag_window : 200);
-    if (o->rel_res_history) memcpy(o->rel_res_history, res.data(), sizeof(double) * (k + 1));
-    if (rep) {
-        rep->iterations = k;
-        rep->status = status;
-        rep->rtr0 = s.rtr0;
-        rep->rtr_final = s.rtr;
-        rep->rel_res_final = res[k];
-        double mn = res[0];
-        for (int i = 1; i <= k; i++) mn = res[i] < mn ? res[i] : mn;
-        rep->rel_res_min = mn;
-        rep->solve_ms = ms;
-        rep->kernel_launches = launches;
-        rep->k_ax_ms = kms[0];
-        rep->k_gs_ms = kms[1];
-        rep->k_upd_ms = kms[2];
-    }
-    if (status == NB_BROKEDOWN) return fail(NB_EBREAKDOWN, "CG breakdown (pap <= 0 or non-finite scalar)");
+    if (ret == NB_EBREAKDOWN) return fail(NB_EBREAKDOWN, "CG breakdown (pap <= 0 or non-finite scalar)");
     return NB_OK;
+}
+
+static int cg_impl(nb_handle *h, const nb_cg_opts *o, const void *b, bool b_host, void *x, bool x_host,
+                   nb_cg_report *rep, cudaStream_t st)
+{
+    nb_handle *hs[1] = {h};
+    const void *bs[1] = {b};
+    void *xs[1] = {x};
+    return cg_run(hs, 1, o, bs, b_host, xs, x_host, rep, st);
 }
 
 static int cg_args(nb_handle *h, const nb_cg_opts *o)
@@ -587,16 +723,34 @@ static int cg_args(nb_handle *h, const nb_cg_opts *o)
     return NB_OK;
 }
 
+// a slab solve (group or attached): the fused consistent-order megakernel only
+static int mr_args(const nb_handle *h, const nb_cg_opts *o)
+{
+    if (o->gs_order != NB_GS_CONSISTENT) return fail(NB_EINVAL, "multi-rank solves use the consistent GS order");
+    if (h->cg_csr || h->cg_graph) return fail(NB_EINVAL, "multi-rank solves run on the fused megakernel only");
+    return NB_OK;
+}
+
 int nb_cg(nb_handle *h, const nb_cg_opts *o, const void *b, void *x, nb_cg_report *rep, void *stream)
 {
     int rc = cg_args(h, o);
     if (rc) return rc;
+    const bool slab = h->nelzl != h->nelz;
+    if (slab && h->ws[o->policy].peer.nrank == 0)
+        return fail(NB_EINVAL, "a slab handle solves with nb_cg_group or after nb_peer_attach");
+    if (h->ws[o->policy].peer.nrank > 0 && (rc = mr_args(h, o))) return rc;
     if ((rc = check_dev_ptr(h, b, "b")) || (rc = check_dev_ptr(h, x, "x"))) return rc;
     return cg_impl(h, o, b, false, x, false, rep, (cudaStream_t)stream);
 }
 
 int nb_cg_host(nb_handle *h, const nb_cg_opts *o, const void *b_host, void *x_host, nb_cg_report *rep, void *stream)
 {
+    if (h && o && o->policy >= NB_FP64 && o->policy <= NB_FP32_DOT2) {
+        if (h->nelzl != h->nelz && h->ws[o->policy].peer.nrank == 0)
+            return fail(NB_EINVAL, "a slab handle solves with nb_cg_group or after nb_peer_attach");
+        int rc0;
+        if (h->ws[o->policy].peer.nrank > 0 && (rc0 = mr_args(h, o))) return rc0;
+    }
     int rc = cg_args(h, o);
     if (rc) return rc;
     if (!b_host || !x_host) return fail(NB_EINVAL, "NULL host buffer");
@@ -653,3 +807,133 @@ int nb_export_basis(const nb_handle *h, double *nodes, double *weights, double *
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// multi-rank z-slab solves
+// ---------------------------------------------------------------------------
+int nb_cg_group(nb_handle *const *hs, int32_t nslab, const nb_cg_opts *o, const void *const *b, void *const *x,
+                nb_cg_report *reps, void *stream)
+{
+    if (!hs || !b || !x) return fail(NB_EINVAL, "NULL argument");
+    if (nslab < 1 || nslab > nb::NB_MAX_LOCAL) return fail(NB_EINVAL, "nslab must be in [1, 4]");
+    int rc;
+    for (int r = 0; r < nslab; r++) {
+        if ((rc = cg_args(hs[r], o))) return rc;
+        if ((rc = mr_args(hs[r], o))) return rc;
+        const nb_handle *h = hs[r], *a = hs[0];
+        if (h->device != a->device || h->nelx != a->nelx || h->nely != a->nely || h->nelz != a->nelz || h->p != a->p ||
+            h->deform != a->deform || h->seed != a->seed)
+            return fail(NB_EINVAL, "slabs must be of the same box on the same device");
+        if (h->ez0 != (r == 0 ? 0 : hs[r - 1]->ez0 + hs[r - 1]->nelzl))
+            return fail(NB_EINVAL, "slabs must be given bottom to top and tile the box");
+        if (h->ws[o->policy].peer.nrank > 0) return fail(NB_EINVAL, "a peer-attached slab cannot join a group");
+        if ((rc = check_dev_ptr(h, b[r], "b")) || (rc = check_dev_ptr(h, x[r], "x"))) return rc;
+    }
+    if (hs[nslab - 1]->ez0 + hs[nslab - 1]->nelzl != hs[0]->nelz)
+        return fail(NB_EINVAL, "slabs must tile the box");
+    if (nslab == 1) return cg_run(hs, 1, o, b, false, x, false, reps, (cudaStream_t)stream);
+    return cg_run(hs, nslab, o, b, false, x, false, reps, (cudaStream_t)stream);
+}
+
+namespace {
+struct PeerBlob {                 // NB_PEER_BLOB_BYTES, one per rank
+    cudaIpcMemHandle_t w, ctl;    // 64 + 64 bytes
+    int32_t magic, policy, nelx, nely, nelz, p, ez0, nelzl;
+    int64_t E;
+    int32_t pid, device;
+    unsigned char pad[NB_PEER_BLOB_BYTES - 2 * sizeof(cudaIpcMemHandle_t) - 8 * 4 - 8 - 2 * 4];
+};
+static_assert(sizeof(PeerBlob) == NB_PEER_BLOB_BYTES, "peer blob size");
+constexpr int32_t kPeerMagic = 0x6e62706b;
+}  // namespace
+
+int nb_peer_export(nb_handle *h, nb_policy policy, void *blob)
+{
+    if (!h || !blob) return fail(NB_EINVAL, "NULL argument");
+    if (policy < NB_FP64 || policy > NB_FP32_DOT2) return fail(NB_EINVAL, "bad policy");
+    NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
+    int rc;
+    if ((rc = ensure_ws(h, policy, 1))) return rc;
+    nb::Workspace &ws = h->ws[policy];
+    PeerBlob pb;
+    memset(&pb, 0, sizeof(pb));
+    NB_CU(cudaIpcGetMemHandle(&pb.w, ws.w), "cudaIpcGetMemHandle w");
+    NB_CU(cudaIpcGetMemHandle(&pb.ctl, ws.ctl), "cudaIpcGetMemHandle ctl");
+    pb.magic = kPeerMagic; pb.policy = policy;
+    pb.nelx = h->nelx; pb.nely = h->nely; pb.nelz = h->nelz; pb.p = h->p; pb.ez0 = h->ez0; pb.nelzl = h->nelzl;
+    pb.E = h->E;
+    pb.pid = (int32_t)getpid();
+    pb.device = h->device;
+    memcpy(blob, &pb, sizeof(pb));
+    return NB_OK;
+}
+
+int nb_peer_attach(nb_handle *h, nb_policy policy, int32_t nrank, int32_t rank, const void *blobs)
+{
+    if (!h || !blobs) return fail(NB_EINVAL, "NULL argument");
+    if (policy < NB_FP64 || policy > NB_FP32_DOT2) return fail(NB_EINVAL, "bad policy");
+    if (nrank < 1 || nrank > nb::NB_MAX_RANKS || rank < 0 || rank >= nrank) return fail(NB_EINVAL, "bad nrank/rank");
+    NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
+    int rc;
+    if ((rc = ensure_ws(h, policy, 1))) return rc;
+    nb::Workspace &ws = h->ws[policy];
+    if (ws.peer.nrank > 0) return fail(NB_ESTATE, "already attached (nb_peer_detach first)");
+    const PeerBlob *pb = (const PeerBlob *)blobs;
+    int32_t z = 0;
+    for (int q = 0; q < nrank; q++) {
+        if (pb[q].magic != kPeerMagic || pb[q].policy != policy) return fail(NB_EINVAL, "bad peer blob");
+        if (pb[q].nelx != h->nelx || pb[q].nely != h->nely || pb[q].nelz != h->nelz || pb[q].p != h->p)
+            return fail(NB_EINVAL, "peers hold slabs of another box");
+        if (pb[q].ez0 != z) return fail(NB_EINVAL, "peer slabs must be ordered by rank and tile the box");
+        z += pb[q].nelzl;
+    }
+    if (z != h->nelz) return fail(NB_EINVAL, "peer slabs must tile the box");
+    if (pb[rank].ez0 != h->ez0 || pb[rank].nelzl != h->nelzl) return fail(NB_EINVAL, "this rank's blob is not this slab");
+    nb::PeerState ps;
+    auto open = [&](const cudaIpcMemHandle_t &hd, void **out) -> int {
+        cudaError_t e = cudaIpcOpenMemHandle(out, hd, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+        ps.opened[ps.nopened++] = *out;
+        return NB_OK;
+    };
+    auto fail_close = [&](int code) {
+        for (int i = 0; i < ps.nopened; i++) cudaIpcCloseMemHandle(ps.opened[i]);
+        return code;
+    };
+    const size_t es = vsize(policy), n3 = (size_t)h->n * h->n * h->n;
+    for (int q = 0; q < nrank; q++) {
+        unsigned char *ctl = nullptr;
+        if (q == rank) ctl = ws.ctl;
+        else if ((rc = open(pb[q].ctl, (void **)&ctl))) return fail_close(rc);
+        ps.flag[q] = (unsigned int *)ctl;
+        ps.slot[q] = (double *)(ctl + nb::NB_CTL_FLAG_BYTES);
+    }
+    if (rank > 0) {
+        void *w = nullptr;
+        if ((rc = open(pb[rank - 1].w, &w))) return fail_close(rc);
+        ps.wlo = (const char *)w + es * (size_t)pb[rank - 1].E * n3;
+    }
+    if (rank + 1 < nrank) {
+        void *w = nullptr;
+        if ((rc = open(pb[rank + 1].w, &w))) return fail_close(rc);
+        ps.whi = (const char *)w - es * (size_t)h->E * n3;
+    }
+    ps.nrank = nrank;
+    ps.rank = rank;
+    // flags count from 0: every rank must attach before any rank solves
+    NB_CU(cudaMemset(ws.ctl, 0, nb::NB_CTL_BYTES), "memset ctl");
+    ps.epoch = 0;
+    ws.peer = ps;
+    return NB_OK;
+}
+
+int nb_peer_detach(nb_handle *h, nb_policy policy)
+{
+    if (!h) return fail(NB_EINVAL, "NULL handle");
+    if (policy < NB_FP64 || policy > NB_FP32_DOT2) return fail(NB_EINVAL, "bad policy");
+    NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
+    nb::Workspace &ws = h->ws[policy];
+    for (int i = 0; i < ws.peer.nopened; i++) cudaIpcCloseMemHandle(ws.peer.opened[i]);
+    ws.peer = nb::PeerState();
+    return NB_OK;
+}

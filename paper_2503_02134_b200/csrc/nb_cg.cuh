@@ -385,7 +385,9 @@ template <int PREC, int N>
 __device__ __forceinline__ void gather_pencil(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ w,
                                               int e, const ElemPos &P, int a, int b,
                                               typename Pol<PREC>::TV (&ww)[N], typename Pol<PREC>::TV own_l,
-                                              typename Pol<PREC>::TV own_r)
+                                              typename Pol<PREC>::TV own_r,
+                                              const typename Pol<PREC>::TV *wlo = nullptr,
+                                              const typename Pol<PREC>::TV *whi = nullptr)
 {
     using TV = typename Pol<PREC>::TV;
     using TG = typename Pol<PREC>::TG;
@@ -402,20 +404,24 @@ __device__ __forceinline__ void gather_pencil(const MeshDev &m, const typename P
     const size_t base = ((size_t)e * N2 + (size_t)(a + N * b)) * N;
     const int64_t sy = (int64_t)ys * (m.nelx * (int64_t)N3) + (int64_t)(ys ? (N - 1 - 2 * a) : 0) * N;
     const int64_t sz = (int64_t)zs * ((int64_t)m.nelx * m.nely * N3) + (int64_t)(zs ? (N - 1 - 2 * b) : 0) * N2;
+    // z-neighbour layer: this slab's own w, or a neighbour slab's (multi-rank; rebased pointers)
+    const TV *wz = w;
+    if (wlo && zs < 0 && P.ez == m.ez0) wz = wlo;
+    if (whi && zs > 0 && P.ez == m.ez0 + m.nelzl - 1) wz = whi;
     if (ys) {
         ld_pencil<TV, N, NB_WLD>(w + base + sy, vy);
         if (xl) ly = ldv<NB_WLD>(w + base + sy - N3 + (N - 1));
         if (xr) ry = ldv<NB_WLD>(w + base + sy + N3);
     }
     if (zs) {
-        ld_pencil<TV, N, NB_WLD>(w + base + sz, vz);
-        if (xl) lz = ldv<NB_WLD>(w + base + sz - N3 + (N - 1));
-        if (xr) rz = ldv<NB_WLD>(w + base + sz + N3);
+        ld_pencil<TV, N, NB_WLD>(wz + base + sz, vz);
+        if (xl) lz = ldv<NB_WLD>(wz + base + sz - N3 + (N - 1));
+        if (xr) rz = ldv<NB_WLD>(wz + base + sz + N3);
     }
     if (ys && zs) {
-        ld_pencil<TV, N, NB_WLD>(w + base + sy + sz, vyz);
-        if (xl) lyz = ldv<NB_WLD>(w + base + sy + sz - N3 + (N - 1));
-        if (xr) ryz = ldv<NB_WLD>(w + base + sy + sz + N3);
+        ld_pencil<TV, N, NB_WLD>(wz + base + sy + sz, vyz);
+        if (xl) lyz = ldv<NB_WLD>(wz + base + sy + sz - N3 + (N - 1));
+        if (xr) ryz = ldv<NB_WLD>(wz + base + sy + sz + N3);
     }
     // ascending element order: lexicographic (dz, dy, dx); a negative offset comes first
     TG s[N];
@@ -482,7 +488,8 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
                                            typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
                                            const void *__restrict__ dinv,
                                            typename Pol<PREC>::TV alpha, int64_t pid, Acc<PREC> &rtr, Acc<PREC> &rho,
-                                           int pc = NB_PC_JACOBI)
+                                           int pc = NB_PC_JACOBI, const typename Pol<PREC>::TV *wlo = nullptr,
+                                           const typename Pol<PREC>::TV *whi = nullptr)
 {
     using TV = typename Pol<PREC>::TV;
     using TJ = typename Pol<PREC>::TJ;
@@ -502,7 +509,7 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
         constexpr int N3 = N * N * N;
         const TV ol = P.ex > 0 ? ldv<NB_WLD>(w + base - N3 + (N - 1)) : TV(0);
         const TV orr = P.ex < m.nelx - 1 ? ldv<NB_WLD>(w + base + N3) : TV(0);
-        gather_pencil<PREC, N>(m, w, e, P, a, b, ww, ol, orr);
+        gather_pencil<PREC, N>(m, w, e, P, a, b, ww, ol, orr, wlo, whi);
     }
     const int mjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz);
 #pragma unroll
@@ -568,25 +575,6 @@ __device__ __forceinline__ int64_t split(int64_t n, int parts, int i) { return n
 // ===========================================================================
 // persistent cooperative megakernel: the whole solve in one launch
 // ===========================================================================
-struct MegaArgs {
-    MeshDev m;
-    const void *b;
-    void *x, *p, *r, *z, *w;
-    const void *g, *dinv;
-    const int32_t *gs_off, *gs_idx;
-    int32_t nseg;
-    int32_t order;          // NB_GS_CONSISTENT / NB_GS_PER_COPY
-    int32_t max_iter;
-    double rtol;
-    double *hist;           // [max_iter + 1]
-    unsigned long long *tim;  // nullable: [3 * (max_iter + 1)] globaltimer stamps (block 0)
-    double *partA, *partS, *partB;   // per-block partials, [G], [G], [2G] (x Acc::W)
-    int32_t pc;             // nb_precond (z aliases r for the identity)
-    int32_t x64;            // NB_MIXED: x is double (x_fp64 option)
-    unsigned int *bar;      // [2] grid barrier: arrival count, generation
-    Scal *scal;             // result scalars (written by block 0)
-};
-
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int *p)
 {
     unsigned int v;
@@ -738,11 +726,86 @@ __device__ __forceinline__ TS all_blocks_sum1(const double *part, int G, TS *sh)
     return o[0];
 }
 
-// VAR = 0: the default options (Jacobi, x in the policy precision) folded at compile time;
-// VAR = 1: the NEXT-3 variants (nb_cg_opts.precond / .x_fp64) as uniform runtime selects.
+__device__ __forceinline__ unsigned int ld_acquire_sys_u32(const unsigned int *p)
+{
+    unsigned int v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Multi-rank reduction + barrier (VAR = 2), after block_reduce_acc left this block's K values
+// in thread 0 of VALS: block partials -> local barrier -> block 0 sums its rank's partials
+// (fixed order) and pushes them to every rank's slot array, bumps every rank's flag, waits for
+// all R ranks, releases its blocks -> every block merges the R rank partials in rank order
+// (bit-identical in every block of every rank).
+template <int PREC, int K>
+__device__ __forceinline__ void mr_reduce(const MegaArgs &A, const MrArgs &mr, int vr, int bid, int G,
+                                          Acc<PREC> (&vals)[K], double *part, unsigned int &tgt, unsigned int ep,
+                                          typename Pol<PREC>::TS (&tot)[K], Acc<PREC> *acc_sh)
+{
+    using TS = typename Pol<PREC>::TS;
+    constexpr int W = Acc<PREC>::W;
+    const int tid = threadIdx.x;
+    const int R = mr.nrank, me = mr.rank0 + vr, par = ep & 1;
+    __shared__ TS bc[K];
+    if (tid == 0) {
+#pragma unroll
+        for (int k = 0; k < K; k++) vals[k].store(part + ((size_t)bid * K + k) * W);
+        tgt += G;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.bar) : "memory");
+    }
+    if (bid == 0) {
+        if (tid == 0)
+            while ((int)(ld_acquire_u32(A.bar) - tgt) < 0) {
+            }
+        __syncthreads();
+        Acc<PREC> s[K];
+        for (int i = tid; i < G; i += blockDim.x) {
+#pragma unroll
+            for (int k = 0; k < K; k++) s[k].merge(Acc<PREC>::load(part + ((size_t)i * K + k) * W));
+        }
+        block_reduce_acc<PREC, K>(s, acc_sh);
+        if (tid == 0) {
+            for (int q = 0; q < R; q++) {
+                double *dst = mr.slot[q] + ((size_t)par * NB_MAX_RANKS + me) * 4;
+#pragma unroll
+                for (int k = 0; k < K; k++) s[k].store(dst + k * W);
+            }
+            __threadfence_system();
+            for (int q = 0; q < R; q++)
+                asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(mr.flag[q]) : "memory");
+            const unsigned int want = (unsigned int)R * ep;
+            while ((int)(ld_acquire_sys_u32(mr.flag[me]) - want) < 0) {
+            }
+            st_release_u32(A.bar + 1, ep);
+        }
+    } else if (tid == 0) {
+        while ((int)(ld_acquire_u32(A.bar + 1) - ep) < 0) {
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        Acc<PREC> t[K];
+        const double *src = mr.slot[me] + (size_t)par * NB_MAX_RANKS * 4;
+        for (int q = 0; q < R; q++) {
+#pragma unroll
+            for (int k = 0; k < K; k++) t[k].merge(Acc<PREC>::load(src + (size_t)q * 4 + k * W));
+        }
+#pragma unroll
+        for (int k = 0; k < K; k++) bc[k] = t[k].value();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; k++) tot[k] = bc[k];
+}
+
+// The solve of one slab (or the whole box) by the blocks [0, G) of its rank (bid = block index
+// within the rank).  VAR = 0: the default options (Jacobi, x in the policy precision) folded at
+// compile time; VAR = 1: the NEXT-3 variants (nb_cg_opts.precond / .x_fp64) as uniform runtime
+// selects; VAR = 2: VAR 1 as one rank of a multi-rank z-slab solve (mr, vr: slab in the launch).
 template <int PREC, int N, int FUSED, int VAR>
-__global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT, AxCfg<typename Pol<PREC>::TV, N>::MINB)
-k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D)
+__device__ __forceinline__ void cg_mega_body(const MegaArgs &A, const DMat<typename Pol<PREC>::TV, N> &D,
+                                             const MrArgs *mr, int vr, int bid, int G)
 {
     using TV = typename Pol<PREC>::TV;
     using TJ = typename Pol<PREC>::TJ;
@@ -759,10 +822,16 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
     };
     __shared__ State st;
     const int tid = threadIdx.x;
-    const bool t0 = (blockIdx.x == 0 && tid == 0);
+    // the block index and count of the rank: the hardware registers unless several slabs share the launch
+#define NB_BID (VAR == 2 ? bid : (int)blockIdx.x)
+#define NB_GR (VAR == 2 ? G : (int)gridDim.x)
+    const bool t0 = (NB_BID == 0 && tid == 0);
     unsigned int tgt = 0;   // grid-barrier arrival target (thread 0)
-#define NB_G0 split(((int64_t)A.m.E + C::EPB - 1) / C::EPB, gridDim.x, blockIdx.x)
-#define NB_G1 split(((int64_t)A.m.E + C::EPB - 1) / C::EPB, gridDim.x, blockIdx.x + 1)
+    unsigned int ep = VAR == 2 ? mr->epoch0 : 0u;   // cross-rank barrier epoch (VAR 2)
+    const TV *const wlo = VAR == 2 ? (const TV *)A.wlo : nullptr;
+    const TV *const whi = VAR == 2 ? (const TV *)A.whi : nullptr;
+#define NB_G0 split(((int64_t)A.m.E + C::EPB - 1) / C::EPB, NB_GR, NB_BID)
+#define NB_G1 split(((int64_t)A.m.E + C::EPB - 1) / C::EPB, NB_GR, NB_BID + 1)
 #define NB_EL (threadIdx.x / C::N2)
 #define NB_A ((threadIdx.x - NB_EL * C::N2) % N)
 #define NB_B ((threadIdx.x - NB_EL * C::N2) / N)
@@ -771,14 +840,19 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
 #define NB_GRID_REDUCE(K, VALS, PART, TOT)                                             \
     do {                                                                                \
         block_reduce_acc<PREC, K>(VALS, acc_sh);                                        \
-        if (tid == 0) {                                                                 \
-            _Pragma("unroll") for (int k_ = 0; k_ < K; k_++)                            \
-                VALS[k_].store((PART) + ((size_t)blockIdx.x * K + k_) * Acc<PREC>::W);  \
-            tgt += gridDim.x;                                                           \
-            grid_arrive_wait(A.bar, tgt);                                               \
+        if constexpr (VAR == 2) {                                                       \
+            ep++;                                                                       \
+            mr_reduce<PREC, K>(A, *mr, vr, bid, G, VALS, PART, tgt, ep, TOT, acc_sh);   \
+        } else {                                                                        \
+            if (tid == 0) {                                                             \
+                _Pragma("unroll") for (int k_ = 0; k_ < K; k_++)                        \
+                    VALS[k_].store((PART) + ((size_t)NB_BID * K + k_) * Acc<PREC>::W);  \
+                tgt += NB_GR;                                                           \
+                grid_arrive_wait(A.bar, tgt);                                           \
+            }                                                                           \
+            __syncthreads();                                                            \
+            all_blocks_reduce_acc<PREC, K>(PART, NB_GR, TOT, acc_sh);                   \
         }                                                                               \
-        __syncthreads();                                                                \
-        all_blocks_reduce_acc<PREC, K>(PART, gridDim.x, TOT, acc_sh);                   \
     } while (0)
 
     // ---- prologue: r = b, x = p = 0, z = M^-1 r; rtr0, rho_1
@@ -800,7 +874,7 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
             if (rtr0 == (TS)0) { st.status = NB_CONVERGED; st.done = 1; }
             else if (!isfinite((double)rtr0)) { st.status = NB_BROKEDOWN; st.done = 1; }
             else if (A.max_iter <= 0) { st.status = NB_MAXITER; st.done = 1; }
-            if (blockIdx.x == 0) A.hist[0] = rtr0 == (TS)0 ? 0.0 : 1.0;
+            if (NB_BID == 0) A.hist[0] = rtr0 == (TS)0 ? 0.0 : 1.0;
         }
         __syncthreads();
     }
@@ -830,7 +904,7 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
         if (t0 && A.tim) A.tim[3 * st.it + 1] = globaltimer();
         if (!FUSED) {
             // ---- CSR gather-scatter phase: per-copy (or consistent) QQ^T, shared pap partial
-            const int64_t s0 = split(A.nseg, gridDim.x, blockIdx.x), s1 = split(A.nseg, gridDim.x, blockIdx.x + 1);
+            const int64_t s0 = split(A.nseg, NB_GR, NB_BID), s1 = split(A.nseg, NB_GR, NB_BID + 1);
             Acc<PREC> v[1];
             for (int64_t s = s0 + tid; s < s1; s += blockDim.x) {
                 if (A.order == NB_GS_CONSISTENT)
@@ -868,14 +942,19 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
             const int pc = VAR ? A.pc : NB_PC_JACOBI;
 #pragma unroll 1
             for (int64_t pid = NB_G0 * C::EPB * C::N2 + tid; pid < p1; pid += blockDim.x)
-                upd_pencil<PREC, N, FUSED>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, A.dinv, av, pid, v[0], v[1], pc);
+                if constexpr (VAR == 2)
+                    upd_pencil<PREC, N, FUSED>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, A.dinv, av, pid, v[0], v[1],
+                                               pc, wlo, whi);
+                else
+                    upd_pencil<PREC, N, FUSED>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, A.dinv, av, pid, v[0], v[1],
+                                               pc);
             TS tot[2];
             NB_GRID_REDUCE(2, v, A.partB, tot);
             if (tid == 0) {
                 const TS rtr = tot[0], rho_new = tot[1];
                 const int it = st.it + 1;
                 const double res = sqrt((double)rtr / (double)st.rtr0);
-                if (blockIdx.x == 0) {
+                if (NB_BID == 0) {
                     A.hist[it] = res;
                     if (A.tim) A.tim[3 * it] = globaltimer();
                 }
@@ -910,6 +989,7 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
         s->rho = (double)st.rho; s->beta = (double)st.beta; s->alpha = (double)st.alpha; s->pap = (double)st.pap;
         s->rtr = (double)st.rtr; s->rtr0 = (double)st.rtr0; s->iter = st.it; s->status = st.status; s->done = 1;
         s->pending = 0;
+        s->epochs = VAR == 2 ? (int32_t)(ep - mr->epoch0) : 0;
     }
 #undef NB_GRID_REDUCE
 #undef NB_G0
@@ -918,6 +998,26 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
 #undef NB_A
 #undef NB_B
 #undef NB_S0
+#undef NB_BID
+#undef NB_GR
+}
+
+template <int PREC, int N, int FUSED, int VAR>
+__global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT, AxCfg<typename Pol<PREC>::TV, N>::MINB)
+k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D)
+{
+    cg_mega_body<PREC, N, FUSED, VAR>(A, D, nullptr, 0, blockIdx.x, gridDim.x);
+}
+
+// Multi-rank solve: nloc slabs in this launch, Gr blocks each (cooperative launch, so the
+// slabs of one GPU that wait on one another are co-resident).
+template <int PREC, int N>
+__global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT, AxCfg<typename Pol<PREC>::TV, N>::MINB)
+k_cg_mega_mr(const __grid_constant__ MultiArgs M, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D)
+{
+    const int vr = blockIdx.x / M.mr.Gr;
+    if (vr >= M.mr.nloc) return;
+    cg_mega_body<PREC, N, 1, 2>(M.a[vr], D, &M.mr, vr, blockIdx.x - vr * M.mr.Gr, M.mr.Gr);
 }
 
 // ===========================================================================
@@ -1220,6 +1320,10 @@ cudaError_t launch_cg_fin(const nb_handle *h, Workspace &ws, cudaStream_t st)
 // the variant (VAR = 1) megakernels: their own translation units (parallel build)
 #define NB_INSTANTIATE_CG_VAR(P)                                                                              \
     template int grid_mega_var<P, 1>(const nb_handle *);                                                      \
-    template cudaError_t launch_cg_mega_var<P, 1>(const nb_handle *, const MegaArgs &, bool, cudaStream_t);
+    template cudaError_t launch_cg_mega_var<P, 1>(const nb_handle *, const MegaArgs &, bool, cudaStream_t);   \
+    template void fill_mega_args<P>(const nb_handle *, Workspace &, const void *, int, int, double, int, int, \
+                                    unsigned long long *, MegaArgs &);                                        \
+    template int grid_mega_mr<P>(const nb_handle *);                                                          \
+    template cudaError_t launch_cg_mr<P>(const nb_handle *, const MultiArgs &, cudaStream_t);
 
 }  // namespace nb

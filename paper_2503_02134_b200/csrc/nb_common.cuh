@@ -277,8 +277,9 @@ __device__ __forceinline__ ElemPos elem_pos(const MeshDev &m, int32_t e)
     ElemPos r;
     const int32_t t = e / m.nelx;
     r.ex = e - t * m.nelx;
-    r.ez = t / m.nely;
-    r.ey = t - r.ez * m.nely;
+    const int32_t zl = t / m.nely;
+    r.ey = t - zl * m.nely;
+    r.ez = zl + m.ez0;   // global layer (slabs: SURVEY.md §8(e))
     return r;
 }
 // multiplicity factor along one axis for local index i of element coordinate ex (nel elements)

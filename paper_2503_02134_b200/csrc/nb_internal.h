@@ -23,7 +23,24 @@ struct Scal {
     int32_t done;      // 1: no further updates (kernels no-op)
     int32_t status;    // NB_CONVERGED / NB_MAXITER / NB_BROKEDOWN (stagnation decided on host)
     int32_t pending;   // 1: x += alpha*p of the last iteration not yet applied (deferred x update)
-    int32_t pad;
+    int32_t epochs;    // multi-rank megakernel: cross-rank barrier epochs used by the solve
+};
+
+// Multi-rank (z-slab) solves: ranks per solve, slabs per launch (one GPU)
+constexpr int NB_MAX_RANKS = 8;
+constexpr int NB_MAX_LOCAL = 4;
+// per-rank control block (peer-visible): arrival flag, then rank-partial slots
+// [2 parities][NB_MAX_RANKS][4 doubles] (K <= 2 accumulators x W <= 2 doubles)
+constexpr int NB_CTL_FLAG_BYTES = 128;
+constexpr int NB_CTL_BYTES = NB_CTL_FLAG_BYTES + 2 * NB_MAX_RANKS * 4 * 8;
+struct PeerState {
+    int32_t nrank = 0, rank = 0;       // nrank 0: not attached
+    const void *wlo = nullptr, *whi = nullptr;   // neighbours' w (below / above), rebased (nb_cg.cuh)
+    unsigned int *flag[NB_MAX_RANKS] = {};
+    double *slot[NB_MAX_RANKS] = {};
+    uint32_t epoch = 0;                // cross-rank barrier epochs completed by earlier solves
+    void *opened[NB_MAX_RANKS + 2] = {};   // IPC mappings to close
+    int nopened = 0;
 };
 
 // Scratch of the deterministic two-level grid reductions (nb_common.cuh grid_reduce).
@@ -35,16 +52,61 @@ struct RedWs {
 
 // Geometry needed by kernels, passed by value.
 struct MeshDev {
-    int32_t nelx, nely, nelz, p, n;
-    int32_t E;
-    int64_t NL, NX, NY, NZ, NG;
+    int32_t nelx, nely, nelz, p, n;   // the whole box (nelz: global layer count)
+    int32_t E;                        // elements held here (a z-slab of the box, or all of it)
+    int32_t ez0, nelzl;               // slab: first global z layer and layer count (box: 0, nelz)
+    int64_t NL, NX, NY, NZ, NG;       // NL local; NX, NY, NZ, NG: the global node lattice
+    int64_t NZl, NGl;                 // the slab's own node lattice (its GS segments)
     int32_t nseg;
+};
+
+// Arguments of the persistent CG megakernel (nb_cg.cuh), one slab's (or the whole box's) solve
+struct MegaArgs {
+    MeshDev m;
+    const void *b;
+    void *x, *p, *r, *z, *w;
+    const void *g, *dinv;
+    const int32_t *gs_off, *gs_idx;
+    int32_t nseg;
+    int32_t order;          // NB_GS_CONSISTENT / NB_GS_PER_COPY
+    int32_t max_iter;
+    double rtol;
+    double *hist;           // [max_iter + 1]
+    unsigned long long *tim;  // nullable: [3 * (max_iter + 1)] globaltimer stamps (block 0)
+    double *partA, *partS, *partB;   // per-block partials, [G], [G], [2G] (x Acc::W)
+    int32_t pc;             // nb_precond (z aliases r for the identity)
+    int32_t x64;            // NB_MIXED: x is double (x_fp64 option)
+    unsigned int *bar;      // [2] grid barrier: arrival count, generation
+    Scal *scal;             // result scalars (written by block 0)
+    // multi-rank (z-slab) solves only: the neighbour slabs' w, rebased so that the element
+    // index of this slab addresses them (wlo + e*N3 for e < 0, whi + e*N3 for e >= E); else null
+    const void *wlo, *whi;
+};
+
+// Multi-rank solve over z-slabs: every rank's block 0 pushes its rank partial
+// into every rank's control block (peer stores over NVLink, or plain stores when the slabs share
+// a GPU), then bumps every rank's arrival flag; the phase-B gather reads the neighbour slabs'
+// w directly from peer memory.  Flags count monotonically across solves (epoch0).
+struct MrArgs {
+    int32_t nrank;           // ranks R of the solve
+    int32_t rank0;           // global rank of this launch's first slab
+    int32_t nloc;            // slabs in this launch (1: one per GPU; >1: slabs sharing this GPU)
+    int32_t Gr;              // blocks per slab
+    uint32_t epoch0;         // barrier epochs completed by earlier solves
+    unsigned int *flag[NB_MAX_RANKS];
+    double *slot[NB_MAX_RANKS];
+};
+struct MultiArgs {
+    MegaArgs a[NB_MAX_LOCAL];
+    MrArgs mr;
 };
 
 struct Workspace {          // per-policy CG workspace (lazily allocated)
     bool ready = false;
     void *r = nullptr, *p = nullptr, *w = nullptr, *x = nullptr, *z = nullptr;
     double *xd = nullptr;       // x accumulated in double (x_fp64 option), lazily allocated
+    unsigned char *ctl = nullptr;   // multi-rank control block (NB_CTL_BYTES), lazily allocated
+    PeerState peer;
     RedWs red = {nullptr, nullptr, nullptr};
     Scal *scal = nullptr;       // device scalars
     Scal *scal_host = nullptr;  // pinned mirror
@@ -63,8 +125,12 @@ struct Workspace {          // per-policy CG workspace (lazily allocated)
 
 struct nb_handle {
     int32_t device;
-    int32_t nelx, nely, nelz, p, n;
-    int64_t E, NL, NX, NY, NZ, NG;
+    int32_t nelx, nely, nelz, p, n;   // nelz: the whole box
+    int32_t ez0 = 0, nelzl = 0;       // z-slab held by this handle
+    int64_t E, NL, NX, NY, NZ, NG;    // E, NL: the slab's; NX..NG: the global lattice
+    int64_t NZl = 0, NGl = 0;         // the slab's node lattice
+    nb_handle *ext = nullptr;         // slab with one ghost layer per side (setup data: diag, rhs)
+    int64_t ext_off = 0;              // first owned element inside ext
     int64_t n_unmasked, nseg, ncopies;
     double deform;
     uint64_t seed;
@@ -86,7 +152,8 @@ struct nb_handle {
     nb::MeshDev md() const {
         nb::MeshDev m;
         m.nelx = nelx; m.nely = nely; m.nelz = nelz; m.p = p; m.n = n;
-        m.E = (int32_t)E; m.NL = NL; m.NX = NX; m.NY = NY; m.NZ = NZ; m.NG = NG;
+        m.E = (int32_t)E; m.ez0 = ez0; m.nelzl = nelzl;
+        m.NL = NL; m.NX = NX; m.NY = NY; m.NZ = NZ; m.NG = NG; m.NZl = NZl; m.NGl = NGl;
         m.nseg = (int32_t)nseg;
         return m;
     }
@@ -127,7 +194,14 @@ template <int PREC> cudaError_t launch_cg_fin(const nb_handle *h, Workspace &ws,
 // the whole solve as one persistent cooperative kernel (grid size: grid_mega)
 template <int PREC> int grid_mega(const nb_handle *h);
 struct MegaArgs;
+struct MultiArgs;
 template <int PREC, int VAR> int grid_mega_var(const nb_handle *h);
+// multi-rank (z-slab) solves: args of one slab, grid of one GPU, the launch (nb_mega_tma.cuh)
+template <int PREC>
+void fill_mega_args(const nb_handle *h, Workspace &ws, const void *b, int order, int max_iter, double rtol,
+                    int precond, int x64, unsigned long long *tim, MegaArgs &A);
+template <int PREC> int grid_mega_mr(const nb_handle *h);
+template <int PREC> cudaError_t launch_cg_mr(const nb_handle *h0, const MultiArgs &M, cudaStream_t st);
 template <int PREC, int VAR>
 cudaError_t launch_cg_mega_var(const nb_handle *h, const MegaArgs &A, bool fused, cudaStream_t st);
 template <int PREC> cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int order,

@@ -542,10 +542,9 @@ cudaError_t launch_cg_mega_var(const nb_handle *h, const MegaArgs &A, bool fused
 }
 
 template <int PREC>
-cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int order, int max_iter, double rtol,
-                           int precond, int x64, unsigned long long *tim, cudaStream_t st)
+void fill_mega_args(const nb_handle *h, Workspace &ws, const void *b, int order, int max_iter, double rtol, int precond,
+                    int x64, unsigned long long *tim, MegaArgs &A)
 {
-    MegaArgs A;
     A.m = h->md();
     A.b = b;
     A.pc = precond;
@@ -563,11 +562,62 @@ cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int
     A.partA = ws.red.part; A.partS = ws.red.part + W * ws.mega_G; A.partB = ws.red.part + 2 * W * ws.mega_G;
     A.bar = ws.bar;
     A.scal = ws.scal;
+    A.wlo = ws.peer.wlo;
+    A.whi = ws.peer.whi;
+}
+
+template <int PREC>
+cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int order, int max_iter, double rtol,
+                           int precond, int x64, unsigned long long *tim, cudaStream_t st)
+{
+    MegaArgs A;
+    fill_mega_args<PREC>(h, ws, b, order, max_iter, rtol, precond, x64, tim, A);
+    A.wlo = A.whi = nullptr;
     const bool fused = order == NB_GS_CONSISTENT && !h->cg_csr;
     cudaError_t e = cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned int), st);   // barrier epoch 0
     if (e != cudaSuccess) return e;
     const bool var = precond != NB_PC_JACOBI || A.x64;
     return var ? launch_cg_mega_var<PREC, 1>(h, A, fused, st) : launch_cg_mega_var<PREC, 0>(h, A, fused, st);
+}
+
+// ---- multi-rank (z-slab) megakernel: consistent order, runtime options ----
+template <int PREC, int N>
+static int mr_occupancy()
+{
+    using C = AxCfg<typename Pol<PREC>::TV, N>;
+    static int occ = -1;
+    if (occ < 0) {
+        const void *fn = (const void *)k_cg_mega_mr<PREC, N>;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, C::NT, C::SMEM);
+        occ = o > 0 ? o : 1;
+    }
+    return occ;
+}
+
+template <int PREC>
+int grid_mega_mr(const nb_handle *h)
+{
+    NB_DISPATCH_N(h->n, return (h->sm_count * mr_occupancy<PREC, NN>()))
+}
+
+template <int PREC, int N>
+static cudaError_t mr_launch_t(const nb_handle *h, const MultiArgs &M, cudaStream_t st)
+{
+    using TV = typename Pol<PREC>::TV;
+    using C = AxCfg<TV, N>;
+    DMat<TV, N> D = make_dmat<TV, N>(h->D);
+    void *params[2] = {(void *)&M, (void *)&D};
+    (void)mr_occupancy<PREC, N>();
+    return cudaLaunchCooperativeKernel((const void *)k_cg_mega_mr<PREC, N>, dim3(M.mr.nloc * M.mr.Gr), dim3(C::NT),
+                                       params, (size_t)C::SMEM, st);
+}
+
+template <int PREC>
+cudaError_t launch_cg_mr(const nb_handle *h0, const MultiArgs &M, cudaStream_t st)
+{
+    NB_DISPATCH_N(h0->n, return (mr_launch_t<PREC, NN>(h0, M, st)))
 }
 
 }  // namespace nb

@@ -154,17 +154,18 @@ __global__ void k_dinv(const MeshDev m, const double *__restrict__ diag, double 
 }
 
 // GS segments (C-4): global nodes with multiplicity >= 2 in ascending gid; copies ascending l.
+// Built over the handle's own node lattice (a slab's nodes, multiplicity among its own copies).
 __device__ __forceinline__ int lattice_mult(int64_t I, int64_t NX, int p)
 {
     return (I % p == 0 && I > 0 && I < NX - 1) ? 2 : 1;
 }
 __global__ void k_gs_count(const MeshDev m, int32_t *__restrict__ flag, int32_t *__restrict__ cnt)
 {
-    for (int64_t gg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gg < m.NG; gg += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t gg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gg < m.NGl; gg += (int64_t)gridDim.x * blockDim.x) {
         const int64_t I = gg % m.NX;
         const int64_t t = gg / m.NX;
         const int64_t J = t % m.NY, K = t / m.NY;
-        const int mu = lattice_mult(I, m.NX, m.p) * lattice_mult(J, m.NY, m.p) * lattice_mult(K, m.NZ, m.p);
+        const int mu = lattice_mult(I, m.NX, m.p) * lattice_mult(J, m.NY, m.p) * lattice_mult(K, m.NZl, m.p);
         flag[gg] = mu >= 2;
         cnt[gg] = mu >= 2 ? mu : 0;
     }
@@ -172,7 +173,7 @@ __global__ void k_gs_count(const MeshDev m, int32_t *__restrict__ flag, int32_t 
 __global__ void k_gs_offsets(const MeshDev m, const int32_t *__restrict__ flag, const int32_t *__restrict__ segid,
                              const int32_t *__restrict__ segoff, int32_t *__restrict__ off, int32_t nseg, int32_t ncopies)
 {
-    for (int64_t gg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gg < m.NG; gg += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t gg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gg < m.NGl; gg += (int64_t)gridDim.x * blockDim.x)
         if (flag[gg]) off[segid[gg]] = segoff[gg];
     if (blockIdx.x == 0 && threadIdx.x == 0) off[nseg] = ncopies;
 }
@@ -186,14 +187,15 @@ __global__ void k_gs_fill(const MeshDev m, const int32_t *__restrict__ flag, con
         const int rq = (int)(l - e * n3);
         const int i = rq % n, j = (rq / n) % n, k = rq / (n * n);
         const ElemPos P = elem_pos(m, (int32_t)e);
-        const int64_t I = (int64_t)P.ex * p + i, J = (int64_t)P.ey * p + j, K = (int64_t)P.ez * p + k;
+        const int zl = P.ez - m.ez0;   // layer within the slab
+        const int64_t I = (int64_t)P.ex * p + i, J = (int64_t)P.ey * p + j, K = (int64_t)zl * p + k;
         const int64_t gg = I + m.NX * (J + m.NY * K);
         if (!flag[gg]) continue;
         // copies of gg are ordered by ascending element index = lexicographic (ez, ey, ex)
         const int cx = axis_mult(i, n, P.ex, m.nelx), cy = axis_mult(j, n, P.ey, m.nely);
         const int rx = (cx == 2 && i == 0) ? 1 : 0;
         const int ry = (cy == 2 && j == 0) ? 1 : 0;
-        const int rz = (axis_mult(k, n, P.ez, m.nelz) == 2 && k == 0) ? 1 : 0;
+        const int rz = (axis_mult(k, n, zl, m.nelzl) == 2 && k == 0) ? 1 : 0;
         idx[segoff[gg] + rz * cy * cx + ry * cx + rx] = (int32_t)l;
     }
 }
@@ -305,24 +307,24 @@ cudaError_t build_gs(nb_handle *h, cudaStream_t st)
     size_t tb1 = 0, tb2 = 0;
     cudaError_t e;
 #define CK(x) do { e = (x); if (e != cudaSuccess) goto done; } while (0)
-    CK(cudaMalloc(&flag, sizeof(int32_t) * m.NG));
-    CK(cudaMalloc(&cnt, sizeof(int32_t) * m.NG));
-    CK(cudaMalloc(&segid, sizeof(int32_t) * m.NG));
-    CK(cudaMalloc(&segoff, sizeof(int32_t) * m.NG));
+    CK(cudaMalloc(&flag, sizeof(int32_t) * m.NGl));
+    CK(cudaMalloc(&cnt, sizeof(int32_t) * m.NGl));
+    CK(cudaMalloc(&segid, sizeof(int32_t) * m.NGl));
+    CK(cudaMalloc(&segoff, sizeof(int32_t) * m.NGl));
     {
-        const int grid = grid_for(m.NG, 256, h->sm_count, 16);
+        const int grid = grid_for(m.NGl, 256, h->sm_count, 16);
         k_gs_count<<<grid, 256, 0, st>>>(m, flag, cnt);
         CK(cudaGetLastError());
-        CK(cub::DeviceScan::ExclusiveSum(nullptr, tb1, flag, segid, (int)m.NG, st));
-        CK(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt, segoff, (int)m.NG, st));
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tb1, flag, segid, (int)m.NGl, st));
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt, segoff, (int)m.NGl, st));
         CK(cudaMalloc(&tmp, tb1 > tb2 ? tb1 : tb2));
-        CK(cub::DeviceScan::ExclusiveSum(tmp, tb1, flag, segid, (int)m.NG, st));
-        CK(cub::DeviceScan::ExclusiveSum(tmp, tb2, cnt, segoff, (int)m.NG, st));
+        CK(cub::DeviceScan::ExclusiveSum(tmp, tb1, flag, segid, (int)m.NGl, st));
+        CK(cub::DeviceScan::ExclusiveSum(tmp, tb2, cnt, segoff, (int)m.NGl, st));
         int32_t last[4];
-        CK(cudaMemcpyAsync(&last[0], segid + m.NG - 1, 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&last[1], flag + m.NG - 1, 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&last[2], segoff + m.NG - 1, 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&last[3], cnt + m.NG - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&last[0], segid + m.NGl - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&last[1], flag + m.NGl - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&last[2], segoff + m.NGl - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&last[3], cnt + m.NGl - 1, 4, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         h->nseg = (int64_t)last[0] + last[1];
         h->ncopies = (int64_t)last[2] + last[3];
