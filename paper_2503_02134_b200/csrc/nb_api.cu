@@ -148,6 +148,11 @@ int ensure_f32(nb_handle *h)
 int ensure_ws(nb_handle *h, int prec, int32_t max_iter)
 {
     nb::Workspace &ws = h->ws[prec];
+    if (!ws.ctl) {
+        // multi-rank control block (small; allocated first so later allocations keep their layout)
+        NB_CU(cudaMalloc(&ws.ctl, nb::NB_CTL_BYTES), "cudaMalloc ctl");
+        NB_CU(cudaMemset(ws.ctl, 0, nb::NB_CTL_BYTES), "memset ctl");
+    }
     if (!ws.ready) {
         const size_t vs = vsize(prec) * h->NL;
         NB_CU(cudaMalloc(&ws.r, vs), "cudaMalloc r");
@@ -171,8 +176,6 @@ int ensure_ws(nb_handle *h, int prec, int32_t max_iter)
         NB_CU(cudaMalloc(&ws.red.part2, sizeof(double) * 2 * nchunk), "cudaMalloc part2");
         NB_CU(cudaMalloc(&ws.red.cnt, sizeof(uint32_t) * (1 + nchunk)), "cudaMalloc cnt");
         NB_CU(cudaMemset(ws.red.cnt, 0, sizeof(uint32_t) * (1 + nchunk)), "memset cnt");
-        NB_CU(cudaMalloc(&ws.ctl, nb::NB_CTL_BYTES), "cudaMalloc ctl");
-        NB_CU(cudaMemset(ws.ctl, 0, nb::NB_CTL_BYTES), "memset ctl");
         NB_CU(cudaMalloc(&ws.scal, sizeof(nb::Scal)), "cudaMalloc scal");
         NB_CU(cudaMallocHost(&ws.scal_host, sizeof(nb::Scal)), "cudaMallocHost scal");
         NB_CU(cudaMemset(ws.scal, 0, sizeof(nb::Scal)), "memset scal");

@@ -129,7 +129,7 @@ __device__ __forceinline__ void st_chunk(T *__restrict__ p, const T (&d)[V])
 #ifndef NB_PHASE_ATTR
 #define NB_PHASE_ATTR __forceinline__
 #endif
-template <int PREC, int N, int MODE>
+template <int PREC, int N, int MODE, bool SLAB = false>
 __device__ NB_PHASE_ATTR Acc<PREC>
 ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typename Pol<PREC>::TV *__restrict__ in,
          typename Pol<PREC>::TV *__restrict__ pv, typename Pol<PREC>::TV *__restrict__ xv,
@@ -262,7 +262,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
             for (int i = 0; i < N; i++) out[i] = (wrt[i] + t1[i]) + t2[i];
         }
         if (MODE != 0 || apply_mask) {
-            const ElemPos P = elem_pos(m, e);
+            const ElemPos P = elem_pos<SLAB>(m, e);
             const bool mjk = axis_bnd(a, N, P.ey, m.nely) || axis_bnd(b, N, P.ez, m.nelz);
 #pragma unroll
             for (int i = 0; i < N; i++)
@@ -354,7 +354,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
             for (int i = 0; i < N; i++) out[i] = (t0[i] + t1[i]) + t2[i];
         }
         if (MODE != 0 || apply_mask) {
-            const ElemPos P = elem_pos(m, e);
+            const ElemPos P = elem_pos<SLAB>(m, e);
             const bool mjk = axis_bnd(a, N, P.ey, m.nely) || axis_bnd(b, N, P.ez, m.nelz);
 #pragma unroll
             for (int i = 0; i < N; i++)
@@ -483,7 +483,7 @@ __device__ __forceinline__ typename Pol<PREC>::TV solve_m(typename Pol<PREC>::TV
     return (TV)((typename Pol<PREC>::TJ)r * d);
 }
 
-template <int PREC, int N, int GATHER>
+template <int PREC, int N, int GATHER, bool SLAB = false>
 __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ w,
                                            typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
                                            const void *__restrict__ dinv,
@@ -501,7 +501,7 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
     const size_t base = (size_t)pid * N;
     TV ww[N], rr[N], zz[N];
     TJ dd[N];
-    const ElemPos P = elem_pos(m, e);
+    const ElemPos P = elem_pos<SLAB>(m, e);
     ld_pencil<TV, N, NB_WLD>(w + base, ww);
     ld_pencil<TV, N>(r + base, rr);
     ld_dinv<TJ, N>(dinv, base, pc, dd);
@@ -526,7 +526,7 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
 }
 
 // CG prologue for one pencil: r = b, x = 0, p = 0, z = M^-1 r; rtr0 and rho_1 partials.
-template <int PREC, int N>
+template <int PREC, int N, bool SLAB = false>
 __device__ __forceinline__ void init_pencil(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ bvec,
                                             typename Pol<PREC>::TV *__restrict__ x, typename Pol<PREC>::TV *__restrict__ pv,
                                             typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
@@ -541,7 +541,7 @@ __device__ __forceinline__ void init_pencil(const MeshDev &m, const typename Pol
     const int q = (int)(pid - (int64_t)e * N2);
     const int a = q % N, b = q / N;
     const size_t base = (size_t)pid * N;
-    const ElemPos P = elem_pos(m, e);
+    const ElemPos P = elem_pos<SLAB>(m, e);
     TV rr[N], zz[N], zero[N];
     TD dd[N];
     ld_pencil<TV, N>(bvec + base, rr);
@@ -799,214 +799,19 @@ __device__ __forceinline__ void mr_reduce(const MegaArgs &A, const MrArgs &mr, i
     for (int k = 0; k < K; k++) tot[k] = bc[k];
 }
 
+
 // The solve of one slab (or the whole box) by the blocks [0, G) of its rank (bid = block index
 // within the rank).  VAR = 0: the default options (Jacobi, x in the policy precision) folded at
 // compile time; VAR = 1: the NEXT-3 variants (nb_cg_opts.precond / .x_fp64) as uniform runtime
 // selects; VAR = 2: VAR 1 as one rank of a multi-rank z-slab solve (mr, vr: slab in the launch).
 template <int PREC, int N, int FUSED, int VAR>
-__device__ __forceinline__ void cg_mega_body(const MegaArgs &A, const DMat<typename Pol<PREC>::TV, N> &D,
-                                             const MrArgs *mr, int vr, int bid, int G)
-{
-    using TV = typename Pol<PREC>::TV;
-    using TJ = typename Pol<PREC>::TJ;
-    using TS = typename Pol<PREC>::TS;
-    using C = AxCfg<TV, N>;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    __shared__ __align__(8) unsigned char acc_raw[64 * sizeof(Acc<PREC>)];   // no constructors in smem
-    Acc<PREC> *const acc_sh = reinterpret_cast<Acc<PREC> *>(acc_raw);
-    // Solver state lives in shared memory, not registers: it is live across both phases,
-    // and every register it held would be taken from the phases' pencils (occupancy).
-    struct State {
-        TS rtr0, rho, rtr, beta, alpha, pap;
-        int it, status, pending, done;
-    };
-    __shared__ State st;
-    const int tid = threadIdx.x;
-    // the block index and count of the rank: the hardware registers unless several slabs share the launch
-#define NB_BID (VAR == 2 ? bid : (int)blockIdx.x)
-#define NB_GR (VAR == 2 ? G : (int)gridDim.x)
-    const bool t0 = (NB_BID == 0 && tid == 0);
-    unsigned int tgt = 0;   // grid-barrier arrival target (thread 0)
-    unsigned int ep = VAR == 2 ? mr->epoch0 : 0u;   // cross-rank barrier epoch (VAR 2)
-    const TV *const wlo = VAR == 2 ? (const TV *)A.wlo : nullptr;
-    const TV *const whi = VAR == 2 ? (const TV *)A.whi : nullptr;
-#define NB_G0 split(((int64_t)A.m.E + C::EPB - 1) / C::EPB, NB_GR, NB_BID)
-#define NB_G1 split(((int64_t)A.m.E + C::EPB - 1) / C::EPB, NB_GR, NB_BID + 1)
-#define NB_EL (threadIdx.x / C::N2)
-#define NB_A ((threadIdx.x - NB_EL * C::N2) % N)
-#define NB_B ((threadIdx.x - NB_EL * C::N2) / N)
-#define NB_S0 (reinterpret_cast<TV *>(smraw) + (NB_EL < C::EPB ? NB_EL : 0) * 3 * C::ESZ)
-    // block partials -> grid barrier (thread 0) -> every block sums all partials in fixed order
-#define NB_GRID_REDUCE(K, VALS, PART, TOT)                                             \
-    do {                                                                                \
-        block_reduce_acc<PREC, K>(VALS, acc_sh);                                        \
-        if constexpr (VAR == 2) {                                                       \
-            ep++;                                                                       \
-            mr_reduce<PREC, K>(A, *mr, vr, bid, G, VALS, PART, tgt, ep, TOT, acc_sh);   \
-        } else {                                                                        \
-            if (tid == 0) {                                                             \
-                _Pragma("unroll") for (int k_ = 0; k_ < K; k_++)                        \
-                    VALS[k_].store((PART) + ((size_t)NB_BID * K + k_) * Acc<PREC>::W);  \
-                tgt += NB_GR;                                                           \
-                grid_arrive_wait(A.bar, tgt);                                           \
-            }                                                                           \
-            __syncthreads();                                                            \
-            all_blocks_reduce_acc<PREC, K>(PART, NB_GR, TOT, acc_sh);                   \
-        }                                                                               \
-    } while (0)
-
-    // ---- prologue: r = b, x = p = 0, z = M^-1 r; rtr0, rho_1
-    {
-        const int64_t p0 = min((int64_t)A.m.E, NB_G0 * C::EPB) * C::N2;
-        const int64_t p1 = min((int64_t)A.m.E, NB_G1 * C::EPB) * C::N2;
-        Acc<PREC> v[2];
-#pragma unroll 1
-        for (int64_t pid = p0 + tid; pid < p1; pid += blockDim.x)
-            init_pencil<PREC, N>(A.m, (const TV *)A.b, (TV *)A.x, (TV *)A.p, (TV *)A.r, (TV *)A.z, A.dinv, pid, v[0],
-                                 v[1], VAR && A.x64 != 0, VAR ? A.pc : NB_PC_JACOBI);
-        TS tot[2];
-        NB_GRID_REDUCE(2, v, A.partB, tot);
-        if (t0 && A.tim) A.tim[0] = globaltimer();
-        if (tid == 0) {
-            const TS rtr0 = tot[0], rho = tot[1];
-            st.rtr0 = rtr0; st.rho = rho; st.rtr = rtr0; st.beta = 0; st.alpha = 0; st.pap = 0;
-            st.it = 0; st.status = NB_MAXITER; st.pending = 0; st.done = 0;
-            if (rtr0 == (TS)0) { st.status = NB_CONVERGED; st.done = 1; }
-            else if (!isfinite((double)rtr0)) { st.status = NB_BROKEDOWN; st.done = 1; }
-            else if (A.max_iter <= 0) { st.status = NB_MAXITER; st.done = 1; }
-            if (NB_BID == 0) A.hist[0] = rtr0 == (TS)0 ? 0.0 : 1.0;
-        }
-        __syncthreads();
-    }
-
-#pragma unroll 1
-    while (!st.done) {
-        // ---- phase A: p update, deferred x update, w = mask A_L p, pap partial
-        TS pap;
-        {
-            Acc<PREC> v[1];
-            const TV bv = (TV)st.beta, av = st.pending ? (TV)st.alpha : TV(0);
-            double *const xd = (VAR && PREC == NB_MIXED && A.x64) ? (double *)A.x : nullptr;
-            const double ad = st.pending ? (double)st.alpha : 0.0;
-            const int64_t g1 = NB_G1;
-#pragma unroll 1
-            for (int64_t gr = NB_G0; gr < g1; gr++) {
-                const int e = (int)(gr * C::EPB) + NB_EL;
-                const bool active = NB_EL < C::EPB && e < A.m.E;
-                v[0].merge(ax_group<PREC, N, FUSED ? 1 : 2>(A.m, D, (const TV *)A.z, (TV *)A.p, (TV *)A.x,
-                                                         (const TV *)A.g, (TV *)A.w, true, bv, av, e, active, NB_A,
-                                                         NB_B, NB_S0, xd, ad));
-            }
-            TS tot[1];
-            NB_GRID_REDUCE(1, v, A.partA, tot);
-            pap = tot[0];
-        }
-        if (t0 && A.tim) A.tim[3 * st.it + 1] = globaltimer();
-        if (!FUSED) {
-            // ---- CSR gather-scatter phase: per-copy (or consistent) QQ^T, shared pap partial
-            const int64_t s0 = split(A.nseg, NB_GR, NB_BID), s1 = split(A.nseg, NB_GR, NB_BID + 1);
-            Acc<PREC> v[1];
-            for (int64_t s = s0 + tid; s < s1; s += blockDim.x) {
-                if (A.order == NB_GS_CONSISTENT)
-                    v[0].merge(gs_segment<PREC, NB_GS_CONSISTENT, 1, TV, typename Pol<PREC>::TG, LD_CG>(
-                        (int32_t)s, A.gs_off, A.gs_idx, (TV *)A.w, (const TV *)A.p));
-                else
-                    v[0].merge(gs_segment<PREC, NB_GS_PER_COPY, 1, TV, typename Pol<PREC>::TG, LD_CG>(
-                        (int32_t)s, A.gs_off, A.gs_idx, (TV *)A.w, (const TV *)A.p));
-            }
-            TS tot[1];
-            NB_GRID_REDUCE(1, v, A.partS, tot);
-            pap = pap + tot[0];
-        }
-        if (t0 && A.tim) A.tim[3 * st.it + 2] = globaltimer();
-        if (tid == 0) {
-            st.pap = pap;
-            if (!(pap > (TS)0) || !isfinite((double)pap) || !isfinite((double)st.rho)) {
-                st.status = NB_BROKEDOWN;
-                st.pending = 0;     // x already holds x_k (alpha_prev p_old applied in phase A)
-                st.done = 2;
-            } else {
-                st.alpha = st.rho / pap;
-                st.pending = 1;
-            }
-        }
-        __syncthreads();
-        if (st.done) break;
-        // ---- phase B: (gather) r -= alpha w, z = M^-1 r, rtr and rho partials
-        {
-            Acc<PREC> v[2];
-            const TV av = (TV)st.alpha;
-            const int64_t g1 = NB_G1;
-            const int e_end = (int)min((int64_t)A.m.E, g1 * C::EPB);
-            const int64_t p1 = (int64_t)e_end * C::N2;
-            const int pc = VAR ? A.pc : NB_PC_JACOBI;
-#pragma unroll 1
-            for (int64_t pid = NB_G0 * C::EPB * C::N2 + tid; pid < p1; pid += blockDim.x)
-                if constexpr (VAR == 2)
-                    upd_pencil<PREC, N, FUSED>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, A.dinv, av, pid, v[0], v[1],
-                                               pc, wlo, whi);
-                else
-                    upd_pencil<PREC, N, FUSED>(A.m, (const TV *)A.w, (TV *)A.r, (TV *)A.z, A.dinv, av, pid, v[0], v[1],
-                                               pc);
-            TS tot[2];
-            NB_GRID_REDUCE(2, v, A.partB, tot);
-            if (tid == 0) {
-                const TS rtr = tot[0], rho_new = tot[1];
-                const int it = st.it + 1;
-                const double res = sqrt((double)rtr / (double)st.rtr0);
-                if (NB_BID == 0) {
-                    A.hist[it] = res;
-                    if (A.tim) A.tim[3 * it] = globaltimer();
-                }
-                if (!isfinite((double)rtr) || !isfinite((double)rho_new)) { st.status = NB_BROKEDOWN; st.done = 1; }
-                else if (res <= A.rtol || rtr == (TS)0) { st.status = NB_CONVERGED; st.done = 1; }
-                else if (it >= A.max_iter) { st.status = NB_MAXITER; st.done = 1; }
-                st.beta = rho_new / st.rho;
-                st.rho = rho_new;
-                st.rtr = rtr;
-                st.it = it;
-            }
-            __syncthreads();
-        }
-    }
-    // ---- epilogue: the deferred x += alpha p of the last iteration (own elements)
-    if (st.pending) {
-        const TV av = (TV)st.alpha;
-        const int64_t l0 = min((int64_t)A.m.E, NB_G0 * C::EPB) * C::N3;
-        const int64_t l1 = min((int64_t)A.m.E, NB_G1 * C::EPB) * C::N3;
-        const TV *pv = (const TV *)A.p;
-        if (VAR && PREC == NB_MIXED && A.x64) {
-            double *x = (double *)A.x;
-            const double ad = (double)st.alpha;
-            for (int64_t l = l0 + tid; l < l1; l += blockDim.x) x[l] = fma(ad, (double)pv[l], x[l]);
-        } else {
-            TV *x = (TV *)A.x;
-            for (int64_t l = l0 + tid; l < l1; l += blockDim.x) x[l] = fma(av, pv[l], x[l]);
-        }
-    }
-    if (t0) {
-        Scal *s = A.scal;
-        s->rho = (double)st.rho; s->beta = (double)st.beta; s->alpha = (double)st.alpha; s->pap = (double)st.pap;
-        s->rtr = (double)st.rtr; s->rtr0 = (double)st.rtr0; s->iter = st.it; s->status = st.status; s->done = 1;
-        s->pending = 0;
-        s->epochs = VAR == 2 ? (int32_t)(ep - mr->epoch0) : 0;
-    }
-#undef NB_GRID_REDUCE
-#undef NB_G0
-#undef NB_G1
-#undef NB_EL
-#undef NB_A
-#undef NB_B
-#undef NB_S0
-#undef NB_BID
-#undef NB_GR
-}
-
-template <int PREC, int N, int FUSED, int VAR>
 __global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT, AxCfg<typename Pol<PREC>::TV, N>::MINB)
 k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D)
 {
-    cg_mega_body<PREC, N, FUSED, VAR>(A, D, nullptr, 0, blockIdx.x, gridDim.x);
+    static_assert(VAR == 0 || VAR == 1, "k_cg_mega: VAR 0 or 1 (VAR 2 is k_cg_mega_mr)");
+    const MrArgs *const mr = nullptr;
+    const int vr = 0, bid = 0, G = 0;
+#include "nb_mega_body.inc"
 }
 
 // Multi-rank solve: nloc slabs in this launch, Gr blocks each (cooperative launch, so the
@@ -1015,9 +820,13 @@ template <int PREC, int N>
 __global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT, AxCfg<typename Pol<PREC>::TV, N>::MINB)
 k_cg_mega_mr(const __grid_constant__ MultiArgs M, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D)
 {
+    constexpr int FUSED = 1, VAR = 2;
     const int vr = blockIdx.x / M.mr.Gr;
     if (vr >= M.mr.nloc) return;
-    cg_mega_body<PREC, N, 1, 2>(M.a[vr], D, &M.mr, vr, blockIdx.x - vr * M.mr.Gr, M.mr.Gr);
+    const MegaArgs &A = M.a[vr];
+    const MrArgs *const mr = &M.mr;
+    const int bid = blockIdx.x - vr * M.mr.Gr, G = M.mr.Gr;
+#include "nb_mega_body.inc"
 }
 
 // ===========================================================================
@@ -1052,7 +861,9 @@ k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
     for (int64_t gr = g0; gr < g1; gr++) {
         const int e = (int)(gr * C::EPB) + el;
         const bool active = el < C::EPB && e < m.E;
-        acc += ax_group<PREC, N, MODE>(m, D, in, pv, xv, g, w, apply_mask != 0, beta, alpha, e, active, a, b, S0)
+        // standalone operator (MODE 0): the handle may be a z-slab (global mask layers)
+        acc += ax_group<PREC, N, MODE, MODE == 0>(m, D, in, pv, xv, g, w, apply_mask != 0, beta, alpha, e, active, a, b,
+                                                  S0)
                    .value();
     }
     if (MODE == 0) return;

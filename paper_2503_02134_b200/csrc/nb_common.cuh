@@ -272,6 +272,9 @@ __device__ __forceinline__ void cp_pencil_async(T *sdst, const T *gsrc)
 struct ElemPos {
     int32_t ex, ey, ez;
 };
+// SLAB: the mesh may be a z-slab (global layer = local + ez0).  The whole-box megakernels use
+// SLAB = false: the extra add measurably slowed the fp32 phase A.
+template <bool SLAB = true>
 __device__ __forceinline__ ElemPos elem_pos(const MeshDev &m, int32_t e)
 {
     ElemPos r;
@@ -279,7 +282,7 @@ __device__ __forceinline__ ElemPos elem_pos(const MeshDev &m, int32_t e)
     r.ex = e - t * m.nelx;
     const int32_t zl = t / m.nely;
     r.ey = t - zl * m.nely;
-    r.ez = zl + m.ez0;   // global layer (slabs: SURVEY.md §8(e))
+    r.ez = SLAB ? zl + m.ez0 : zl;   // global layer (slabs: SURVEY.md §8(e))
     return r;
 }
 // multiplicity factor along one axis for local index i of element coordinate ex (nel elements)

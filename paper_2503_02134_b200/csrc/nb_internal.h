@@ -54,10 +54,10 @@ struct RedWs {
 struct MeshDev {
     int32_t nelx, nely, nelz, p, n;   // the whole box (nelz: global layer count)
     int32_t E;                        // elements held here (a z-slab of the box, or all of it)
-    int32_t ez0, nelzl;               // slab: first global z layer and layer count (box: 0, nelz)
     int64_t NL, NX, NY, NZ, NG;       // NL local; NX, NY, NZ, NG: the global node lattice
-    int64_t NZl, NGl;                 // the slab's own node lattice (its GS segments)
     int32_t nseg;
+    int32_t ez0, nelzl;               // slab: first global z layer and layer count (box: 0, nelz)
+    int64_t NZl, NGl;                 // the slab's own node lattice (its GS segments)
 };
 
 // Arguments of the persistent CG megakernel (nb_cg.cuh), one slab's (or the whole box's) solve

@@ -155,7 +155,7 @@ ax_group_tma(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const t
 #pragma unroll
             for (int i = 0; i < N; i++) out[i] = (t0[i] + t1[i]) + t2[i];
         }
-        const ElemPos P = elem_pos(m, e);
+        const ElemPos P = elem_pos<false>(m, e);
         const bool mjk = axis_bnd(a, N, P.ey, m.nely) || axis_bnd(b, N, P.ez, m.nelz);
 #pragma unroll
         for (int i = 0; i < N; i++)
@@ -192,7 +192,7 @@ __device__ __forceinline__ void upd_group_tma(const MeshDev &m, const typename P
     const int off = el * N3 + q * N;
     if (active) {
         const size_t base = ((size_t)e * N2 + q) * N;
-        const ElemPos P = elem_pos(m, e);
+        const ElemPos P = elem_pos<false>(m, e);
         TV ww[N];
         ld_pencil<TV, N>(sw + off, ww);
         if (GATHER) {

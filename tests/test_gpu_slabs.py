@@ -182,3 +182,28 @@ def test_peer_attach_single_rank_repeated_solves():
     assert torch.equal(x2, x0)
     g.close()
     ref.close()
+
+
+def test_slab_operator_matches_box():
+    """nb_ax on a slab: the local operator equals the box's slice bit-for-bit, and the masked,
+    (slab-)assembled operator equals the box's away from the slab interface planes (global mask)."""
+    nel, p = (5, 4, 6), 5
+    n = p + 1
+    box = nb.Mesh(*nel, p, deform=0.1, seed=0)
+    u = box.rhs(nb.NB_FP64, seed=4)
+    wl = box.ax(u, nb.NB_FP64, local=True).cpu().numpy()
+    wa = box.ax(u, nb.NB_FP64).cpu().numpy()
+    off = 0
+    for m in slabs(nel, p, 2, deform=0.1):
+        nl = m.n_local
+        us = u[off:off + nl].clone()
+        assert np.array_equal(m.ax(us, nb.NB_FP64, local=True).cpu().numpy(), wl[off:off + nl])
+        ws = m.ax(us, nb.NB_FP64).cpu().numpy()
+        k = (np.arange(nl) // (n * n)) % n                       # local k of every node
+        ez = m.info.ez0 + np.arange(nl) // (n ** 3) // (nel[0] * nel[1])
+        interface = ((k == 0) & (ez == m.info.ez0) & (m.info.ez0 > 0)) | \
+                    ((k == n - 1) & (ez == m.info.ez0 + m.info.nelz_local - 1) & (ez < nel[2] - 1))
+        np.testing.assert_allclose(ws[~interface], wa[off:off + nl][~interface], rtol=1e-13, atol=1e-13)
+        off += nl
+        m.close()
+    box.close()
