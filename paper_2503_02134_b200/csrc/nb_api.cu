@@ -578,11 +578,12 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
                 M.mr.slot[r] = (double *)(ws.ctl + nb::NB_CTL_FLAG_BYTES);
                 NB_CU(cudaMemsetAsync(ws.ctl, 0, nb::NB_CTL_BYTES, st), "memset ctl");
             }
-            M.mr.nrank = nh; M.mr.rank0 = 0; M.mr.nloc = nh; M.mr.epoch0 = 0;
+            M.mr.nrank = nh; M.mr.rank0 = 0; M.mr.nloc = nh; M.mr.epoch0 = 0; M.mr.sys = 0;
         } else {
             const nb::PeerState &ps = ws0.peer;
             for (int q = 0; q < ps.nrank; q++) { M.mr.flag[q] = ps.flag[q]; M.mr.slot[q] = ps.slot[q]; }
             M.mr.nrank = ps.nrank; M.mr.rank0 = ps.rank; M.mr.nloc = 1; M.mr.epoch0 = ps.epoch;
+            M.mr.sys = ps.nrank > 1 ? 1 : 0;
         }
         M.mr.Gr = NB_POL(prec, nb::grid_mega_mr, h0) / nh;
         if (M.mr.Gr < 1) return fail(NB_EINVAL, "too many slabs for one launch");

@@ -734,10 +734,11 @@ __device__ __forceinline__ unsigned int ld_acquire_sys_u32(const unsigned int *p
 }
 
 // Multi-rank reduction + barrier (VAR = 2), after block_reduce_acc left this block's K values
-// in thread 0 of VALS: block partials -> local barrier -> block 0 sums its rank's partials
-// (fixed order) and pushes them to every rank's slot array, bumps every rank's flag, waits for
-// all R ranks, releases its blocks -> every block merges the R rank partials in rank order
-// (bit-identical in every block of every rank).
+// in thread 0 of VALS: block partials -> rank-local grid barrier -> every block sums its rank's
+// partials (fixed order, the same value in every block) -> block 0 pushes that rank partial into
+// every rank's slot array and bumps every rank's flag -> every block waits until its rank's flag
+// counts all R pushes and merges the R rank partials in rank order (bit-identical in every block
+// of every rank).  One local barrier, one push, one flag wait per reduction.
 template <int PREC, int K>
 __device__ __forceinline__ void mr_reduce(const MegaArgs &A, const MrArgs &mr, int vr, int bid, int G,
                                           Acc<PREC> (&vals)[K], double *part, unsigned int &tgt, unsigned int ep,
@@ -752,44 +753,44 @@ __device__ __forceinline__ void mr_reduce(const MegaArgs &A, const MrArgs &mr, i
 #pragma unroll
         for (int k = 0; k < K; k++) vals[k].store(part + ((size_t)bid * K + k) * W);
         tgt += G;
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.bar) : "memory");
+        grid_arrive_wait(A.bar, tgt);
     }
-    if (bid == 0) {
-        if (tid == 0)
-            while ((int)(ld_acquire_u32(A.bar) - tgt) < 0) {
-            }
-        __syncthreads();
-        Acc<PREC> s[K];
-        for (int i = tid; i < G; i += blockDim.x) {
+    __syncthreads();
+    Acc<PREC> s[K];
+    for (int i = tid; i < G; i += blockDim.x) {
 #pragma unroll
-            for (int k = 0; k < K; k++) s[k].merge(Acc<PREC>::load(part + ((size_t)i * K + k) * W));
-        }
-        block_reduce_acc<PREC, K>(s, acc_sh);
-        if (tid == 0) {
+        for (int k = 0; k < K; k++) s[k].merge(Acc<PREC>::load(part + ((size_t)i * K + k) * W));
+    }
+    block_reduce_acc<PREC, K>(s, acc_sh);   // the rank partial, in thread 0 of every block
+    if (tid == 0) {
+        const unsigned int want = (unsigned int)R * ep;
+        if (bid == 0) {
             for (int q = 0; q < R; q++) {
                 double *dst = mr.slot[q] + ((size_t)par * NB_MAX_RANKS + me) * 4;
 #pragma unroll
                 for (int k = 0; k < K; k++) s[k].store(dst + k * W);
             }
-            __threadfence_system();
-            for (int q = 0; q < R; q++)
-                asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(mr.flag[q]) : "memory");
-            const unsigned int want = (unsigned int)R * ep;
+        }
+        // the release orders the slot stores before the flag bumps; system scope only when ranks
+        // live on other GPUs (peer memory), GPU scope when they share this launch
+        if (mr.sys) {
+            if (bid == 0)
+                for (int q = 0; q < R; q++)
+                    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(mr.flag[q]) : "memory");
             while ((int)(ld_acquire_sys_u32(mr.flag[me]) - want) < 0) {
             }
-            st_release_u32(A.bar + 1, ep);
+        } else {
+            if (bid == 0)
+                for (int q = 0; q < R; q++)
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(mr.flag[q]) : "memory");
+            while ((int)(ld_acquire_u32(mr.flag[me]) - want) < 0) {
+            }
         }
-    } else if (tid == 0) {
-        while ((int)(ld_acquire_u32(A.bar + 1) - ep) < 0) {
-        }
-    }
-    __syncthreads();
-    if (tid == 0) {
         Acc<PREC> t[K];
         const double *src = mr.slot[me] + (size_t)par * NB_MAX_RANKS * 4;
         for (int q = 0; q < R; q++) {
 #pragma unroll
-            for (int k = 0; k < K; k++) t[k].merge(Acc<PREC>::load(src + (size_t)q * 4 + k * W));
+            for (int k = 0; k < K; k++) t[k].merge(q == me ? s[k] : Acc<PREC>::load(src + (size_t)q * 4 + k * W));
         }
 #pragma unroll
         for (int k = 0; k < K; k++) bc[k] = t[k].value();

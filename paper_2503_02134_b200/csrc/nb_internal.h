@@ -93,6 +93,7 @@ struct MrArgs {
     int32_t nloc;            // slabs in this launch (1: one per GPU; >1: slabs sharing this GPU)
     int32_t Gr;              // blocks per slab
     uint32_t epoch0;         // barrier epochs completed by earlier solves
+    int32_t sys;             // 1: ranks on other GPUs (system-scope flags); 0: all in this launch
     unsigned int *flag[NB_MAX_RANKS];
     double *slot[NB_MAX_RANKS];
 };
