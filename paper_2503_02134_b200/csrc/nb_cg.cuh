@@ -126,9 +126,27 @@ __device__ __forceinline__ void st_chunk(T *__restrict__ p, const T (&d)[V])
 #ifndef NB_AXV64
 #define NB_AXV64 2
 #endif
+#ifndef NB_ELEM_BAR
+#define NB_ELEM_BAR 1
+#endif
 #ifndef NB_PHASE_ATTR
 #define NB_PHASE_ATTR __forceinline__
 #endif
+// Barrier over the threads of one element of the group: a named barrier per element when the
+// elements are warp-aligned (their shared-memory slots are disjoint, so elements of one block
+// need not wait for each other), else the block barrier.
+template <int N2, int EPB>
+__device__ __forceinline__ void elem_sync()
+{
+#if NB_ELEM_BAR
+    if constexpr (N2 % 32 == 0 && EPB > 1 && EPB < 16) {
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / N2)), "r"(N2) : "memory");
+        return;
+    }
+#endif
+    __syncthreads();
+}
+
 template <int PREC, int N, int MODE, bool SLAB = false>
 __device__ NB_PHASE_ATTR Acc<PREC>
 ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typename Pol<PREC>::TV *__restrict__ in,
@@ -184,7 +202,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         }
         st_pencil<TV, N>(S0 + rp, u);
     }
-    __syncthreads();
+    elem_sync<C::N2, C::EPB>();
     // ---- 2. us (D along s) and ut (D along t) from shared pencils
     if (active) {
         TV v[N], o[N];
@@ -199,7 +217,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
 #pragma unroll
         for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
     }
-    __syncthreads();
+    elem_sync<C::N2, C::EPB>();
     Acc<PREC> acc;
     if constexpr (AXV == 0) {
     // ---- 3. ur in registers; geometric factors (C-7); r-part of local_grad3_t
@@ -235,7 +253,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         }
         contract_t<TV, N>(D, wr, wrt);
     }
-    __syncthreads();
+    elem_sync<C::N2, C::EPB>();
     // ---- 4. s- and t-parts of local_grad3_t, in place on the owner's pencils
     if (active) {
         TV v[N], o[N];
@@ -250,7 +268,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
 #pragma unroll
         for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
     }
-    __syncthreads();
+    elem_sync<C::N2, C::EPB>();
     // ---- 5. w = (w_r + w_s) + w_t, Dirichlet mask, store; CG: pap partial (p from S0)
     if (active) {
         TV out[N];
@@ -326,7 +344,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
             st_pencil<TV, N>(S0 + rp, o);
         }
     }
-    __syncthreads();
+    elem_sync<C::N2, C::EPB>();
     // ---- 4. s- and t-parts of local_grad3_t, in place on the owner's pencils
     if (active) {
         TV v[N], o[N];
@@ -341,7 +359,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
 #pragma unroll
         for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
     }
-    __syncthreads();
+    elem_sync<C::N2, C::EPB>();
     // ---- 5. w = (w_r + w_s) + w_t, Dirichlet mask, store
     if (active) {
         TV out[N];
