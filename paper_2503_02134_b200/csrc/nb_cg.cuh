@@ -71,8 +71,15 @@ template <typename T, int N> struct AxCfg {
     static constexpr int P = LAY == 1 ? 104 : LAY == 2 ? 88 : LAY == 3 ? 140 : LAY == 4 ? 172
                            : N2 + (((N - N2) % BANKS) + BANKS) % BANKS;
     static constexpr int ESZ = P * N;                          // one array, one element
-    static constexpr int EPB = (N2 >= 256) ? 1 : (256 / N2);   // elements per group
-    static constexpr int NT = ((EPB * N2 + 31) / 32) * 32;     // threads per block
+    // threads per element slot: N^2 (one per r-pencil), padded to whole warps for N = 10 so that
+    // the elements of a group can synchronise separately (named barriers, elem_sync); measured
+    // neutral at p = 9 (fp32 -2.5%, mixed +1%, fp64 +1%: the padding costs registers), so off
+#ifndef NB_PAD_ELEM
+#define NB_PAD_ELEM 0
+#endif
+    static constexpr int N2P = (NB_PAD_ELEM && N == 10) ? 128 : N2;
+    static constexpr int EPB = (N2P >= 256) ? 1 : (256 / N2P);  // elements per group
+    static constexpr int NT = ((EPB * N2P + 31) / 32) * 32;     // threads per block
     static constexpr int SMEM = 3 * EPB * ESZ * (int)sizeof(T);
     // resident blocks per SM the register allocation must allow (launch bound); fp64 pencils
     // need twice the registers
@@ -202,7 +209,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         }
         st_pencil<TV, N>(S0 + rp, u);
     }
-    elem_sync<C::N2, C::EPB>();
+    elem_sync<C::N2P, C::EPB>();
     // ---- 2. us (D along s) and ut (D along t) from shared pencils
     if (active) {
         TV v[N], o[N];
@@ -217,7 +224,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
 #pragma unroll
         for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
     }
-    elem_sync<C::N2, C::EPB>();
+    elem_sync<C::N2P, C::EPB>();
     Acc<PREC> acc;
     if constexpr (AXV == 0) {
     // ---- 3. ur in registers; geometric factors (C-7); r-part of local_grad3_t
@@ -253,7 +260,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         }
         contract_t<TV, N>(D, wr, wrt);
     }
-    elem_sync<C::N2, C::EPB>();
+    elem_sync<C::N2P, C::EPB>();
     // ---- 4. s- and t-parts of local_grad3_t, in place on the owner's pencils
     if (active) {
         TV v[N], o[N];
@@ -268,7 +275,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
 #pragma unroll
         for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
     }
-    elem_sync<C::N2, C::EPB>();
+    elem_sync<C::N2P, C::EPB>();
     // ---- 5. w = (w_r + w_s) + w_t, Dirichlet mask, store; CG: pap partial (p from S0)
     if (active) {
         TV out[N];
@@ -344,7 +351,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
             st_pencil<TV, N>(S0 + rp, o);
         }
     }
-    elem_sync<C::N2, C::EPB>();
+    elem_sync<C::N2P, C::EPB>();
     // ---- 4. s- and t-parts of local_grad3_t, in place on the owner's pencils
     if (active) {
         TV v[N], o[N];
@@ -359,7 +366,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
 #pragma unroll
         for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
     }
-    elem_sync<C::N2, C::EPB>();
+    elem_sync<C::N2P, C::EPB>();
     // ---- 5. w = (w_r + w_s) + w_t, Dirichlet mask, store
     if (active) {
         TV out[N];
@@ -864,8 +871,8 @@ k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
     extern __shared__ __align__(16) unsigned char smraw[];
     if (MODE != 0 && scal->done) return;   // grid-uniform
     const int tid = threadIdx.x;
-    const int el = tid / C::N2;
-    const int q = tid - el * C::N2;
+    const int el = tid / C::N2P;
+    const int q = tid - el * C::N2P;
     const int a = q % N, b = q / N;
     TV *S0 = reinterpret_cast<TV *>(smraw) + (el < C::EPB ? el : 0) * 3 * C::ESZ;
     TV beta = 0, alpha = 0;
@@ -879,7 +886,7 @@ k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
 #pragma unroll 1
     for (int64_t gr = g0; gr < g1; gr++) {
         const int e = (int)(gr * C::EPB) + el;
-        const bool active = el < C::EPB && e < m.E;
+        const bool active = el < C::EPB && q < C::N2 && e < m.E;
         // standalone operator (MODE 0): the handle may be a z-slab (global mask layers)
         acc += ax_group<PREC, N, MODE, MODE == 0>(m, D, in, pv, xv, g, w, apply_mask != 0, beta, alpha, e, active, a, b,
                                                   S0)
