@@ -774,51 +774,58 @@ __device__ __forceinline__ void mr_reduce(const MegaArgs &A, const MrArgs &mr, i
     const int tid = threadIdx.x;
     const int R = mr.nrank, me = mr.rank0 + vr, par = ep & 1;
     __shared__ TS bc[K];
-    if (tid == 0) {
+    if (tid < 32) {
+        if (tid == 0) {
 #pragma unroll
-        for (int k = 0; k < K; k++) vals[k].store(part + ((size_t)bid * K + k) * W);
-        tgt += G;
-        grid_arrive_wait(A.bar, tgt);
-    }
-    __syncthreads();
-    Acc<PREC> s[K];
-    for (int i = tid; i < G; i += blockDim.x) {
+            for (int k = 0; k < K; k++) vals[k].store(part + ((size_t)bid * K + k) * W);
+            tgt += G;
+            grid_arrive_wait(A.bar, tgt);
+        }
+        __syncwarp();
+        // warp 0: the rank partial (fixed order, the same value in every block of the rank)
+        Acc<PREC> s[K];
+        for (int i = tid; i < G; i += 32) {
 #pragma unroll
-        for (int k = 0; k < K; k++) s[k].merge(Acc<PREC>::load(part + ((size_t)i * K + k) * W));
-    }
-    block_reduce_acc<PREC, K>(s, acc_sh);   // the rank partial, in thread 0 of every block
-    if (tid == 0) {
-        const unsigned int want = (unsigned int)R * ep;
-        if (bid == 0) {
+            for (int k = 0; k < K; k++) s[k].merge(Acc<PREC>::load(part + ((size_t)i * K + k) * W));
+        }
+#pragma unroll
+        for (int k = 0; k < K; k++)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s[k].merge(s[k].shfl_down(o));
+        if (tid == 0) {
+            const unsigned int want = (unsigned int)R * ep;
+            if (bid == 0) {
+                for (int q = 0; q < R; q++) {
+                    double *dst = mr.slot[q] + ((size_t)par * NB_MAX_RANKS + me) * 4;
+#pragma unroll
+                    for (int k = 0; k < K; k++) s[k].store(dst + k * W);
+                }
+            }
+            // the release orders the slot stores before the flag bumps; system scope only when
+            // ranks live on other GPUs (peer memory), GPU scope when they share this launch
+            if (mr.sys) {
+                if (bid == 0)
+                    for (int q = 0; q < R; q++)
+                        asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(mr.flag[q]) : "memory");
+                while ((int)(ld_acquire_sys_u32(mr.flag[me]) - want) < 0) {
+                }
+            } else {
+                if (bid == 0)
+                    for (int q = 0; q < R; q++)
+                        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(mr.flag[q]) : "memory");
+                while ((int)(ld_acquire_u32(mr.flag[me]) - want) < 0) {
+                }
+            }
+            Acc<PREC> t[K];
+            const double *src = mr.slot[me] + (size_t)par * NB_MAX_RANKS * 4;
             for (int q = 0; q < R; q++) {
-                double *dst = mr.slot[q] + ((size_t)par * NB_MAX_RANKS + me) * 4;
 #pragma unroll
-                for (int k = 0; k < K; k++) s[k].store(dst + k * W);
+                for (int k = 0; k < K; k++)
+                    t[k].merge(q == me ? s[k] : Acc<PREC>::load(src + (size_t)q * 4 + k * W));
             }
-        }
-        // the release orders the slot stores before the flag bumps; system scope only when ranks
-        // live on other GPUs (peer memory), GPU scope when they share this launch
-        if (mr.sys) {
-            if (bid == 0)
-                for (int q = 0; q < R; q++)
-                    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(mr.flag[q]) : "memory");
-            while ((int)(ld_acquire_sys_u32(mr.flag[me]) - want) < 0) {
-            }
-        } else {
-            if (bid == 0)
-                for (int q = 0; q < R; q++)
-                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(mr.flag[q]) : "memory");
-            while ((int)(ld_acquire_u32(mr.flag[me]) - want) < 0) {
-            }
-        }
-        Acc<PREC> t[K];
-        const double *src = mr.slot[me] + (size_t)par * NB_MAX_RANKS * 4;
-        for (int q = 0; q < R; q++) {
 #pragma unroll
-            for (int k = 0; k < K; k++) t[k].merge(q == me ? s[k] : Acc<PREC>::load(src + (size_t)q * 4 + k * W));
+            for (int k = 0; k < K; k++) bc[k] = t[k].value();
         }
-#pragma unroll
-        for (int k = 0; k < K; k++) bc[k] = t[k].value();
     }
     __syncthreads();
 #pragma unroll
@@ -886,7 +893,7 @@ k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
 #pragma unroll 1
     for (int64_t gr = g0; gr < g1; gr++) {
         const int e = (int)(gr * C::EPB) + el;
-        const bool active = el < C::EPB && q < C::N2 && e < m.E;
+        const bool active = el < C::EPB && (C::N2P == C::N2 || q < C::N2) && e < m.E;
         // standalone operator (MODE 0): the handle may be a z-slab (global mask layers)
         acc += ax_group<PREC, N, MODE, MODE == 0>(m, D, in, pv, xv, g, w, apply_mask != 0, beta, alpha, e, active, a, b,
                                                   S0)

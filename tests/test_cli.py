@@ -33,8 +33,12 @@ def test_bad_order_is_1():
 
 
 @pytest.mark.gpu
-def test_per_copy_fp32_stagnation_is_2():
+def test_per_copy_fp32_failure_exit_codes():
+    """fp32 with the per-copy GS order fails (the paper's stagnation); which of the two failure
+    modes ends the run -- C-11 stagnation (exit 2) or the residual blowing up into a pap <= 0
+    breakdown (exit 3) -- depends on rounding order.  The exit code must match the status."""
     r = run("solve", "--nel", "8", "8", "8", "--p", "7", "--policy", "fp32", "--gs-order", "per_copy",
             "--max-iter", "1200")
-    assert r.returncode == 2, r.stdout
-    assert json.loads(r.stdout)["status"] == "stagnated"
+    st = json.loads(r.stdout)["status"]
+    assert (r.returncode, st) in ((2, "stagnated"), (3, "breakdown")), r.stdout
+    assert json.loads(r.stdout)["rel_res_min"] > 1e-8
