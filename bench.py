@@ -209,10 +209,28 @@ def run_reference(args):
 
 # ---------------------------------------------------------------------------- GPU arm
 def time_launches(fn, n, stream):
-    """Average device time (ms) of fn() over n back-to-back launches, CUDA events on `stream`."""
+    """Average device time (ms) of one fn() launch: n launches captured in a CUDA graph and
+    replayed between CUDA events (the per-call host work of the ctypes binding -- argument checks,
+    pointer queries -- would otherwise leave the GPU idle between these ~20 us kernels).  Falls
+    back to back-to-back direct launches if the capture fails."""
     import torch
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     fn()
+    torch.cuda.synchronize()
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(n):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        a.record(stream)
+        g.replay()
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b) / n
+    except Exception:
+        torch.cuda.synchronize()
     a.record(stream)
     for _ in range(n):
         fn()

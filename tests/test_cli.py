@@ -42,3 +42,20 @@ def test_per_copy_fp32_failure_exit_codes():
     st = json.loads(r.stdout)["status"]
     assert (r.returncode, st) in ((2, "stagnated"), (3, "breakdown")), r.stdout
     assert json.loads(r.stdout)["rel_res_min"] > 1e-8
+
+
+@pytest.mark.gpu
+def test_variants_and_slabs_from_cli():
+    r = run("solve", "--nel", "6", "6", "6", "--p", "5", "--policy", "mixed", "--precond", "identity", "--x64",
+            "--slabs", "3")
+    assert r.returncode == 0, r.stderr
+    out = json.loads(r.stdout)
+    assert out["status"] == "converged" and out["slabs"] == 3 and out["precond"] == "identity"
+    r1 = run("solve", "--nel", "6", "6", "6", "--p", "5", "--policy", "mixed", "--precond", "identity")
+    assert abs(json.loads(r1.stdout)["iterations"] - out["iterations"]) <= 2
+
+
+@pytest.mark.gpu
+def test_slabs_need_consistent_order():
+    r = run("solve", "--nel", "4", "4", "4", "--slabs", "2", "--gs-order", "per_copy")
+    assert r.returncode == 1
