@@ -480,6 +480,22 @@ static bool env_no_tma()
     return v == 1;
 }
 
+// Shared-memory carve-out: just what the resident blocks need, the rest of the 256 KB stays L1
+// (phase B's neighbour-copy loads hit in L1).  NB_CARVEOUT=0 leaves the driver's choice.
+static void set_carveout(const void *fn, int occ, int smem)
+{
+    static int mode = -1;
+    if (mode < 0) {
+        const char *s = std::getenv("NB_CARVEOUT");
+        mode = (s && s[0] == '0') ? 0 : 1;
+    }
+    if (!mode) return;
+    const int need = occ * (smem + 1024) + 1024;                   // + per-block reservation
+    int pct = (int)((100LL * need + 228 * 1024 - 1) / (228 * 1024));
+    if (pct > 100) pct = 100;
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 template <int PREC, int N, int FUSED, bool TMA, int VAR>
 static int mega_grid_t(const nb_handle *h)
 {
@@ -490,6 +506,7 @@ static int mega_grid_t(const nb_handle *h)
         int o = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, Sel::fn(), Sel::nt(), Sel::smem());
         occ = o > 0 ? o : 1;
+        set_carveout(Sel::fn(), occ, Sel::smem());
     }
     return h->sm_count * occ;
 }
