@@ -127,6 +127,8 @@ size_t vsize(int prec) { return prec == NB_FP64 ? sizeof(double) : sizeof(float)
 
 int ensure_f32(nb_handle *h)
 {
+    // one-time casts (first single-precision call only; no synchronisation afterwards)
+    if (h->g32 && h->dinv32) return NB_OK;
     if (!h->g32) {
         NB_CU(cudaMalloc(&h->g32, sizeof(float) * 6 * h->NL), "cudaMalloc g32");
         NB_CU(nb::launch_cast(h->g64, h->g32, 6 * h->NL, 0), "cast g");
