@@ -720,9 +720,30 @@ __device__ __forceinline__ void all_blocks_reduce_acc(const double *part, int G,
     using TS = typename Pol<PREC>::TS;
     __shared__ TS bc[K];
     Acc<PREC> s[K];
-    for (int i = threadIdx.x; i < G; i += blockDim.x) {
+    // 16-byte loads (L2): one block's K*W doubles per thread, or two blocks' single values
+    constexpr int W = Acc<PREC>::W, KW = K * W;
+    if constexpr (KW % 2 == 0) {
+        for (int i = threadIdx.x; i < G; i += blockDim.x) {
+            double d[KW];
 #pragma unroll
-        for (int k = 0; k < K; k++) s[k].merge(Acc<PREC>::load(part + ((size_t)i * K + k) * Acc<PREC>::W));
+            for (int j = 0; j < KW / 2; j++) {
+                const double2 t = __ldcg(reinterpret_cast<const double2 *>(part + (size_t)i * KW) + j);
+                d[2 * j] = t.x;
+                d[2 * j + 1] = t.y;
+            }
+#pragma unroll
+            for (int k = 0; k < K; k++) s[k].merge(Acc<PREC>::from(d + k * W));
+        }
+    } else {
+        for (int i2 = threadIdx.x; 2 * i2 < G; i2 += blockDim.x) {
+            if (2 * i2 + 1 < G) {
+                const double2 t = __ldcg(reinterpret_cast<const double2 *>(part) + i2);
+                s[0].merge(Acc<PREC>::from(&t.x));
+                s[0].merge(Acc<PREC>::from(&t.y));
+            } else {
+                s[0].merge(Acc<PREC>::load(part + 2 * (size_t)i2));
+            }
+        }
     }
     block_reduce_acc<PREC, K>(s, sh);   // caller: sh free (a __syncthreads since its last use)
     if (threadIdx.x == 0) {

@@ -41,6 +41,12 @@ template <int PREC> struct Acc {
         return r;
     }
     __device__ __forceinline__ void store(double *d) const { d[0] = (double)v; }
+    __device__ __forceinline__ static Acc from(const double *s)
+    {
+        Acc r;
+        r.v = (TS)s[0];
+        return r;
+    }
     __device__ __forceinline__ static Acc load(const double *s)
     {
         Acc r;
@@ -89,6 +95,13 @@ template <> struct Acc<NB_FP32_DOT2> {
         return r;
     }
     __device__ __forceinline__ void store(double *d) const { d[0] = (double)p; d[1] = (double)s; }
+    __device__ __forceinline__ static Acc from(const double *src)
+    {
+        Acc r;
+        r.p = (float)src[0];
+        r.s = (float)src[1];
+        return r;
+    }
     __device__ __forceinline__ static Acc load(const double *src)
     {
         Acc r;
