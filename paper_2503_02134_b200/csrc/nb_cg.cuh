@@ -93,7 +93,14 @@ template <typename T, int N> struct AxCfg {
 #ifndef NB_MINB_MODE
 #define NB_MINB_MODE 3
 #endif
-    static constexpr int MINB = NB_MINB_MODE == 0 ? 1
+// p = 11 in single precision: 3 resident blocks of 160 threads (128 registers, a few spills)
+// instead of 2 -- phase B gains from the extra warps (fp32 32^3: 829 -> 795 us/iteration;
+// mixed neutral to -3%)
+#ifndef NB_MINB_N12
+#define NB_MINB_N12 3
+#endif
+    static constexpr int MINB = (NB_MINB_N12 && N == 12 && sizeof(T) == 4) ? NB_MINB_N12
+                              : NB_MINB_MODE == 0 ? 1
                               : NB_MINB_MODE == 3 ? ((sizeof(T) == 4) ? (NT <= 128 ? 4 : 2) : (N <= 8 ? 1 : 2))
                               : NB_MINB_MODE == 1 ? ((sizeof(T) == 4) ? ((NT <= 128) ? 8 : (NT <= 256 ? 4 : 2)) : ((NT <= 128) ? 4 : 2))
                                                   : ((sizeof(T) == 4) ? ((NT <= 128) ? 6 : (NT <= 256 ? 3 : 1)) : 1);
