@@ -18,7 +18,7 @@ LIB = os.environ.get("NB_LIBPATH") or os.path.join(PKG, "libnb.so")
 UNITS = ("nb_api.cu", "nb_setup_k.cu", "nb_gs.cu", "nb_cg_fp64.cu", "nb_cg_fp32.cu", "nb_cg_mixed.cu",
          "nb_cg_dot2.cu", "nb_cg_fp64_var.cu", "nb_cg_fp32_var.cu", "nb_cg_mixed_var.cu", "nb_cg_dot2_var.cu")
 SOURCES = [os.path.join(CSRC, f) for f in UNITS]
-HEADERS = [os.path.join(CSRC, f) for f in ("nb_internal.h", "nb_common.cuh", "nb_cg.cuh", "nb_mega_body.inc", "nb_gs.cuh", "nb_tma.cuh", "nb_mega_tma.cuh")] + [
+HEADERS = [os.path.join(CSRC, f) for f in ("nb_internal.h", "nb_common.cuh", "nb_cg.cuh", "nb_mega_body.inc", "nb_gs.cuh", "nb_mega_launch.cuh")] + [
     os.path.join(ROOT, "include", "nb.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -169,7 +169,7 @@ int ensure_ws(nb_handle *h, int prec, int32_t max_iter)
         const int nchunk = (maxblk + 255) / 256;
         ws.mega_G = NB_POL(prec, nb::grid_mega, h);
         // megakernel partials: 4 accumulators per block (pap, shared pap, rtr, rho), 2 doubles
-        // each for the Dot2 expansions (nb_mega_tma.cuh: launch_cg_mega)
+        // each for the Dot2 expansions (nb_mega_launch.cuh: launch_cg_mega)
         const int mslots = (prec == NB_FP32_DOT2 ? 8 : 4) * ws.mega_G;
         const int nslots = 2 * maxblk > mslots ? 2 * maxblk : mslots;
         NB_CU(cudaMalloc(&ws.red.part, sizeof(double) * nslots), "cudaMalloc part");

@@ -1,6 +1,6 @@
 // nb_cg_fp64.cu -- instantiates the Ax / CG kernels of nb_cg.cuh for the fp64 policy
 // (one translation unit per policy so the build compiles them in parallel).
-#include "nb_mega_tma.cuh"
+#include "nb_mega_launch.cuh"
 
 namespace nb {
 NB_INSTANTIATE_CG(NB_FP64)

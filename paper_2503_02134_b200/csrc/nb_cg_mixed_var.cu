@@ -1,6 +1,6 @@
 // nb_cg_mixed_var.cu -- the mixed policy's megakernels for the preconditioner / x_fp64 variants
 // (VAR = 1), in their own translation unit so the build runs in parallel.
-#include "nb_mega_tma.cuh"
+#include "nb_mega_launch.cuh"
 
 namespace nb {
 NB_INSTANTIATE_CG_VAR(NB_MIXED)

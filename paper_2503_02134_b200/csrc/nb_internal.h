@@ -197,7 +197,7 @@ template <int PREC> int grid_mega(const nb_handle *h);
 struct MegaArgs;
 struct MultiArgs;
 template <int PREC, int VAR> int grid_mega_var(const nb_handle *h);
-// multi-rank (z-slab) solves: args of one slab, grid of one GPU, the launch (nb_mega_tma.cuh)
+// multi-rank (z-slab) solves: args of one slab, grid of one GPU, the launch (nb_mega_launch.cuh)
 template <int PREC>
 void fill_mega_args(const nb_handle *h, Workspace &ws, const void *b, int order, int max_iter, double rtol,
                     int precond, int x64, unsigned long long *tim, MegaArgs &A);

@@ -1,0 +1,160 @@
+// nb_mega_launch.cuh -- host launchers of the CG megakernels (nb_cg.cuh): occupancy-sized
+// persistent grids (every block resident: cooperative launches), the shared-memory carve-out,
+// the kernel arguments of one slab or whole box, and the multi-rank (z-slab) launch.
+// Included by the per-policy translation units (nb_cg_<policy>[_var].cu).
+// (A variant that staged every phase operand through 1-D TMA bulk copies and an mbarrier ring
+// measured slower on B200 and was removed.)
+#pragma once
+#include "nb_cg.cuh"
+
+#include <cstdlib>
+
+namespace nb {
+
+// Shared-memory carve-out: just what the resident blocks need, the rest of the 256 KB stays L1
+// (phase B's neighbour-copy loads hit in L1).  NB_CARVEOUT=0 leaves the driver's choice.
+static void set_carveout(const void *fn, int occ, int smem)
+{
+    static int mode = -1;
+    if (mode < 0) {
+        const char *s = std::getenv("NB_CARVEOUT");
+        mode = (s && s[0] == '0') ? 0 : 1;
+    }
+    if (!mode) return;
+    const int need = occ * (smem + 1024) + 1024;                   // + per-block reservation
+    int pct = (int)((100LL * need + 228 * 1024 - 1) / (228 * 1024));
+    if (pct > 100) pct = 100;
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
+template <int PREC, int N, int FUSED, int VAR>
+static int mega_grid_t(const nb_handle *h)
+{
+    using C = AxCfg<typename Pol<PREC>::TV, N>;
+    const void *fn = (const void *)k_cg_mega<PREC, N, FUSED, VAR>;
+    static int occ = -1;
+    if (occ < 0) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, C::NT, C::SMEM);
+        occ = o > 0 ? o : 1;
+        set_carveout(fn, occ, C::SMEM);
+    }
+    return h->sm_count * occ;
+}
+
+template <int PREC, int VAR>
+int grid_mega_var(const nb_handle *h)
+{
+    NB_DISPATCH_N(h->n, return (mega_grid_t<PREC, NN, 1, VAR>(h) > mega_grid_t<PREC, NN, 0, VAR>(h)
+                                    ? mega_grid_t<PREC, NN, 1, VAR>(h)
+                                    : mega_grid_t<PREC, NN, 0, VAR>(h)))
+}
+
+// grid size of every megakernel of the policy (sizes the per-block partials)
+template <int PREC>
+int grid_mega(const nb_handle *h)
+{
+    const int g0 = grid_mega_var<PREC, 0>(h), g1 = grid_mega_var<PREC, 1>(h);
+    return g0 > g1 ? g0 : g1;
+}
+
+template <int PREC, int N, int FUSED, int VAR>
+static cudaError_t mega_launch_t(const nb_handle *h, const MegaArgs &args, cudaStream_t st)
+{
+    using TV = typename Pol<PREC>::TV;
+    using C = AxCfg<TV, N>;
+    DMat<TV, N> D = make_dmat<TV, N>(h->D);
+    void *params[2] = {(void *)&args, (void *)&D};
+    const int grid = mega_grid_t<PREC, N, FUSED, VAR>(h);
+    return cudaLaunchCooperativeKernel((const void *)k_cg_mega<PREC, N, FUSED, VAR>, dim3(grid), dim3(C::NT), params,
+                                       (size_t)C::SMEM, st);
+}
+
+template <int PREC, int VAR>
+cudaError_t launch_cg_mega_var(const nb_handle *h, const MegaArgs &A, bool fused, cudaStream_t st)
+{
+    if (fused) { NB_DISPATCH_N(h->n, return (mega_launch_t<PREC, NN, 1, VAR>(h, A, st))) }
+    NB_DISPATCH_N(h->n, return (mega_launch_t<PREC, NN, 0, VAR>(h, A, st)))
+}
+
+template <int PREC>
+void fill_mega_args(const nb_handle *h, Workspace &ws, const void *b, int order, int max_iter, double rtol, int precond,
+                    int x64, unsigned long long *tim, MegaArgs &A)
+{
+    A.m = h->md();
+    A.b = b;
+    A.pc = precond;
+    A.x64 = (PREC == NB_MIXED && x64) ? 1 : 0;
+    A.x = A.x64 ? (void *)ws.xd : ws.x; A.p = ws.p; A.r = ws.r; A.w = ws.w;
+    A.z = precond == NB_PC_IDENTITY ? ws.r : ws.z;   // identity: z aliases r (never stored)
+    A.g = (sizeof(typename Pol<PREC>::TV) == 8) ? (const void *)h->g64 : (const void *)h->g32;
+    A.dinv = (sizeof(typename Pol<PREC>::TJ) == 4 || precond == NB_PC_JACOBI_F32) ? (const void *)h->dinv32
+                                                                                  : (const void *)h->dinv64;
+    A.gs_off = h->gs_off; A.gs_idx = h->gs_idx; A.nseg = (int32_t)h->nseg;
+    A.order = order; A.max_iter = max_iter; A.rtol = rtol;
+    A.hist = ws.hist; A.tim = tim;
+    // per-block partials: W doubles per accumulator (2 for the Dot2 expansions)
+    const size_t W = (size_t)Acc<PREC>::W;
+    A.partA = ws.red.part; A.partS = ws.red.part + W * ws.mega_G; A.partB = ws.red.part + 2 * W * ws.mega_G;
+    A.bar = ws.bar;
+    A.scal = ws.scal;
+    A.wlo = ws.peer.wlo;
+    A.whi = ws.peer.whi;
+}
+
+template <int PREC>
+cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int order, int max_iter, double rtol,
+                           int precond, int x64, unsigned long long *tim, cudaStream_t st)
+{
+    MegaArgs A;
+    fill_mega_args<PREC>(h, ws, b, order, max_iter, rtol, precond, x64, tim, A);
+    A.wlo = A.whi = nullptr;
+    const bool fused = order == NB_GS_CONSISTENT && !h->cg_csr;
+    cudaError_t e = cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned int), st);   // barrier epoch 0
+    if (e != cudaSuccess) return e;
+    const bool var = precond != NB_PC_JACOBI || A.x64;
+    return var ? launch_cg_mega_var<PREC, 1>(h, A, fused, st) : launch_cg_mega_var<PREC, 0>(h, A, fused, st);
+}
+
+// ---- multi-rank (z-slab) megakernel: consistent order, runtime options ----
+template <int PREC, int N>
+static int mr_occupancy()
+{
+    using C = AxCfg<typename Pol<PREC>::TV, N>;
+    static int occ = -1;
+    if (occ < 0) {
+        const void *fn = (const void *)k_cg_mega_mr<PREC, N>;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, C::NT, C::SMEM);
+        occ = o > 0 ? o : 1;
+    }
+    return occ;
+}
+
+template <int PREC>
+int grid_mega_mr(const nb_handle *h)
+{
+    NB_DISPATCH_N(h->n, return (h->sm_count * mr_occupancy<PREC, NN>()))
+}
+
+template <int PREC, int N>
+static cudaError_t mr_launch_t(const nb_handle *h, const MultiArgs &M, cudaStream_t st)
+{
+    using TV = typename Pol<PREC>::TV;
+    using C = AxCfg<TV, N>;
+    DMat<TV, N> D = make_dmat<TV, N>(h->D);
+    void *params[2] = {(void *)&M, (void *)&D};
+    (void)mr_occupancy<PREC, N>();
+    return cudaLaunchCooperativeKernel((const void *)k_cg_mega_mr<PREC, N>, dim3(M.mr.nloc * M.mr.Gr), dim3(C::NT),
+                                       params, (size_t)C::SMEM, st);
+}
+
+template <int PREC>
+cudaError_t launch_cg_mr(const nb_handle *h0, const MultiArgs &M, cudaStream_t st)
+{
+    NB_DISPATCH_N(h0->n, return (mr_launch_t<PREC, NN>(h0, M, st)))
+}
+
+}  // namespace nb
