@@ -105,3 +105,19 @@ def test_dot2_rejected_by_graph_driver():
     with pytest.raises(nb.NbError):
         g.cg(b, nb.NB_FP32_DOT2, max_iter=10)
     g.close()
+
+
+@pytest.mark.parametrize("nel,p", [((5, 4, 4), 1), ((3, 2, 2), 3), ((2, 3, 2), 5), ((2, 2, 3), 9), ((2, 2, 1), 15)])
+def test_dot2_every_order_vs_oracle(nel, p):
+    """20 fixed iterations of the fp32 + Dot2 policy on every polynomial order: x within fp32
+    round-off of the oracle's sequential-Dot2 run."""
+    g = nb.Mesh(*nel, p, deform=0.1, seed=3)
+    o = oracle.Mesh(*nel, p, deform=0.1, seed=3)
+    xo, ho, _ = o.cg(o.rhs(seed=2), oracle.FP32_DOT2, max_iter=20, rtol=0.0)
+    x, r = g.cg(g.rhs(nb.NB_FP32_DOT2, seed=2), nb.NB_FP32_DOT2, max_iter=20, rtol=0.0)
+    err = np.max(np.abs(x.cpu().numpy().astype(np.float64) - xo)) / np.max(np.abs(xo))
+    assert err <= 2e-5, err
+    k = min(len(r.history), len(ho))
+    assert k == len(ho) == 21
+    assert np.max(np.abs(np.log10(r.history[1:k]) - np.log10(ho[1:k]))) <= 0.1
+    g.close()

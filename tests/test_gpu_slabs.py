@@ -207,3 +207,21 @@ def test_slab_operator_matches_box():
         off += nl
         m.close()
     box.close()
+
+
+@pytest.mark.parametrize("nel,p,R", [((2, 2, 3), 1, 3), ((3, 2, 4), 3, 2), ((2, 3, 5), 5, 4), ((2, 2, 2), 11, 2),
+                                     ((2, 1, 3), 15, 3), ((3, 3, 7), 2, 3)])
+def test_group_every_order_matches_single(nel, p, R):
+    """Every polynomial order / slab count: 20 fixed fp64 iterations of the slab solve equal the
+    whole-box solve to round-off (the multi-rank kernel for N = 2..16)."""
+    g = nb.Mesh(*nel, p, deform=0.1, seed=2)
+    b = g.rhs(nb.NB_FP64, seed=1)
+    x1, r1 = g.cg(b, nb.NB_FP64, max_iter=20, rtol=0.0)
+    ms = [nb.Mesh(*nel, p, deform=0.1, seed=2, slab=nb.slab_bounds(nel[2], R, r)) for r in range(R)]
+    xs, rs = nb.cg_group(ms, [m.rhs(nb.NB_FP64, seed=1) for m in ms], nb.NB_FP64, max_iter=20, rtol=0.0)
+    x = torch.cat(xs)
+    scale = float(torch.max(torch.abs(x1)))
+    assert float(torch.max(torch.abs(x - x1))) <= 1e-11 * scale
+    assert np.max(np.abs(rs[0].history - r1.history)) <= 1e-11
+    close_all(ms)
+    g.close()
