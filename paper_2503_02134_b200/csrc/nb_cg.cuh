@@ -1,6 +1,7 @@
-// nb_cg.cuh -- the per-iteration work of the Jacobi-PCG hot path (templates; one
-// translation unit per precision policy instantiates them: nb_cg_fp64.cu, nb_cg_fp32.cu,
-// nb_cg_mixed.cu).
+// nb_cg.cuh -- the per-iteration work of the Jacobi-PCG hot path (templates; the translation
+// units nb_cg_<policy>.cu (default options) and nb_cg_<policy>_var.cu (preconditioner / x_fp64
+// variants and the multi-rank kernel) instantiate them per precision policy: fp64, fp32,
+// mixed, fp32_dot2).
 //
 // One CG iteration (Table 2 of the paper) is two phases in consistent
 // gather-scatter order:
@@ -33,7 +34,9 @@
 //     element range; grid-wide barriers separate the phases; after each barrier every block
 //     reduces the per-block partials itself, in the same fixed order, so all blocks take the
 //     same (bit-identical) scalar decisions -- no host round trip, no launch gaps, no serial
-//     last-block tail.  (Default.)
+//     last-block tail.  (Default.)  k_cg_mega_mr is the same body for z-slabs of a box spread
+//     over ranks (GPUs, or slabs sharing one launch): the gather reads the neighbour slab's w,
+//     the reductions add a per-rank push/flag step (mr_reduce).  Body: nb_mega_body.inc.
 //   * k_ax / k_upd: one persistent kernel per phase, chained in a CUDA graph with a
 //     conditional WHILE node; scalars finalised by the last block (NB_CG_DRIVER=graph).
 #pragma once
