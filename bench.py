@@ -181,6 +181,68 @@ def oracle_sample(iters: int, policy: str = "mixed"):
     return m.n_local * rep.iterations / dt, dt, t_setup, rep.iterations, m.n_local
 
 
+def run_oracle_timing(args):
+    """--oracle-timing: SURVEY.md §8(d) "Oracle timing" on this box's host (one core, the plain C
+    oracle as it stands): per config setup, one Ax, one dssum and the CG rate; full solves for
+    configs[0..1]; configs[2..3] from 5 iterations, extrapolated to the GPU's iteration count
+    measured in the same run (labelled as such).  Prints one JSON document."""
+    import platform
+
+    import oracle
+    import paper_2503_02134_b200 as nb
+    cases = [("configs[0]", (2, 2, 2), 7, 0.0, 0, 0.0, ["fp64"], True, 100),
+             ("configs[1]", (16, 16, 16), 7, 0.0, 0, 1e-8, ["fp64", "fp32", "mixed"], True, 4000),
+             ("configs[2]", (32, 32, 32), 9, 0.1, 0, 1e-8, ["mixed", "fp64"], False, 8000),
+             ("configs[3]", (64, 32, 32), 11, 0.0, 1, 1e-10, ["fp64", "mixed"], False, 8000)]
+    opol = {"fp64": oracle.FP64, "fp32": oracle.FP32, "mixed": oracle.MIXED}
+    model = ""
+    try:
+        txt = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        model = next((ln.split(":", 1)[1].strip() for ln in txt.splitlines() if ln.startswith("Model name")), "")
+    except Exception:
+        pass
+    out = {"host": {"cpu_model": model or platform.processor(), "nproc": os.cpu_count(), "threads_used": 1,
+                    "oracle_cflags": " ".join(oracle.CFLAGS)}, "cases": []}
+    for name, nel, p, d, kind, rtol, pols, full, max_iter in cases:
+        if args.oracle_max_dof and nel[0] * nel[1] * nel[2] * (p + 1) ** 3 > args.oracle_max_dof:
+            continue
+        t0 = time.perf_counter()
+        m = oracle.Mesh(*nel, p, deform=d, seed=0)
+        rec = {"config": name, "nel": nel, "p": p, "deform": d, "n_local": m.n_local,
+               "setup_s": time.perf_counter() - t0}
+        b = m.rhs(oracle.RHS_UNIFORM if kind == 0 else oracle.RHS_MANUFACTURED, noise=1e-3, seed=0)
+        for pol in pols:
+            t0 = time.perf_counter()
+            m.ax(b, opol[pol])
+            rec[f"ax_s_{pol}"] = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            m.dssum(b, opol[pol])
+            rec[f"dssum_s_{pol}"] = time.perf_counter() - t0
+            if full:
+                t0 = time.perf_counter()
+                _, _, r = m.cg(b, opol[pol], max_iter=max_iter, rtol=rtol)
+                dt = time.perf_counter() - t0
+                rec[f"solve_{pol}"] = {"iterations": r.iterations, "status": r.status, "seconds": dt,
+                                       "dof_iter_per_s": m.n_local * r.iterations / dt}
+            else:
+                g = nb.Mesh(*nel, p, deform=d, seed=0)
+                gb = g.rhs(POLICIES[pol], nb.NB_RHS_UNIFORM if kind == 0 else nb.NB_RHS_MANUFACTURED, noise=1e-3, seed=0)
+                _, gr = g.cg(gb, POLICIES[pol], max_iter=max_iter, rtol=rtol)
+                g.close()
+                t0 = time.perf_counter()
+                m.cg(b, opol[pol], max_iter=5, rtol=0.0)
+                dt = (time.perf_counter() - t0) / 5
+                rec[f"solve_{pol}"] = {"seconds_per_iteration": dt, "dof_iter_per_s": m.n_local / dt,
+                                       "gpu_iterations": gr.iterations, "gpu_solve_ms": gr.solve_ms,
+                                       "extrapolated_seconds_to_rtol": dt * gr.iterations,
+                                       "note": "extrapolated: 5 oracle iterations x the GPU's iteration count"}
+            print(json.dumps({"progress": name, "policy": pol}), file=sys.stderr, flush=True)
+        out["cases"].append(rec)
+        del m
+    print(json.dumps(out, indent=1), flush=True)
+    return 0
+
+
 def run_reference(args):
     rank, world, _ = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0
     if rank != 0:
@@ -451,7 +513,12 @@ def main():
     ap.add_argument("--mode", default="replicas", choices=["replicas", "slab"],
                     help="N>1: independent replicas, or one box split in z-slabs over the GPUs")
     ap.add_argument("--slabs", type=int, default=2, help="--mode slab on one GPU: slabs in the launch")
+    ap.add_argument("--oracle-timing", action="store_true",
+                    help="instead of the bench line: time the CPU oracle per config (SURVEY §8(d))")
+    ap.add_argument("--oracle-max-dof", type=float, default=0, help="--oracle-timing: skip larger configs")
     args = ap.parse_args()
+    if args.oracle_timing:
+        return run_oracle_timing(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

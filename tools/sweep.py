@@ -37,8 +37,6 @@ def main():
     ap.add_argument("--iters", type=int, default=200)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--standalone", action="store_true", help="also time nb_ax (local) and nb_dssum")
-    ap.add_argument("--oracle-max-dof", type=float, default=0, help="time the CPU oracle (5 iterations) "
-                    "on points with at most this many local DOF")
     ap.add_argument("--configs4", action="store_true", help="BASELINE configs[4]: cubes 10..50, p 7/9/11, "
                     "undeformed and deformed")
     a = ap.parse_args()
@@ -86,14 +84,6 @@ def main():
                         m.info.n_shared_copies * (2 * SV[pol] + 4) + (m.info.n_shared_global + 1) * 4
                     extra[what + "_us"] = us
                     extra[what + "_GBps"] = byts / (us * 1e-6) / 1e9
-            if a.oracle_max_dof and NL <= a.oracle_max_dof:
-                import time
-                import oracle
-                o = oracle.Mesh(*nel, p, deform=d)
-                bo = o.rhs(seed=0)
-                t0 = time.perf_counter()
-                o.cg(bo, {"fp64": oracle.FP64, "fp32": oracle.FP32, "mixed": oracle.MIXED, "fp32_dot2": oracle.FP32_DOT2}[name], max_iter=5, rtol=0.0)
-                extra["oracle_dof_iter_per_s"] = NL * 5 / (time.perf_counter() - t0)
             print(json.dumps({**extra, "case": c, "policy": name, "n_local": NL, "iters": it, "solve_ms": best.solve_ms,
                               "dof_iter_per_s": NL * it / (best.solve_ms * 1e-3),
                               "us_per_iter": 1e3 * best.solve_ms / it, "phaseA_us": k1, "phaseS_us": kg,
