@@ -147,7 +147,9 @@ int ensure_f32(nb_handle *h)
      : (prec) == NB_FP32 ? F<NB_FP32>(__VA_ARGS__)                                                 \
      : (prec) == NB_MIXED ? F<NB_MIXED>(__VA_ARGS__) : F<NB_FP32_DOT2>(__VA_ARGS__))
 
-int ensure_ws(nb_handle *h, int prec, int32_t max_iter)
+void free_ws(nb::Workspace &ws);
+
+static int alloc_ws(nb_handle *h, int prec, int32_t max_iter)
 {
     nb::Workspace &ws = h->ws[prec];
     if (!ws.ctl) {
@@ -200,6 +202,19 @@ int ensure_ws(nb_handle *h, int prec, int32_t max_iter)
         }
     }
     return NB_OK;
+}
+
+// The policy's CG workspace, allocated on first use; a failed allocation releases everything
+// allocated so far (the next call starts clean).
+int ensure_ws(nb_handle *h, int prec, int32_t max_iter)
+{
+    const int rc = alloc_ws(h, prec, max_iter);
+    if (rc != NB_OK) {
+        const std::string msg = g_err;   // keep the failing call's message
+        free_ws(h->ws[prec]);
+        g_err = msg;
+    }
+    return rc;
 }
 
 void free_ws(nb::Workspace &ws)
@@ -511,6 +526,25 @@ int nb_dssum(nb_handle *h, nb_policy prec, nb_gs_order order, void *u, void *str
     return NB_OK;
 }
 
+// CUDA events released on every return path
+struct EventSet {
+    std::vector<cudaEvent_t> ev;
+    cudaError_t create(size_t n)
+    {
+        ev.assign(n, nullptr);
+        for (auto &e : ev) {
+            const cudaError_t r = cudaEventCreate(&e);
+            if (r != cudaSuccess) return r;
+        }
+        return cudaSuccess;
+    }
+    ~EventSet()
+    {
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
 // One solve over nh handles: nh = 1 -> the handle's own solve (whole box, or one slab of a
 // multi-rank solve when nb_peer_attach'ed); nh > 1 -> slabs of one box sharing this GPU, one
 // cooperative launch (nb_cg_group).  b, x: per handle.
@@ -533,9 +567,9 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
     const bool mega = !h0->cg_graph;
     if (!multi && !mega && !o->time_kernels && (rc = build_graph(h0, prec, order))) return rc;
 
-    cudaEvent_t t0, t1;
-    NB_CU(cudaEventCreate(&t0), "event");
-    NB_CU(cudaEventCreate(&t1), "event");
+    EventSet tev;
+    NB_CU(tev.create(2), "event");
+    cudaEvent_t t0 = tev.ev[0], t1 = tev.ev[1];
     nb::Scal s0;
     memset(&s0, 0, sizeof(s0));
     s0.rtol = o->rtol;
@@ -603,10 +637,10 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
             NB_CU(cudaGraphLaunch(ws0.exec[order], st), "graph launch");
         } else {
             // per-kernel CUDA-event timing: direct launches, check the done flag every 16 iterations
-            std::vector<cudaEvent_t> ev;
             const int chunk = 16;
-            ev.resize(4 * chunk);
-            for (auto &e : ev) NB_CU(cudaEventCreate(&e), "event");
+            EventSet evs;
+            NB_CU(evs.create(4 * chunk), "event");
+            std::vector<cudaEvent_t> &ev = evs.ev;
             int k = 0;
             bool done = false;
             while (!done && k < o->max_iter) {
@@ -631,7 +665,6 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
                 k += m;
                 done = ws0.scal_host->done != 0;
             }
-            for (auto &e : ev) cudaEventDestroy(e);
             NB_CU(NB_POL(prec, nb::launch_cg_fin, h0, ws0, st), "cg fin");
         }
     }
@@ -647,8 +680,6 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
     NB_CU(cudaStreamSynchronize(st), "solve sync");
     float ms = 0.f;
     cudaEventElapsedTime(&ms, t0, t1);
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
     int ret = NB_OK;
     for (int r = 0; r < nh; r++) {
         nb_handle *h = hs[r];
