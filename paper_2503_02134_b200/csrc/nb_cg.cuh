@@ -80,10 +80,18 @@ template <typename T, int N> struct AxCfg {
 #ifndef NB_PAD_ELEM
 #define NB_PAD_ELEM 0
 #endif
-    static constexpr int N2P = (NB_PAD_ELEM && N == 10) ? 128 : N2;
+    // fp64, p = 7: two threads per r-pencil (ax_group_half), four arrays per element, 16 warps/SM.
+    // Parity-clean but off: at the 128-register cap of two blocks per SM the kernel spills 416 B
+    // (phase A 347 -> 411 us, phase B 176 -> 167 us at 32^3 p7).
+#ifndef NB_HALF64
+#define NB_HALF64 0
+#endif
+    static constexpr bool HALF = NB_HALF64 && sizeof(T) == 8 && N == 8;
+    static constexpr int N2P = HALF ? 2 * N2 : (NB_PAD_ELEM && N == 10) ? 128 : N2;
+    static constexpr int NARR = HALF ? 4 : 3;
     static constexpr int EPB = (N2P >= 256) ? 1 : (256 / N2P);  // elements per group
     static constexpr int NT = ((EPB * N2P + 31) / 32) * 32;     // threads per block
-    static constexpr int SMEM = 3 * EPB * ESZ * (int)sizeof(T);
+    static constexpr int SMEM = NARR * EPB * ESZ * (int)sizeof(T);
     // resident blocks per SM the register allocation must allow (launch bound); fp64 pencils
     // need twice the registers
 // Phase-B loads of w (own pencil, neighbour copies): w was written by other blocks in phase A,
@@ -104,7 +112,7 @@ template <typename T, int N> struct AxCfg {
 #endif
     static constexpr int MINB = (NB_MINB_N12 && N == 12 && sizeof(T) == 4) ? NB_MINB_N12
                               : NB_MINB_MODE == 0 ? 1
-                              : NB_MINB_MODE == 3 ? ((sizeof(T) == 4) ? (NT <= 128 ? 4 : 2) : (N <= 8 ? 1 : 2))
+                              : NB_MINB_MODE == 3 ? ((sizeof(T) == 4) ? (NT <= 128 ? 4 : 2) : (N <= 8 && !HALF ? 1 : 2))
                               : NB_MINB_MODE == 1 ? ((sizeof(T) == 4) ? ((NT <= 128) ? 8 : (NT <= 256 ? 4 : 2)) : ((NT <= 128) ? 4 : 2))
                                                   : ((sizeof(T) == 4) ? ((NT <= 128) ? 6 : (NT <= 256 ? 3 : 1)) : 1);
 };
@@ -405,6 +413,178 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         }
         st_pencil<TV, N>(w + gbase, out);
     }
+    }
+    return acc;
+}
+
+// o[i'] = sum_l M[I0 + i'][l] v[l] for NO consecutive output rows starting at the compile-time row
+// I0 (M column-pair-adjacent as in contract_pairs): the partial contraction of a half pencil.
+template <typename T, int N, int I0, int NO>
+__device__ __forceinline__ void contract_rows(const T *__restrict__ mt, const T (&v)[N], T (&o)[NO])
+{
+#pragma unroll
+    for (int i = 0; i < NO; i++) {
+        T s = mt[I0 + i] * v[0];
+#pragma unroll
+        for (int l = 1; l < N; l++) s = fma(mt[l * N + I0 + i], v[l], s);
+        o[i] = s;
+    }
+}
+
+// ax_group with TWO threads per r-pencil (AxCfg::HALF, fp64): the element's 2 N^2 threads are
+// two warp-aligned halves -- half h owns nodes [h N/2, (h+1) N/2) of its pencil for the pointwise
+// work (operand, geometric factors, output) and does the s-contractions (h = 0) or the
+// t-contractions (h = 1) of its pencil index.  Half the pencil registers per thread lets fp64
+// run twice the warps per SM (16 instead of 8).  h is warp-uniform, so the row split of the
+// r-contractions keeps D in constant-bank operands without divergence.  Arrays: S0 = u, then
+// w_r^T; A1 = us, ws, then w_s^T; A2 = ut, wt, then w_t^T; A3 = wr.
+template <int PREC, int N, int MODE, bool SLAB = false>
+__device__ __forceinline__ Acc<PREC>
+ax_group_half(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typename Pol<PREC>::TV *__restrict__ in,
+              typename Pol<PREC>::TV *__restrict__ pv, typename Pol<PREC>::TV *__restrict__ xv,
+              const typename Pol<PREC>::TV *__restrict__ g, typename Pol<PREC>::TV *__restrict__ w, bool apply_mask,
+              typename Pol<PREC>::TV beta, typename Pol<PREC>::TV alpha, int e, bool active, int a, int b, int h,
+              typename Pol<PREC>::TV *__restrict__ S0)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TS = typename Pol<PREC>::TS;
+    using C = AxCfg<TV, N>;
+    constexpr int H = N / 2;
+    static_assert(N % 2 == 0 && (H * sizeof(TV)) % 16 == 0 || H % 2 == 0, "half pencils of whole 16-byte chunks");
+    TV *A1 = S0 + C::ESZ;
+    TV *A2 = A1 + C::ESZ;
+    TV *A3 = A2 + C::ESZ;
+    const int q = a + N * b;
+    const int i0 = h * H;
+    const int rp = C::R * a + C::P * b;
+    const int sp = a + C::P * b;
+    const int tp = C::TT ? b + C::R * a : a + C::R * b;
+    const size_t gbase = (size_t)e * C::N3 + (size_t)N * q + i0;
+    Acc<PREC> acc;
+
+    // ---- 1. operand half: u, or p = z + beta p_old with the deferred x update
+    if (active) {
+        TV u[H];
+        if (MODE == 0) {
+            ld_pencil<TV, H>(in + gbase, u);
+        } else {
+            TV zz[H], po[H], xx[H];
+            ld_pencil<TV, H, LD_CS>(in + gbase, zz);
+            ld_pencil<TV, H>(pv + gbase, po);
+            ld_pencil<TV, H, LD_CS>(xv + gbase, xx);
+#pragma unroll
+            for (int i = 0; i < H; i++) {
+                u[i] = fma(beta, po[i], zz[i]);      // add2s1
+                xx[i] = fma(alpha, po[i], xx[i]);    // add2s2(x, p_old, alpha_prev)
+            }
+            st_pencil<TV, H>(pv + gbase, u);
+            st_pencil<TV, H, LD_CS>(xv + gbase, xx);
+        }
+        st_pencil<TV, H>(S0 + rp + i0, u);
+    }
+    elem_sync<C::N2P, C::EPB>();
+    // ---- 2. us (h = 0) or ut (h = 1) of pencil index (a, b)
+    if (active) {
+        TV v[N], o[N];
+        if (h == 0) {
+#pragma unroll
+            for (int j = 0; j < N; j++) v[j] = S0[sp + C::R * j];
+            contract<TV, N>(D, v, o);
+#pragma unroll
+            for (int j = 0; j < N; j++) A1[sp + C::R * j] = o[j];
+        } else {
+#pragma unroll
+            for (int k = 0; k < N; k++) v[k] = S0[tp + C::P * k];
+            contract<TV, N>(D, v, o);
+#pragma unroll
+            for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
+        }
+    }
+    elem_sync<C::N2P, C::EPB>();
+    // ---- 3. ur of the owned rows from the full u pencil; geometric factors; wr -> A3, ws/wt in place
+    if (active) {
+        TV ur[H];
+        {
+            TV v[N];
+            ld_pencil<TV, N>(S0 + rp, v);
+            if (h == 0) contract_rows<TV, N, 0, H>(D.dt, v, ur);
+            else contract_rows<TV, N, H, H>(D.dt, v, ur);
+        }
+        const TV *ge = g + (size_t)e * 6 * C::N3 + (size_t)N * q + i0;
+        TV g1[H], g2[H], g3[H], g4[H], g5[H], g6[H], us[H], ut[H], wr[H], ws[H], wt[H];
+        ld_pencil<TV, H, LD_CS>(ge + 0 * C::N3, g1);
+        ld_pencil<TV, H, LD_CS>(ge + 1 * C::N3, g2);
+        ld_pencil<TV, H, LD_CS>(ge + 2 * C::N3, g3);
+        ld_pencil<TV, H, LD_CS>(ge + 3 * C::N3, g4);
+        ld_pencil<TV, H, LD_CS>(ge + 4 * C::N3, g5);
+        ld_pencil<TV, H, LD_CS>(ge + 5 * C::N3, g6);
+        ld_pencil<TV, H>(A1 + rp + i0, us);
+        ld_pencil<TV, H>(A2 + rp + i0, ut);
+#pragma unroll
+        for (int t = 0; t < H; t++) {
+            wr[t] = fma(g3[t], ut[t], fma(g2[t], us[t], g1[t] * ur[t]));
+            ws[t] = fma(g5[t], ut[t], fma(g4[t], us[t], g2[t] * ur[t]));
+            wt[t] = fma(g6[t], ut[t], fma(g5[t], us[t], g3[t] * ur[t]));
+            if (MODE == 1) acc.add_sum(((TS)ur[t] * (TS)wr[t] + (TS)us[t] * (TS)ws[t]) + (TS)ut[t] * (TS)wt[t]);
+        }
+        st_pencil<TV, H>(A3 + rp + i0, wr);
+        st_pencil<TV, H>(A1 + rp + i0, ws);
+        st_pencil<TV, H>(A2 + rp + i0, wt);
+    }
+    elem_sync<C::N2P, C::EPB>();
+    // ---- 3b. r-part of local_grad3_t for the owned rows (S0's u is no longer read);
+    // ---- 4. s- (h = 0) or t-part (h = 1) of local_grad3_t, in place
+    if (active) {
+        {
+            TV v[N], o[H];
+            ld_pencil<TV, N>(A3 + rp, v);
+            if (h == 0) contract_rows<TV, N, 0, H>(D.d, v, o);
+            else contract_rows<TV, N, H, H>(D.d, v, o);
+            st_pencil<TV, H>(S0 + rp + i0, o);
+        }
+        TV v[N], o[N];
+        if (h == 0) {
+#pragma unroll
+            for (int j = 0; j < N; j++) v[j] = A1[sp + C::R * j];
+            contract_t<TV, N>(D, v, o);
+#pragma unroll
+            for (int j = 0; j < N; j++) A1[sp + C::R * j] = o[j];
+        } else {
+#pragma unroll
+            for (int k = 0; k < N; k++) v[k] = A2[tp + C::P * k];
+            contract_t<TV, N>(D, v, o);
+#pragma unroll
+            for (int k = 0; k < N; k++) A2[tp + C::P * k] = o[k];
+        }
+    }
+    elem_sync<C::N2P, C::EPB>();
+    // ---- 5. w = (w_r + w_s) + w_t on the owned nodes, Dirichlet mask, store
+    if (active) {
+        TV out[H];
+        {
+            TV t0[H], t1[H], t2[H];
+            ld_pencil<TV, H>(S0 + rp + i0, t0);
+            ld_pencil<TV, H>(A1 + rp + i0, t1);
+            ld_pencil<TV, H>(A2 + rp + i0, t2);
+#pragma unroll
+            for (int i = 0; i < H; i++) out[i] = (t0[i] + t1[i]) + t2[i];
+        }
+        if (MODE != 0 || apply_mask) {
+            const ElemPos P = elem_pos<SLAB>(m, e);
+            const bool mjk = axis_bnd(a, N, P.ey, m.nely) || axis_bnd(b, N, P.ez, m.nelz);
+#pragma unroll
+            for (int i = 0; i < H; i++)
+                if (mjk || axis_bnd(i0 + i, N, P.ex, m.nelx)) out[i] = TV(0);
+            if (MODE == 2) {   // unshared nodes only (c = 1); the CSR phase adds the shared ones
+                const bool sjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz) > 1;
+                TV pp[H];
+                ld_pencil<TV, H>(pv + gbase, pp);   // written by this thread in step 1
+#pragma unroll
+                for (int i = 0; i < H; i++)
+                    if (!sjk && axis_mult(i0 + i, N, P.ex, m.nelx) == 1) acc.add((TS)out[i], (TS)pp[i]);
+            }
+        }
+        st_pencil<TV, H>(w + gbase, out);
     }
     return acc;
 }
@@ -911,8 +1091,10 @@ k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
     const int tid = threadIdx.x;
     const int el = tid / C::N2P;
     const int q = tid - el * C::N2P;
-    const int a = q % N, b = q / N;
-    TV *S0 = reinterpret_cast<TV *>(smraw) + (el < C::EPB ? el : 0) * 3 * C::ESZ;
+    const int qp = C::HALF ? q % C::N2 : q;   // pencil index (two threads per pencil: HALF)
+    const int h = C::HALF ? q / C::N2 : 0;
+    const int a = qp % N, b = qp / N;
+    TV *S0 = reinterpret_cast<TV *>(smraw) + (el < C::EPB ? el : 0) * C::NARR * C::ESZ;
     TV beta = 0, alpha = 0;
     if (MODE != 0) {
         beta = (TV)(TS)scal->beta;
@@ -924,11 +1106,16 @@ k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
 #pragma unroll 1
     for (int64_t gr = g0; gr < g1; gr++) {
         const int e = (int)(gr * C::EPB) + el;
-        const bool active = el < C::EPB && (C::N2P == C::N2 || q < C::N2) && e < m.E;
+        const bool active = el < C::EPB && (C::N2P == C::N2 || C::HALF || q < C::N2) && e < m.E;
         // standalone operator (MODE 0): the handle may be a z-slab (global mask layers)
-        acc += ax_group<PREC, N, MODE, MODE == 0>(m, D, in, pv, xv, g, w, apply_mask != 0, beta, alpha, e, active, a, b,
-                                                  S0)
-                   .value();
+        if constexpr (C::HALF)
+            acc += ax_group_half<PREC, N, MODE, MODE == 0>(m, D, in, pv, xv, g, w, apply_mask != 0, beta, alpha, e,
+                                                           active, a, b, h, S0)
+                       .value();
+        else
+            acc += ax_group<PREC, N, MODE, MODE == 0>(m, D, in, pv, xv, g, w, apply_mask != 0, beta, alpha, e, active,
+                                                      a, b, S0)
+                       .value();
     }
     if (MODE == 0) return;
     __shared__ TS red[32];
