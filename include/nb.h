@@ -118,8 +118,12 @@ typedef struct {
     double rtr0, rtr_final, rel_res_final, rel_res_min;
     double solve_ms;           /* device time of the solve (CUDA events on the caller stream) */
     int64_t kernel_launches;   /* kernels of this library launched by the solve */
-    double k_ax_ms, k_gs_ms, k_upd_ms;  /* when time_kernels: summed durations of the three
-                                           per-iteration kernels (Ax, dssum, update) */
+    double k_ax_ms, k_gs_ms, k_upd_ms;  /* summed per-phase device time over the iterations:
+                                           phase A (p update + Ax), the CSR gather-scatter phase
+                                           (per-copy order only), phase B (gather + update + dots);
+                                           megakernel: block 0's %globaltimer stamps after each
+                                           grid barrier; graph driver: CUDA events per kernel when
+                                           time_kernels = 1, else 0 */
 } nb_cg_report;
 
 /* Build the box mesh [0,1]^3 of nelx*nely*nelz hexes of order p on `device`
@@ -142,7 +146,7 @@ int nb_destroy(nb_handle *h);                 /* NULL is a no-op; frees all devi
  * Errors as nb_setup, plus NB_EINVAL unless 0 <= ez0 < ez1 <= nelz. */
 int nb_setup_slab(int32_t nelx, int32_t nely, int32_t nelz, int32_t ez0, int32_t ez1, int32_t p,
                   double deform_amp, uint64_t seed, int32_t device, nb_handle **out);
-int nb_query(const nb_handle *h, nb_info *out);
+int nb_query(const nb_handle *h, nb_info *out);   /* sizes of the handle's mesh (nb_info) */
 
 /* Fill device vector b (policy precision of `prec`) with a right-hand side. Async. */
 int nb_rhs(nb_handle *h, nb_rhs_kind kind, double noise_amp, uint64_t seed, nb_policy prec,
