@@ -151,9 +151,6 @@ __device__ __forceinline__ void st_chunk(T *__restrict__ p, const T (&d)[V])
 #ifndef NB_AXV64
 #define NB_AXV64 2
 #endif
-#ifndef NB_LEAN_ALL
-#define NB_LEAN_ALL 0
-#endif
 #ifndef NB_LEAN_UNROLL
 #define NB_LEAN_UNROLL 2
 #endif
@@ -347,7 +344,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         const TV *ge = g + (size_t)e * 6 * C::N3 + (size_t)N * q;
 // two chunks of geometric factors in flight for p >= 7 (fp64 phase A -3% / -14% / -7% at p = 7 / 9 / 11;
 // +2% at p = 5, so not below)
-constexpr int LEAN_U = (N >= 8 || NB_LEAN_ALL) ? NB_LEAN_UNROLL : 1;
+constexpr int LEAN_U = N >= 8 ? NB_LEAN_UNROLL : 1;
 #pragma unroll LEAN_U
         for (int c = 0; c < N / V; c++) {
             TV g1[V], g2[V], g3[V], g4[V], g5[V], g6[V], ur[V], us[V], ut[V], wr[V], ws[V], wt[V];
