@@ -154,6 +154,9 @@ __device__ __forceinline__ void st_chunk(T *__restrict__ p, const T (&d)[V])
 #ifndef NB_LEAN_UNROLL
 #define NB_LEAN_UNROLL 2
 #endif
+#ifndef NB_POLL_NS
+#define NB_POLL_NS 32
+#endif
 #ifndef NB_ELEM_BAR
 #define NB_ELEM_BAR 1
 #endif
@@ -840,6 +843,9 @@ __device__ __forceinline__ void grid_arrive_wait(unsigned int *cnt, unsigned int
 {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
     while ((int)(ld_acquire_u32(cnt) - target) < 0) {
+#if NB_POLL_NS
+        __nanosleep(NB_POLL_NS);
+#endif
     }
 }
 
