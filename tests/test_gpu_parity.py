@@ -222,3 +222,27 @@ def test_cg_csr_path_matches_fused(box8, monkeypatch):
         assert r2.kernel_launches in (1, 1 + 3 * r2.iterations + 1)
         assert r1.kernel_launches in (1, 1 + 2 * r1.iterations + 1)
     gc.close()
+
+
+@pytest.mark.parametrize("policy", [nb.NB_FP64, nb.NB_FP32, nb.NB_MIXED, nb.NB_FP32_DOT2])
+def test_cg_degenerate_cases(policy):
+    """Degenerate inputs every driver must handle: no unknowns at all (1x1x1, p=1: every node on
+    the Dirichlet boundary), a zero right-hand side, max_iter = 0, and a one-unknown system."""
+    g = nb.Mesh(1, 1, 1, 1)
+    b = g.rhs(policy)
+    assert float(torch.count_nonzero(b)) == 0
+    x, r = g.cg(b, policy, max_iter=50, rtol=1e-8)
+    assert r.status == nb.NB_CONVERGED and r.iterations == 0 and float(torch.count_nonzero(x)) == 0
+    g.close()
+    g = nb.Mesh(3, 2, 2, 3)
+    zero = g.empty(policy).zero_()
+    x, r = g.cg(zero, policy, max_iter=50, rtol=1e-8)
+    assert r.status == nb.NB_CONVERGED and r.iterations == 0 and float(torch.count_nonzero(x)) == 0
+    b = g.rhs(policy, seed=1)
+    x, r = g.cg(b, policy, max_iter=0, rtol=1e-8)
+    assert r.iterations == 0 and r.status in (nb.NB_MAXITER, nb.NB_STAGNATED) and float(torch.count_nonzero(x)) == 0
+    g.close()
+    g = nb.Mesh(1, 1, 1, 2)          # one interior node: exact after one iteration
+    x, r = g.cg(g.rhs(policy, seed=2), policy, max_iter=5, rtol=1e-6)
+    assert r.status == nb.NB_CONVERGED and r.iterations == 1
+    g.close()
