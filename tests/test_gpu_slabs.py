@@ -225,3 +225,18 @@ def test_group_every_order_matches_single(nel, p, R):
     assert np.max(np.abs(rs[0].history - r1.history)) <= 1e-11
     close_all(ms)
     g.close()
+
+
+def test_group_degenerate_cases():
+    """Zero right-hand side and max_iter = 0 through the multi-rank kernel; a one-layer-per-slab split."""
+    ms = slabs((3, 2, 3), 3, 3)
+    zeros = [m.empty(nb.NB_MIXED).zero_() for m in ms]
+    xs, rs = nb.cg_group(ms, zeros, nb.NB_MIXED, max_iter=50, rtol=1e-8)
+    assert all(r.status == nb.NB_CONVERGED and r.iterations == 0 for r in rs)
+    assert all(float(torch.count_nonzero(x)) == 0 for x in xs)
+    bs = [m.rhs(nb.NB_MIXED, seed=1) for m in ms]
+    xs, rs = nb.cg_group(ms, bs, nb.NB_MIXED, max_iter=0, rtol=1e-8)
+    assert all(r.iterations == 0 for r in rs)
+    xs, rs = nb.cg_group(ms, bs, nb.NB_MIXED, max_iter=500, rtol=1e-8)
+    assert rs[0].status == nb.NB_CONVERGED
+    close_all(ms)
