@@ -141,7 +141,7 @@ __device__ __forceinline__ void st_chunk(T *__restrict__ p, const T (&d)[V])
 // pap only.  Returns this thread's pap partial.  Contains 4 __syncthreads; consecutive calls
 // need no barrier in between (phase 1 of the next group touches only the caller's own
 // r-pencil slots, which only the caller read in phase 5).
-// Phase-A step 3 variants (measured per data size, tools/var_run.sh): NB_AXV32 / NB_AXV64 for
+// Phase-A step 3 variants (measured per data size, tools/ab_run.sh): NB_AXV32 / NB_AXV64 for
 // 4- / 8-byte data.  0: w_r^T kept in registers, pap = sum w p (p from shared); 2: register-lean
 // (fp64 needs 255 registers otherwise): the geometric factors streamed chunk by chunk through a
 // non-unrolled loop, w_r^T via shared memory, pap in its energy form.
