@@ -101,6 +101,17 @@ template <typename T, int N> struct AxCfg {
 #ifndef NB_WLD
 #define NB_WLD LD_DEF
 #endif
+// register cap for MINB resident blocks of NT threads via __maxnreg__ instead of the minimum-
+// blocks launch bound (NB_MAXNREG=1): lets ptxas use the whole budget (144 instead of 128 at
+// p = 9) but measured 25-40% slower at p = 9 / 11 in single precision (not investigated), so off
+#ifndef NB_MAXNREG
+#define NB_MAXNREG 0
+#endif
+#if NB_MAXNREG
+#define NB_KERNEL_BOUNDS(...) __launch_bounds__(__VA_ARGS__::NT) __maxnreg__((__VA_ARGS__::MAXNREG))
+#else
+#define NB_KERNEL_BOUNDS(...) __launch_bounds__(__VA_ARGS__::NT, __VA_ARGS__::MINB)
+#endif
 #ifndef NB_MINB_MODE
 #define NB_MINB_MODE 3
 #endif
@@ -115,6 +126,7 @@ template <typename T, int N> struct AxCfg {
                               : NB_MINB_MODE == 3 ? ((sizeof(T) == 4) ? (NT <= 128 ? 4 : 2) : (N <= 8 && !HALF ? 1 : 2))
                               : NB_MINB_MODE == 1 ? ((sizeof(T) == 4) ? ((NT <= 128) ? 8 : (NT <= 256 ? 4 : 2)) : ((NT <= 128) ? 4 : 2))
                                                   : ((sizeof(T) == 4) ? ((NT <= 128) ? 6 : (NT <= 256 ? 3 : 1)) : 1);
+    static constexpr int MAXNREG = (65536 / (MINB * NT)) / 8 * 8 > 255 ? 255 : (65536 / (MINB * NT)) / 8 * 8;
 };
 
 template <typename T, int V>
@@ -1061,7 +1073,7 @@ __device__ __forceinline__ void mr_reduce(const MegaArgs &A, const MrArgs &mr, i
 // compile time; VAR = 1: the NEXT-3 variants (nb_cg_opts.precond / .x_fp64) as uniform runtime
 // selects; VAR = 2: VAR 1 as one rank of a multi-rank z-slab solve (mr, vr: slab in the launch).
 template <int PREC, int N, int FUSED, int VAR>
-__global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT, AxCfg<typename Pol<PREC>::TV, N>::MINB)
+__global__ void NB_KERNEL_BOUNDS(AxCfg<typename Pol<PREC>::TV, N>)
 k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D)
 {
     static_assert(VAR == 0 || VAR == 1, "k_cg_mega: VAR 0 or 1 (VAR 2 is k_cg_mega_mr)");
@@ -1073,7 +1085,7 @@ k_cg_mega(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typen
 // Multi-rank solve: nloc slabs in this launch, Gr blocks each (cooperative launch, so the
 // slabs of one GPU that wait on one another are co-resident).
 template <int PREC, int N>
-__global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT, AxCfg<typename Pol<PREC>::TV, N>::MINB)
+__global__ void NB_KERNEL_BOUNDS(AxCfg<typename Pol<PREC>::TV, N>)
 k_cg_mega_mr(const __grid_constant__ MultiArgs M, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D)
 {
     constexpr int FUSED = 1, VAR = 2;
@@ -1089,7 +1101,7 @@ k_cg_mega_mr(const __grid_constant__ MultiArgs M, const __grid_constant__ DMat<t
 // graph driver: one persistent kernel per phase, last-block finalize
 // ===========================================================================
 template <int PREC, int N, int MODE>
-__global__ void __launch_bounds__(AxCfg<typename Pol<PREC>::TV, N>::NT, AxCfg<typename Pol<PREC>::TV, N>::MINB)
+__global__ void NB_KERNEL_BOUNDS(AxCfg<typename Pol<PREC>::TV, N>)
 k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
      const typename Pol<PREC>::TV *__restrict__ in, typename Pol<PREC>::TV *__restrict__ pv,
      typename Pol<PREC>::TV *__restrict__ xv, const typename Pol<PREC>::TV *__restrict__ g,
