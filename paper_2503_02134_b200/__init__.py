@@ -7,7 +7,11 @@ if the library cannot be loaded, importing the binding functions raises.
 
 Names follow include/nb.h (``nb_setup``, ``nb_ax``, ``nb_dssum``, ``nb_cg`` ...).
 The method is arxiv 2503.02134's Nekbone CG loop (Table 2)
-under the fp64 / fp32 / mixed policies.
+under the fp64 / fp32 / mixed policies and the fp32+Dot2
+policy; options: identity / fp32-copy Jacobi preconditioners, x in fp64.
+Multi-rank z-slab solves: ``Mesh(..., slab=(ez0, ez1))`` with ``cg_group`` (slabs sharing a
+GPU, one launch) or ``peer_attach_dist`` (one slab per GPU over CUDA IPC) then ``Mesh.cg``.
+Convenience layer: ``Mesh`` (owning handle wrapper), ``CgResult``, ``cg_group``.
 """
 from __future__ import annotations
 
