@@ -165,7 +165,8 @@ int nb_dssum(nb_handle *h, nb_policy prec, nb_gs_order order, void *u, void *str
  * nb_rhs).  Blocks until done.  The graph driver (env NB_CG_DRIVER=graph) supports the default
  * options only (policies 0-2, NB_PC_JACOBI, x_fp64 = 0): NB_EINVAL otherwise.
  * Returns NB_OK for converged / max_iter / stagnated runs, NB_EBREAKDOWN on breakdown
- * (report filled in either case). */
+ * (report filled in either case); NB_EINVAL for bad options or a mesh without unknowns
+ * (every node on the Dirichlet boundary, e.g. p = 1 with one element along an axis). */
 int nb_cg(nb_handle *h, const nb_cg_opts *o, const void *b, void *x, nb_cg_report *rep, void *stream);
 
 /* Same solve with HOST buffers (pinned or pageable): copies b in and x out on `stream`. */

@@ -756,6 +756,7 @@ static int cg_args(nb_handle *h, const nb_cg_opts *o)
         return fail(NB_EINVAL, "the graph driver supports policies 0-2 with the default options only (unset NB_CG_DRIVER)");
     if (o->gs_order != NB_GS_CONSISTENT && o->gs_order != NB_GS_PER_COPY) return fail(NB_EINVAL, "bad gs order");
     if (o->max_iter < 0 || !(o->rtol >= 0.0)) return fail(NB_EINVAL, "bad max_iter/rtol");
+    if (h->n_unmasked == 0) return fail(NB_EINVAL, "the mesh has no unknowns (every node is on the Dirichlet boundary)");
     NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
     return NB_OK;
 }
