@@ -59,6 +59,20 @@ int grid_mega(const nb_handle *h)
     return g0 > g1 ? g0 : g1;
 }
 
+// element groups on the busiest SM when G blocks split ng groups into contiguous ranges
+// (split(): block i gets [i ng / G, (i+1) ng / G)) and block i runs on SM i mod S
+static long long balanced_sm_max(long long ng, long long G, int S)
+{
+    if (S < 1) S = 1;
+    long long best = 0;
+    for (int j = 0; j < S && j < G; j++) {
+        long long w = 0;
+        for (long long i = j; i < G; i += S) w += (i + 1) * ng / G - i * ng / G;
+        if (w > best) best = w;
+    }
+    return best;
+}
+
 template <int PREC, int N, int FUSED, int VAR>
 static cudaError_t mega_launch_t(const nb_handle *h, const MegaArgs &args, cudaStream_t st)
 {
@@ -69,8 +83,9 @@ static cudaError_t mega_launch_t(const nb_handle *h, const MegaArgs &args, cudaS
     int grid = mega_grid_t<PREC, N, FUSED, VAR>(h);
     // Balanced grid: the fewest blocks that keep the same number of element groups on the
     // busiest block (configs[1]: 1024 groups on 256 blocks x 4 instead of 296 blocks x 3-4), so
-    // no wave is partly idle and the barriers have fewer arrivals (-1% single
-    // precision at 16^3, neutral for fp64).  NB_GRID_BALANCE=0: the full occupancy grid.
+    // no wave is partly idle and the barriers have fewer arrivals -- unless that raises the
+    // busiest SM's group count (blocks i -> SM i mod #SMs; e.g. 20^3 p = 11: 55 -> 57 groups,
+    // measured +4%).  DESIGN.md §6.  NB_GRID_BALANCE=0: the full occupancy grid.
     static int balance = -1;
     if (balance < 0) {
         const char *s = std::getenv("NB_GRID_BALANCE");
@@ -80,7 +95,8 @@ static cudaError_t mega_launch_t(const nb_handle *h, const MegaArgs &args, cudaS
         const long long ng = ((long long)h->E + C::EPB - 1) / C::EPB;
         const long long waves = (ng + grid - 1) / grid;
         const long long g = waves > 0 ? (ng + waves - 1) / waves : grid;
-        if (g >= 1 && g < grid) grid = (int)g;
+        if (g >= 1 && g < grid && balanced_sm_max(ng, g, h->sm_count) <= balanced_sm_max(ng, grid, h->sm_count))
+            grid = (int)g;
     }
     return cudaLaunchCooperativeKernel((const void *)k_cg_mega<PREC, N, FUSED, VAR>, dim3(grid), dim3(C::NT), params,
                                        (size_t)C::SMEM, st);
