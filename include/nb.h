@@ -163,7 +163,9 @@ int nb_dssum(nb_handle *h, nb_policy prec, nb_gs_order order, void *u, void *str
 /* Jacobi-PCG (Table 2 order) from x0 = 0.  b, x: device vectors in the
  * policy precision (x: double when o->x_fp64); b must be continuous and masked (e.g. from
  * nb_rhs).  Blocks until done.  The graph driver (env NB_CG_DRIVER=graph) supports the default
- * options only (policies 0-2, NB_PC_JACOBI, x_fp64 = 0): NB_EINVAL otherwise.
+ * options only (policies 0-2, NB_PC_JACOBI, x_fp64 = 0): NB_EINVAL otherwise.  The default
+ * driver sizes its persistent grid to balance element groups per block (env NB_GRID_BALANCE=0:
+ * full occupancy grid); the grid changes only the summation order of the dot-product partials.
  * Returns NB_OK for converged / max_iter / stagnated runs, NB_EBREAKDOWN on breakdown
  * (report filled in either case); NB_EINVAL for bad options or a mesh without unknowns
  * (every node on the Dirichlet boundary, e.g. p = 1 with one element along an axis). */
