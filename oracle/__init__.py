@@ -90,7 +90,7 @@ def lib():
         L.or_two_sum_f.argtypes = [C.c_float, C.c_float, P, P]
         L.or_two_prod_f.argtypes = [C.c_float, C.c_float, P, P]
         L.or_cg.argtypes = [P, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
-                            C.c_int, P, P, P, C.POINTER(_Report)]
+                            C.c_int, P, P, P, P, C.POINTER(_Report)]
         _lib = L
     return _lib
 
@@ -216,17 +216,23 @@ class Mesh:
 
     def cg(self, b64: np.ndarray, policy: int = FP64, max_iter: int = 100, rtol: float = 0.0,
            gs_order: int = GS_CONSISTENT, stag_window: int = 200, seqdot: bool = False,
-           x64: bool = False, precond: int = 0):
+           x64: bool = False, precond: int = 0, scalars: bool = False):
+        """C-10 PCG.  Returns (x, residual history, Report), plus with ``scalars=True`` an
+        (iterations, 3) array of the scalar recurrence rho_k, alpha_k, beta_k as the policy
+        computes them (binary64 under fp64/mixed, binary32 widened under fp32)."""
         b64 = np.ascontiguousarray(b64, dtype=np.float64)
         x = np.zeros(self.n_local)
         hist = np.zeros(max_iter + 1)
+        sc = np.zeros(3 * max(max_iter, 1))
         rep = _Report()
         rc = lib().or_cg(self._h, policy, max_iter, rtol, gs_order, stag_window, int(seqdot),
-                         int(x64), int(precond), _p(b64), _p(x), _p(hist), C.byref(rep))
+                         int(x64), int(precond), _p(b64), _p(x), _p(hist), _p(sc), C.byref(rep))
         if rc:
             raise ValueError("or_cg: bad arguments")
         r = Report(rep.iterations, rep.status, rep.rtr0, rep.rtr_final, rep.rel_res_final,
                    rep.rel_res_min, rep.true_res)
+        if scalars:
+            return x, hist[: r.iterations + 1], r, sc[: 3 * r.iterations].reshape(-1, 3)
         return x, hist[: r.iterations + 1], r
 
 

@@ -725,8 +725,19 @@ static double true_residual(const or_mesh *m, const double *b64, const double *x
     return bb > 0.0 ? sqrt(rr / bb) : 0.0;
 }
 
+/* sc (nullable): per iteration k = 1..iterations, sc[3(k-1) + 0..2] = rho_k, alpha_k, beta_k as
+   the policy computes them (widened to double) -- the scalar recurrence of Table 2, exported so
+   that tests can pin its precision (C-10 table, "rho, pap, alpha, beta" row). */
+static void put_scal(double *sc, int k, double rho, double alpha, double beta)
+{
+    if (!sc) return;
+    sc[3 * (k - 1) + 0] = rho;
+    sc[3 * (k - 1) + 1] = alpha;
+    sc[3 * (k - 1) + 2] = beta;
+}
+
 static int cg_fp64(const or_mesh *m, int max_iter, double rtol, int order, int W, int pc, const double *b64,
-                   double *x, double *res, or_report *rep)
+                   double *x, double *res, double *sc, or_report *rep)
 {
     const int64_t NL = m->NL;
     double *r = (double *)malloc(NL * sizeof(double)), *p = (double *)malloc(NL * sizeof(double));
@@ -748,6 +759,7 @@ static int cg_fp64(const or_mesh *m, int max_iter, double rtol, int order, int W
             double pap = or_glsc3_d(w, m->c, p, NL);                                 /* glsc3 */
             if (!(pap > 0.0) || !isfinite(pap) || !isfinite(rho)) { status = OR_BREAKDOWN; res[k] = res[k - 1]; break; }
             double alpha = rho / pap;
+            put_scal(sc, k, rho, alpha, beta);
             for (int64_t l = 0; l < NL; l++) x[l] = x[l] + alpha * p[l];             /* add2s2 */
             for (int64_t l = 0; l < NL; l++) r[l] = r[l] - alpha * w[l];             /* add2s2 */
             rtr = or_glsc3_d(r, m->c, r, NL);                                        /* glsc3 */
@@ -764,7 +776,7 @@ static int cg_fp64(const or_mesh *m, int max_iter, double rtol, int order, int W
 
 /* fp32 and mixed policies (C-10 table). */
 static int cg_f32(const or_mesh *m, int policy, int max_iter, double rtol, int order, int W, int seqdot,
-                  int x64, int pc, const double *b64, double *x_out, double *res, or_report *rep)
+                  int x64, int pc, const double *b64, double *x_out, double *res, double *sc, or_report *rep)
 {
     const int64_t NL = m->NL;
     const int mixed = (policy == OR_MIXED);
@@ -794,16 +806,19 @@ static int cg_f32(const or_mesh *m, int policy, int max_iter, double rtol, int o
             else if (mixed && pc == OR_PC_JACOBI) for (int64_t l = 0; l < NL; l++) z[l] = (float)((double)r[l] * m->dinv[l]);
             else for (int64_t l = 0; l < NL; l++) z[l] = r[l] * m->dinvf[l];
             float beta_f;
+            double beta_sc;
             if (mixed) {
                 rho = DOT(r, z);
                 double beta = (k == 1) ? 0.0 : rho / rho_old;
                 rho_old = rho;
+                beta_sc = beta;
                 beta_f = (float)beta;
             } else {
                 rho_f = (float)DOT(r, z);
                 beta_f = (k == 1) ? 0.0f : rho_f / rho_old_f;
                 rho_old_f = rho_f;
                 rho = rho_f;
+                beta_sc = beta_f;
             }
             for (int64_t l = 0; l < NL; l++) p[l] = z[l] + beta_f * p[l];           /* add2s1 */
             or_ax_f(m, policy, order, p, w);                                         /* ax */
@@ -813,6 +828,7 @@ static int cg_f32(const or_mesh *m, int policy, int max_iter, double rtol, int o
                 pap = DOT(w, p);
                 if (!(pap > 0.0) || !isfinite(pap) || !isfinite(rho)) { status = OR_BREAKDOWN; res[k] = res[k - 1]; break; }
                 alpha_f = (float)(rho / pap);
+                put_scal(sc, k, rho, rho / pap, beta_sc);
                 if (xd) {
                     double alpha = rho / pap;
                     for (int64_t l = 0; l < NL; l++) xd[l] = xd[l] + alpha * (double)p[l];
@@ -822,6 +838,7 @@ static int cg_f32(const or_mesh *m, int policy, int max_iter, double rtol, int o
                 pap = pap_f;
                 if (!(pap_f > 0.0f) || !isfinite(pap_f) || !isfinite(rho_f)) { status = OR_BREAKDOWN; res[k] = res[k - 1]; break; }
                 alpha_f = rho_f / pap_f;
+                put_scal(sc, k, rho_f, alpha_f, beta_sc);
             }
             for (int64_t l = 0; l < NL; l++) x[l] = x[l] + alpha_f * p[l];           /* add2s2 */
             for (int64_t l = 0; l < NL; l++) r[l] = r[l] - alpha_f * w[l];           /* add2s2 */
@@ -840,7 +857,8 @@ static int cg_f32(const or_mesh *m, int policy, int max_iter, double rtol, int o
 }
 
 int or_cg(const or_mesh *m, int policy, int max_iter, double rtol, int gs_order, int stag_window,
-          int seqdot, int x64, int precond, const double *b64, double *x_out, double *hist, or_report *rep)
+          int seqdot, int x64, int precond, const double *b64, double *x_out, double *hist, double *scal,
+          or_report *rep)
 {
     if (!m || !b64 || !x_out || !rep || max_iter < 0 || rtol < 0.0) return 1;
     if (policy < OR_FP64 || policy > OR_FP32_DOT2) return 1;
@@ -849,8 +867,8 @@ int or_cg(const or_mesh *m, int policy, int max_iter, double rtol, int gs_order,
     if (x64 && policy != OR_MIXED) return 1;
     double *res = (double *)calloc((size_t)max_iter + 1, sizeof(double));
     int rc;
-    if (policy == OR_FP64) rc = cg_fp64(m, max_iter, rtol, gs_order, stag_window, precond, b64, x_out, res, rep);
-    else rc = cg_f32(m, policy, max_iter, rtol, gs_order, stag_window, seqdot, x64, precond, b64, x_out, res, rep);
+    if (policy == OR_FP64) rc = cg_fp64(m, max_iter, rtol, gs_order, stag_window, precond, b64, x_out, res, scal, rep);
+    else rc = cg_f32(m, policy, max_iter, rtol, gs_order, stag_window, seqdot, x64, precond, b64, x_out, res, scal, rep);
     if (hist) for (int i = 0; i <= rep->iterations; i++) hist[i] = res[i];
     rep->true_res = true_residual(m, b64, x_out);
     free(res);

@@ -86,11 +86,14 @@ float or_glsc3_f_dot2(const float *a, const float *c, const float *b, int64_t n)
  *   OR_PC_IDENTITY = none, z = r ("CG with the identity ... preconditioner");
  *   OR_PC_JACOBI_F32 = Neko's single-precision copy of the Jacobi diagonal, z = r * (float)dinv in
  *   binary32 -- for fp32/dot2 the same as OR_PC_JACOBI; rejected for fp64.
+ * scal: nullable, len 3*max_iter: scal[3(k-1) + 0..2] = rho_k, alpha_k, beta_k of iteration k (the
+ *   policy's own scalar values widened to double: binary64 under fp64/mixed, binary32 under fp32).
  * Returns 0, or 1 on bad arguments.
  */
 enum { OR_PC_JACOBI = 0, OR_PC_IDENTITY = 1, OR_PC_JACOBI_F32 = 2 };
 int or_cg(const or_mesh *m, int policy, int max_iter, double rtol, int gs_order, int stag_window,
-          int seqdot, int x64, int precond, const double *b64, double *x_out, double *hist, or_report *rep);
+          int seqdot, int x64, int precond, const double *b64, double *x_out, double *hist, double *scal,
+          or_report *rep);
 
 #ifdef __cplusplus
 }
