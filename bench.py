@@ -325,11 +325,11 @@ def run_ours(args):
     max_iter = 4000
     st = torch.cuda.current_stream()
 
-    def solve(time_kernels=False):
+    def solve():
         if group:
             reps, _ = nb.nb_cg_group([m.h for m in group], gb, gx, pol, max_iter, WORKLOAD["rtol"], history=False)
             return reps[0]
-        rep, _ = nb.nb_cg(mesh.h, b, x, pol, max_iter, WORKLOAD["rtol"], time_kernels=time_kernels, history=False)
+        rep, _ = nb.nb_cg(mesh.h, b, x, pol, max_iter, WORKLOAD["rtol"], history=False)
         return rep
 
     for _ in range(max(3, args.warmup)):
@@ -356,8 +356,8 @@ def run_ours(args):
     value, t_max = aggregate(NL * sum(iters), t_local, world)
 
     # per-phase device time of the same solve: the megakernel's block 0 stamps %globaltimer after
-    # every grid barrier (nb_cg_report k_ax_ms / k_upd_ms); graph driver: CUDA events per launch
-    kt = [solve(time_kernels=True) for _ in range(max(1, min(args.steps, 3)))]
+    # every grid barrier (nb_cg_report k_ax_ms / k_upd_ms)
+    kt = [solve() for _ in range(max(1, min(args.steps, 3)))]
     it_k = sum(r.iterations for r in kt)
     k1_ms = sum(r.k_ax_ms for r in kt) / it_k
     k2_ms = sum(r.k_upd_ms for r in kt) / it_k
@@ -408,7 +408,7 @@ def run_ours(args):
                 flush.zero_()
                 r, _ = nb.nb_cg(mesh.h, bb, xx, pp, max_iter, WORKLOAD["rtol"], history=False)
                 reps.append(r)
-            rk, _ = nb.nb_cg(mesh.h, bb, xx, pp, max_iter, WORKLOAD["rtol"], time_kernels=True, history=False)
+            rk, _ = nb.nb_cg(mesh.h, bb, xx, pp, max_iter, WORKLOAD["rtol"], history=False)
             n_it = rk.iterations
             tmed = statistics.median(r.solve_ms for r in reps)
             ttr[name] = {"iterations": reps[-1].iterations, "status": reps[-1].status, "time_ms": tmed,

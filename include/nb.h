@@ -105,11 +105,15 @@ typedef struct {
     double rtol;               /* stop when sqrt(rtr/rtr0) <= rtol; 0 = run exactly max_iter */
     nb_gs_order gs_order;
     int32_t stag_window;       /* C-11 window W (default 200 when <= 0) */
-    int32_t time_kernels;      /* 1: record per-kernel CUDA-event durations into the report */
+    int32_t reserved0;         /* must be 0 */
     double *rel_res_history;   /* host, length max_iter+1, nullable: [0] = 1, [k] = sqrt(rtr_k/rtr0) */
     nb_precond precond;        /* 0 = NB_PC_JACOBI (zero-initialised options keep the default) */
     int32_t x_fp64;            /* NB_MIXED only (else NB_EINVAL): x += alpha p accumulated in double
                                   with the double alpha, and x returned as n_local DOUBLES (C-15 variant) */
+    double *scal_history;      /* host, length 3*max_iter, nullable: for k = 1..iterations,
+                                  [3(k-1) + 0..2] = rho_k, alpha_k, beta_k of Table 2
+                                  as the policy computes them: binary64 under NB_FP64 / NB_MIXED,
+                                  binary32 (widened exactly) under NB_FP32 / NB_FP32_DOT2 (C-10 table) */
 } nb_cg_opts;
 
 typedef struct {
@@ -118,12 +122,11 @@ typedef struct {
     double rtr0, rtr_final, rel_res_final, rel_res_min;
     double solve_ms;           /* device time of the solve (CUDA events on the caller stream) */
     int64_t kernel_launches;   /* kernels of this library launched by the solve */
-    double k_ax_ms, k_gs_ms, k_upd_ms;  /* summed per-phase device time over the iterations:
-                                           phase A (p update + Ax), the CSR gather-scatter phase
-                                           (per-copy order only), phase B (gather + update + dots);
-                                           megakernel: block 0's %globaltimer stamps after each
-                                           grid barrier; graph driver: CUDA events per kernel when
-                                           time_kernels = 1, else 0 */
+    double k_ax_ms, k_gs_ms, k_upd_ms;  /* summed per-phase device time over the iterations (block 0's
+                                           %globaltimer stamps after each grid barrier of the
+                                           megakernel): phase A (p update + Ax), the CSR gather-
+                                           scatter phase (per-copy order only), phase B (gather +
+                                           update + dots) */
 } nb_cg_report;
 
 /* Build the box mesh [0,1]^3 of nelx*nely*nelz hexes of order p on `device`

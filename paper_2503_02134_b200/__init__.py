@@ -54,8 +54,8 @@ class nb_info(C.Structure):
 
 class nb_cg_opts(C.Structure):
     _fields_ = [("policy", C.c_int), ("max_iter", C.c_int32), ("rtol", C.c_double), ("gs_order", C.c_int),
-                ("stag_window", C.c_int32), ("time_kernels", C.c_int32), ("rel_res_history", C.c_void_p),
-                ("precond", C.c_int), ("x_fp64", C.c_int32)]
+                ("stag_window", C.c_int32), ("reserved0", C.c_int32), ("rel_res_history", C.c_void_p),
+                ("precond", C.c_int), ("x_fp64", C.c_int32), ("scal_history", C.c_void_p)]
 
 
 class nb_cg_report(C.Structure):
@@ -175,7 +175,7 @@ def nb_cg_group(hs, bs, xs, policy: int = NB_MIXED, max_iter: int = 1000, rtol: 
     n = len(hs)
     dt = policy_dtype(policy)
     hist = np.zeros(max_iter + 1) if history else None
-    o = _opts(policy, max_iter, rtol, NB_GS_CONSISTENT, stag_window, False, hist, precond, x64)
+    o = _opts(policy, max_iter, rtol, NB_GS_CONSISTENT, stag_window, hist, precond, x64)
     reps = (nb_cg_report * n)()
     H = (C.c_void_p * n)(*[h.value if isinstance(h, C.c_void_p) else h for h in hs])
     B = (C.c_void_p * n)(*[_dptr(b, dt).value for b in bs])
@@ -241,24 +241,28 @@ def nb_dssum(h, prec: int, order: int, u, stream=None):
     _check(lib().nb_dssum(h, prec, order, _dptr(u, policy_dtype(prec)), _stream(stream)))
 
 
-def _opts(policy, max_iter, rtol, gs_order, stag_window, time_kernels, hist, precond=NB_PC_JACOBI, x64=False):
+def _opts(policy, max_iter, rtol, gs_order, stag_window, hist, precond=NB_PC_JACOBI, x64=False, scal=None):
     o = nb_cg_opts()
     o.policy, o.max_iter, o.rtol, o.gs_order = policy, max_iter, rtol, gs_order
-    o.stag_window, o.time_kernels = stag_window, int(time_kernels)
+    o.stag_window, o.reserved0 = stag_window, 0
     o.precond, o.x_fp64 = precond, int(x64)
     o.rel_res_history = hist.ctypes.data if hist is not None else None
+    if scal is not None:
+        assert scal.dtype == np.float64 and scal.flags["C_CONTIGUOUS"] and scal.size >= 3 * max_iter
+    o.scal_history = scal.ctypes.data if scal is not None else None
     return o
 
 
 def nb_cg(h, b, x, policy: int = NB_MIXED, max_iter: int = 1000, rtol: float = 1e-8,
-          gs_order: int = NB_GS_CONSISTENT, stag_window: int = 200, time_kernels: bool = False,
+          gs_order: int = NB_GS_CONSISTENT, stag_window: int = 200,
           history: bool = True, stream=None, allow_breakdown: bool = True, precond: int = NB_PC_JACOBI,
-          x64: bool = False):
-    """PCG from x0 = 0; returns (report, rel_res_history).  x is float64 when x64."""
+          x64: bool = False, scal_out: np.ndarray | None = None):
+    """PCG from x0 = 0; returns (report, rel_res_history).  x is float64 when x64.
+    scal_out (float64, >= 3*max_iter): receives rho_k, alpha_k, beta_k per iteration."""
     import torch
     dt = policy_dtype(policy)
     hist = np.zeros(max_iter + 1) if history else None
-    o = _opts(policy, max_iter, rtol, gs_order, stag_window, time_kernels, hist, precond, x64)
+    o = _opts(policy, max_iter, rtol, gs_order, stag_window, hist, precond, x64, scal_out)
     rep = nb_cg_report()
     rc = lib().nb_cg(h, C.byref(o), _dptr(b, dt), _dptr(x, torch.float64 if x64 else dt), C.byref(rep),
                      _stream(stream))
@@ -278,7 +282,7 @@ def nb_cg_host(h, b_host, x_host, policy: int = NB_MIXED, max_iter: int = 1000, 
         assert a.device.type == "cpu" and a.is_contiguous() and a.dtype == policy_dtype(pol)
         return C.c_void_p(a.data_ptr())
     hist = np.zeros(max_iter + 1) if history else None
-    o = _opts(policy, max_iter, rtol, gs_order, stag_window, False, hist, precond, x64)
+    o = _opts(policy, max_iter, rtol, gs_order, stag_window, hist, precond, x64)
     rep = nb_cg_report()
     rc = lib().nb_cg_host(h, C.byref(o), hp(b_host, policy), hp(x_host, NB_FP64 if x64 else policy), C.byref(rep),
                           _stream(stream))
@@ -335,6 +339,7 @@ class CgResult:
     k_gs_ms: float
     k_upd_ms: float
     history: np.ndarray | None
+    scalars: np.ndarray | None = None   # (iterations, 3): rho_k, alpha_k, beta_k
 
 
 class Mesh:
@@ -386,12 +391,14 @@ class Mesh:
         return v
 
     def cg(self, b, policy=NB_MIXED, max_iter=1000, rtol=1e-8, gs_order=NB_GS_CONSISTENT, stag_window=200,
-           time_kernels=False, precond=NB_PC_JACOBI, x64=False):
+           precond=NB_PC_JACOBI, x64=False, scalars=False):
         x = self.empty(NB_FP64 if x64 else policy)
-        rep, hist = nb_cg(self.h, b, x, policy, max_iter, rtol, gs_order, stag_window, time_kernels,
-                          precond=precond, x64=x64)
+        sc = np.zeros(3 * max(max_iter, 1)) if scalars else None
+        rep, hist = nb_cg(self.h, b, x, policy, max_iter, rtol, gs_order, stag_window,
+                          precond=precond, x64=x64, scal_out=sc)
         r = CgResult(rep.iterations, rep.status, rep.rtr0, rep.rel_res_final, rep.rel_res_min, rep.solve_ms,
-                     rep.kernel_launches, rep.k_ax_ms, rep.k_gs_ms, rep.k_upd_ms, hist)
+                     rep.kernel_launches, rep.k_ax_ms, rep.k_gs_ms, rep.k_upd_ms, hist,
+                     sc[: 3 * rep.iterations].reshape(-1, 3) if sc is not None else None)
         return x, r
 
 

@@ -1,6 +1,6 @@
 // nb_api.cu -- the C ABI (include/nb.h): argument checking, setup orchestration,
-// GLL basis on the host, CG driver (device-resident scalars, CUDA graph with a
-// conditional WHILE node so the whole iteration loop runs without host round trips).
+// GLL basis on the host, CG driver (one persistent megakernel per solve: device-resident
+// scalars, the whole iteration loop without host round trips).
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -164,22 +164,13 @@ static int alloc_ws(nb_handle *h, int prec, int32_t max_iter)
         NB_CU(cudaMalloc(&ws.w, vs), "cudaMalloc w");
         NB_CU(cudaMalloc(&ws.x, vs), "cudaMalloc x");
         NB_CU(cudaMalloc(&ws.z, vs), "cudaMalloc z");
-        int maxblk = NB_POL(prec, nb::grid_k1, h);
-        const int g2 = NB_POL(prec, nb::grid_k2, h), gg = nb::grid_gs(h);
-        if (g2 > maxblk) maxblk = g2;
-        if (gg > maxblk) maxblk = gg;
-        const int nchunk = (maxblk + 255) / 256;
         ws.mega_G = NB_POL(prec, nb::grid_mega, h);
         // megakernel partials: 4 accumulators per block (pap, shared pap, rtr, rho), 2 doubles
         // each for the Dot2 expansions (nb_mega_launch.cuh: launch_cg_mega)
         const int mslots = (prec == NB_FP32_DOT2 ? 8 : 4) * ws.mega_G;
-        const int nslots = 2 * maxblk > mslots ? 2 * maxblk : mslots;
-        NB_CU(cudaMalloc(&ws.red.part, sizeof(double) * nslots), "cudaMalloc part");
+        NB_CU(cudaMalloc(&ws.part, sizeof(double) * mslots), "cudaMalloc part");
         NB_CU(cudaMalloc(&ws.bar, sizeof(unsigned int) * 2), "cudaMalloc bar");
         NB_CU(cudaMemset(ws.bar, 0, sizeof(unsigned int) * 2), "memset bar");
-        NB_CU(cudaMalloc(&ws.red.part2, sizeof(double) * 2 * nchunk), "cudaMalloc part2");
-        NB_CU(cudaMalloc(&ws.red.cnt, sizeof(uint32_t) * (1 + nchunk)), "cudaMalloc cnt");
-        NB_CU(cudaMemset(ws.red.cnt, 0, sizeof(uint32_t) * (1 + nchunk)), "memset cnt");
         NB_CU(cudaMalloc(&ws.scal, sizeof(nb::Scal)), "cudaMalloc scal");
         NB_CU(cudaMallocHost(&ws.scal_host, sizeof(nb::Scal)), "cudaMallocHost scal");
         NB_CU(cudaMemset(ws.scal, 0, sizeof(nb::Scal)), "memset scal");
@@ -188,18 +179,17 @@ static int alloc_ws(nb_handle *h, int prec, int32_t max_iter)
     }
     if (ws.hist_cap < max_iter + 1) {
         if (ws.hist) cudaFree(ws.hist);
+        if (ws.shist) cudaFree(ws.shist);
         if (ws.tim) cudaFree(ws.tim);
         ws.hist = nullptr;
+        ws.shist = nullptr;
         ws.tim = nullptr;
         ws.hist_cap = 0;
         const int cap = max_iter + 1 < 1024 ? 1024 : max_iter + 1;
         NB_CU(cudaMalloc(&ws.hist, sizeof(double) * cap), "cudaMalloc hist");
+        NB_CU(cudaMalloc(&ws.shist, sizeof(double) * 3 * cap), "cudaMalloc shist");
         NB_CU(cudaMalloc(&ws.tim, sizeof(unsigned long long) * 3 * cap), "cudaMalloc tim");
         ws.hist_cap = cap;
-        for (int o = 0; o < 2; o++) {   // graphs captured the old history pointer
-            if (ws.exec[o]) { cudaGraphExecDestroy(ws.exec[o]); ws.exec[o] = nullptr; }
-            if (ws.graph[o]) { cudaGraphDestroy(ws.graph[o]); ws.graph[o] = nullptr; }
-        }
     }
     return NB_OK;
 }
@@ -219,76 +209,12 @@ int ensure_ws(nb_handle *h, int prec, int32_t max_iter)
 
 void free_ws(nb::Workspace &ws)
 {
-    for (int o = 0; o < 2; o++) {
-        if (ws.exec[o]) cudaGraphExecDestroy(ws.exec[o]);
-        if (ws.graph[o]) cudaGraphDestroy(ws.graph[o]);
-    }
     for (int i = 0; i < ws.peer.nopened; i++) cudaIpcCloseMemHandle(ws.peer.opened[i]);
     cudaFree(ws.r); cudaFree(ws.p); cudaFree(ws.w); cudaFree(ws.x); cudaFree(ws.z); cudaFree(ws.xd); cudaFree(ws.ctl);
-    cudaFree(ws.red.part); cudaFree(ws.red.part2); cudaFree(ws.red.cnt);
-    cudaFree(ws.scal); cudaFree(ws.hist); cudaFree(ws.tim); cudaFree(ws.bar);
+    cudaFree(ws.part);
+    cudaFree(ws.scal); cudaFree(ws.hist); cudaFree(ws.shist); cudaFree(ws.tim); cudaFree(ws.bar);
     if (ws.scal_host) cudaFreeHost(ws.scal_host);
     ws = nb::Workspace();
-}
-
-// One CG iteration.  Consistent order: K1 (Ax + pap + alpha) -> K2 (gather + update).
-// Per-copy order (or NB_CG_GS=csr): K1 (Ax, unshared pap) -> CSR dssum (+ shared pap, alpha)
-// -> K2 (update without gather).  Returns the number of kernels launched; launch errors in err.
-int iteration(nb_handle *h, int prec, int order, nb::Workspace &ws, cudaStream_t st,
-              cudaGraphConditionalHandle cond, bool use_cond, cudaError_t &err, cudaEvent_t *ev = nullptr)
-{
-    const bool fused = order == NB_GS_CONSISTENT && !h->cg_csr;
-    if (ev) cudaEventRecord(ev[0], st);
-    err = NB_POL(prec, nb::launch_cg_k1, h, ws, fused, st);
-    if (err != cudaSuccess) return 0;
-    if (ev) cudaEventRecord(ev[1], st);
-    if (!fused) {
-        err = nb::launch_cg_gs(h, prec, order, ws, st);
-        if (err != cudaSuccess) return 1;
-    }
-    if (ev) cudaEventRecord(ev[2], st);
-    err = NB_POL(prec, nb::launch_cg_k2, h, ws, fused, st, cond, use_cond);
-    if (ev) cudaEventRecord(ev[3], st);
-    return fused ? 2 : 3;
-}
-
-// Conditional-WHILE graph: body = one iteration; its last kernel clears the condition when
-// the solve is done.  After the loop, the deferred x += alpha p.  One graph launch per solve.
-int build_graph(nb_handle *h, int prec, int order)
-{
-    nb::Workspace &ws = h->ws[prec];
-    if (ws.exec[order]) return NB_OK;
-    cudaGraph_t graph;
-    NB_CU(cudaGraphCreate(&graph, 0), "cudaGraphCreate");
-    cudaGraphConditionalHandle cond;
-    NB_CU(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault), "cond handle");
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = cond;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t node;
-    NB_CU(cudaGraphAddNode(&node, graph, nullptr, 0, &cp), "add conditional node");
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
-    NB_CU(cudaStreamBeginCaptureToGraph(h->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed),
-          "begin capture");
-    cudaError_t e1;
-    iteration(h, prec, order, ws, h->cap_stream, cond, true, e1);
-    cudaGraph_t captured;
-    cudaError_t ec = cudaStreamEndCapture(h->cap_stream, &captured);
-    if (e1 != cudaSuccess) return cuda_fail(e1, "capture iteration");
-    if (ec != cudaSuccess) return cuda_fail(ec, "end capture");
-    NB_CU(cudaStreamBeginCaptureToGraph(h->cap_stream, graph, &node, nullptr, 1, cudaStreamCaptureModeRelaxed),
-          "begin capture fin");
-    e1 = NB_POL(prec, nb::launch_cg_fin, h, ws, h->cap_stream);
-    ec = cudaStreamEndCapture(h->cap_stream, &captured);
-    if (e1 != cudaSuccess) return cuda_fail(e1, "capture fin");
-    if (ec != cudaSuccess) return cuda_fail(ec, "end capture fin");
-    cudaGraphExec_t exec;
-    NB_CU(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
-    ws.graph[order] = graph;
-    ws.exec[order] = exec;
-    return NB_OK;
 }
 
 // C-11 stagnation rule on the host history (only for runs that did not converge)
@@ -335,8 +261,6 @@ static int setup_box(nb_handle *h, bool jacobi)
     {
         const char *gs = std::getenv("NB_CG_GS");
         h->cg_csr = (gs && std::strcmp(gs, "csr") == 0) ? 1 : 0;
-        const char *dr = std::getenv("NB_CG_DRIVER");
-        h->cg_graph = (dr && std::strcmp(dr, "graph") == 0) ? 1 : 0;
     }
     if ((e = cudaMalloc(&h->g64, sizeof(double) * 6 * NL)) != cudaSuccess) return fail(NB_ENOMEM, "cudaMalloc g64");
     if ((e = cudaMalloc(&h->B, sizeof(double) * NL)) != cudaSuccess) return fail(NB_ENOMEM, "cudaMalloc B");
@@ -564,8 +488,6 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
     nb_handle *h0 = hs[0];
     nb::Workspace &ws0 = h0->ws[prec];
     const bool multi = nh > 1 || ws0.peer.nrank > 0;
-    const bool mega = !h0->cg_graph;
-    if (!multi && !mega && !o->time_kernels && (rc = build_graph(h0, prec, order))) return rc;
 
     EventSet tev;
     NB_CU(tev.create(2), "event");
@@ -588,9 +510,6 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
         NB_CU(cudaMemcpyAsync(ws.scal, ws.scal_host, sizeof(nb::Scal), cudaMemcpyHostToDevice, st), "copy scal");
     }
     int64_t launches = 0;
-    const bool fused = order == NB_GS_CONSISTENT && !h0->cg_csr;
-    const int per_it = fused ? 2 : 3;
-    double kms[3] = {0.0, 0.0, 0.0};
     if (multi) {
         // z-slab solve: one MR megakernel for this GPU's slabs
         nb::MultiArgs M;
@@ -625,48 +544,11 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
         if (M.mr.Gr < 1) return fail(NB_EINVAL, "too many slabs for one launch");
         NB_CU(NB_POL(prec, nb::launch_cg_mr, h0, M, st), "cg multi-rank megakernel");
         launches = 1;
-    } else if (mega) {
+    } else {
         NB_CU(NB_POL(prec, nb::launch_cg_mega, h0, ws0, bdev[0], order, o->max_iter, o->rtol, (int)o->precond,
                      (int)o->x_fp64, ws0.tim, st),
               "cg megakernel");
         launches = 1;
-    } else {
-        NB_CU(NB_POL(prec, nb::launch_cg_init, h0, ws0, bdev[0], st), "cg init");
-        launches = 1;
-        if (!o->time_kernels) {
-            NB_CU(cudaGraphLaunch(ws0.exec[order], st), "graph launch");
-        } else {
-            // per-kernel CUDA-event timing: direct launches, check the done flag every 16 iterations
-            const int chunk = 16;
-            EventSet evs;
-            NB_CU(evs.create(4 * chunk), "event");
-            std::vector<cudaEvent_t> &ev = evs.ev;
-            int k = 0;
-            bool done = false;
-            while (!done && k < o->max_iter) {
-                const int m = (o->max_iter - k) < chunk ? (o->max_iter - k) : chunk;
-                for (int c = 0; c < m; c++) {
-                    cudaError_t e;
-                    iteration(h0, prec, order, ws0, st, 0, false, e, &ev[4 * c]);
-                    NB_CU(e, "iteration");
-                }
-                NB_CU(cudaMemcpyAsync(ws0.scal_host, ws0.scal, sizeof(nb::Scal), cudaMemcpyDeviceToHost, st), "scal");
-                NB_CU(cudaStreamSynchronize(st), "sync");
-                const int before = k;
-                const int it_now = ws0.scal_host->iter;
-                for (int c = 0; c < m; c++) {
-                    if (before + c >= it_now && ws0.scal_host->done) break;   // no-op launches after the end
-                    float a, b2, c3;
-                    cudaEventElapsedTime(&a, ev[4 * c], ev[4 * c + 1]);
-                    cudaEventElapsedTime(&b2, ev[4 * c + 1], ev[4 * c + 2]);
-                    cudaEventElapsedTime(&c3, ev[4 * c + 2], ev[4 * c + 3]);
-                    kms[0] += a; kms[1] += b2; kms[2] += c3;
-                }
-                k += m;
-                done = ws0.scal_host->done != 0;
-            }
-            NB_CU(NB_POL(prec, nb::launch_cg_fin, h0, ws0, st), "cg fin");
-        }
     }
     for (int r = 0; r < nh; r++) {
         nb_handle *h = hs[r];
@@ -689,9 +571,9 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
         const int k = s.iter;
         std::vector<double> res(k + 1, 0.0);
         NB_CU(cudaMemcpy(res.data(), ws.hist, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost), "copy hist");
-        double km[3] = {kms[0], kms[1], kms[2]};
-        int64_t nl = launches;
-        if (mega || multi) {
+        double km[3] = {0.0, 0.0, 0.0};
+        const int64_t nl = launches;
+        {
             // phase durations from the block-0 globaltimer stamps taken after each grid barrier
             std::vector<unsigned long long> tm(3 * (size_t)(k + 1), 0ull);
             NB_CU(cudaMemcpy(tm.data(), ws.tim, sizeof(unsigned long long) * 3 * (k + 1), cudaMemcpyDeviceToHost),
@@ -702,11 +584,9 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
                 const double tB = (double)tm[3 * i] - (double)tm[3 * (i - 1) + 2];
                 km[0] += 1e-6 * tA; km[1] += 1e-6 * tS; km[2] += 1e-6 * tB;
             }
-        } else {
-            // kernels that did work: init, per_it per completed iteration (+ the partial iteration of a
-            // breakdown), the deferred-x kernel
-            nl += (int64_t)per_it * k + (s.status == NB_BROKEDOWN ? per_it - 1 : 0) + 1;
         }
+        if (o->scal_history && r == 0 && k > 0)
+            NB_CU(cudaMemcpy(o->scal_history, ws.shist, sizeof(double) * 3 * k, cudaMemcpyDeviceToHost), "copy shist");
         int status = s.status;
         if (status == NB_MAXITER && o->rtol > 0.0) status = classify(res, k, o->stag_window > 0 ? o->stag_window : 200);
         if (o->rel_res_history && r == 0) memcpy(o->rel_res_history, res.data(), sizeof(double) * (k + 1));
@@ -749,11 +629,8 @@ static int cg_args(nb_handle *h, const nb_cg_opts *o)
     if (o->precond == NB_PC_JACOBI_F32 && o->policy == NB_FP64)
         return fail(NB_EINVAL, "NB_PC_JACOBI_F32 is a single-precision variant (not for NB_FP64)");
     if (o->x_fp64 != 0 && o->x_fp64 != 1) return fail(NB_EINVAL, "x_fp64 must be 0 or 1");
+    if (o->reserved0 != 0) return fail(NB_EINVAL, "nb_cg_opts.reserved0 must be 0");
     if (o->x_fp64 && o->policy != NB_MIXED) return fail(NB_EINVAL, "x_fp64 applies to NB_MIXED only");
-    // the graph driver's last-block grid reduction carries one plain value per block, and its
-    // kernels implement the default options only
-    if (h->cg_graph && (o->policy == NB_FP32_DOT2 || o->precond != NB_PC_JACOBI || o->x_fp64))
-        return fail(NB_EINVAL, "the graph driver supports policies 0-2 with the default options only (unset NB_CG_DRIVER)");
     if (o->gs_order != NB_GS_CONSISTENT && o->gs_order != NB_GS_PER_COPY) return fail(NB_EINVAL, "bad gs order");
     if (o->max_iter < 0 || !(o->rtol >= 0.0)) return fail(NB_EINVAL, "bad max_iter/rtol");
     if (h->n_unmasked == 0) return fail(NB_EINVAL, "the mesh has no unknowns (every node is on the Dirichlet boundary)");
@@ -765,7 +642,7 @@ static int cg_args(nb_handle *h, const nb_cg_opts *o)
 static int mr_args(const nb_handle *h, const nb_cg_opts *o)
 {
     if (o->gs_order != NB_GS_CONSISTENT) return fail(NB_EINVAL, "multi-rank solves use the consistent GS order");
-    if (h->cg_csr || h->cg_graph) return fail(NB_EINVAL, "multi-rank solves run on the fused megakernel only");
+    if (h->cg_csr) return fail(NB_EINVAL, "multi-rank solves run on the fused megakernel only");
     return NB_OK;
 }
 

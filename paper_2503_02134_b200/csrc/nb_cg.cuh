@@ -29,16 +29,14 @@
 // sums: phase A contributes only the unshared nodes, a CSR phase (nb_gs.cuh) does QQ^T and
 // the shared part of pap, and phase B runs without the gather.
 //
-// Two drivers run these phases:
-//   * k_cg_mega: ONE persistent cooperative kernel per solve.  Every block owns a contiguous
-//     element range; grid-wide barriers separate the phases; after each barrier every block
-//     reduces the per-block partials itself, in the same fixed order, so all blocks take the
-//     same (bit-identical) scalar decisions -- no host round trip, no launch gaps, no serial
-//     last-block tail.  (Default.)  k_cg_mega_mr is the same body for z-slabs of a box spread
-//     over ranks (GPUs, or slabs sharing one launch): the gather reads the neighbour slab's w,
-//     the reductions add a per-rank push/flag step (mr_reduce).  Body: nb_mega_body.inc.
-//   * k_ax / k_upd: one persistent kernel per phase, chained in a CUDA graph with a
-//     conditional WHILE node; scalars finalised by the last block (NB_CG_DRIVER=graph).
+// The driver is ONE persistent cooperative kernel per solve (k_cg_mega).  Every block owns a
+// contiguous element range; grid-wide barriers separate the phases; after each barrier every
+// block reduces the per-block partials itself, in the same fixed order, so all blocks take the
+// same (bit-identical) scalar decisions -- no host round trip, no launch gaps, no serial
+// last-block tail.  k_cg_mega_mr is the same body for z-slabs of a box spread over ranks (GPUs,
+// or slabs sharing one launch): the gather reads the neighbour slab's w, the reductions add a
+// per-rank push/flag step (mr_reduce).  Body: nb_mega_body.inc.  k_ax is the standalone
+// operator of nb_ax.
 #pragma once
 #include "nb_common.cuh"
 #include "nb_gs.cuh"
@@ -1098,20 +1096,17 @@ k_cg_mega_mr(const __grid_constant__ MultiArgs M, const __grid_constant__ DMat<t
 }
 
 // ===========================================================================
-// graph driver: one persistent kernel per phase, last-block finalize
+// standalone operator (nb_ax): w = A_L u (+ dssum-free mask), one persistent kernel
 // ===========================================================================
-template <int PREC, int N, int MODE>
+template <int PREC, int N>
 __global__ void NB_KERNEL_BOUNDS(AxCfg<typename Pol<PREC>::TV, N>)
 k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
-     const typename Pol<PREC>::TV *__restrict__ in, typename Pol<PREC>::TV *__restrict__ pv,
-     typename Pol<PREC>::TV *__restrict__ xv, const typename Pol<PREC>::TV *__restrict__ g,
-     typename Pol<PREC>::TV *__restrict__ w, int apply_mask, Scal *__restrict__ scal, const RedWs rw)
+     const typename Pol<PREC>::TV *__restrict__ in, const typename Pol<PREC>::TV *__restrict__ g,
+     typename Pol<PREC>::TV *__restrict__ w, int apply_mask)
 {
     using TV = typename Pol<PREC>::TV;
-    using TS = typename Pol<PREC>::TS;
     using C = AxCfg<TV, N>;
     extern __shared__ __align__(16) unsigned char smraw[];
-    if (MODE != 0 && scal->done) return;   // grid-uniform
     const int tid = threadIdx.x;
     const int el = tid / C::N2P;
     const int q = tid - el * C::N2P;
@@ -1119,179 +1114,50 @@ k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
     const int h = C::HALF ? q / C::N2 : 0;
     const int a = qp % N, b = qp / N;
     TV *S0 = reinterpret_cast<TV *>(smraw) + (el < C::EPB ? el : 0) * C::NARR * C::ESZ;
-    TV beta = 0, alpha = 0;
-    if (MODE != 0) {
-        beta = (TV)(TS)scal->beta;
-        alpha = scal->pending ? (TV)(TS)scal->alpha : TV(0);
-    }
     const int64_t ngroups = ((int64_t)m.E + C::EPB - 1) / C::EPB;
     const int64_t g0 = split(ngroups, gridDim.x, blockIdx.x), g1 = split(ngroups, gridDim.x, blockIdx.x + 1);
-    TS acc = 0;
 #pragma unroll 1
     for (int64_t gr = g0; gr < g1; gr++) {
         const int e = (int)(gr * C::EPB) + el;
         const bool active = el < C::EPB && (C::N2P == C::N2 || C::HALF || q < C::N2) && e < m.E;
-        // standalone operator (MODE 0): the handle may be a z-slab (global mask layers)
+        // the handle may be a z-slab (global mask layers): SLAB = true
         if constexpr (C::HALF)
-            acc += ax_group_half<PREC, N, MODE, MODE == 0>(m, D, in, pv, xv, g, w, apply_mask != 0, beta, alpha, e,
-                                                           active, a, b, h, S0)
-                       .value();
+            ax_group_half<PREC, N, 0, true>(m, D, in, nullptr, nullptr, g, w, apply_mask != 0, TV(0), TV(0), e, active,
+                                            a, b, h, S0);
         else
-            acc += ax_group<PREC, N, MODE, MODE == 0>(m, D, in, pv, xv, g, w, apply_mask != 0, beta, alpha, e, active,
-                                                      a, b, S0)
-                       .value();
+            ax_group<PREC, N, 0, true>(m, D, in, nullptr, nullptr, g, w, apply_mask != 0, TV(0), TV(0), e, active, a, b,
+                                       S0);
     }
-    if (MODE == 0) return;
-    __shared__ TS red[32];
-    TS v[1] = {block_sum<TS>(acc, red)};
-    TS tot[1];
-    if (grid_reduce<TS, 1>(v, rw, tot) && tid == 0) {
-        if (MODE == 2) {
-            scal->pap = (double)tot[0];
-        } else {
-            const TS pap = tot[0];
-            const TS rho = (TS)scal->rho;
-            scal->pap = (double)pap;
-            if (!(pap > (TS)0) || !isfinite((double)pap) || !isfinite((double)rho)) {
-                scal->status = NB_BROKEDOWN;
-                scal->done = 1;
-                scal->pending = 0;
-            } else {
-                scal->alpha = (double)(rho / pap);
-                scal->pending = 1;
-            }
-        }
-    }
-}
-
-constexpr int UPD_NT = 256;
-
-template <int PREC, int N, int GATHER>
-__global__ void __launch_bounds__(UPD_NT)
-k_upd(const MeshDev m, const typename Pol<PREC>::TV *__restrict__ w, typename Pol<PREC>::TV *__restrict__ r,
-      typename Pol<PREC>::TV *__restrict__ z, const typename Pol<PREC>::TJ *__restrict__ dinv,
-      Scal *__restrict__ scal, const RedWs rw, double *__restrict__ hist, cudaGraphConditionalHandle cond,
-      int use_cond)
-{
-    using TV = typename Pol<PREC>::TV;
-    using TS = typename Pol<PREC>::TS;
-    if (scal->done) {
-        if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
-        return;
-    }
-    const TV alpha = (TV)(TS)scal->alpha;
-    Acc<PREC> artr, arho;
-    const int64_t np = (int64_t)m.E * N * N;
-    const int64_t p0 = split(np, gridDim.x, blockIdx.x), p1 = split(np, gridDim.x, blockIdx.x + 1);
-    for (int64_t pid = p0 + threadIdx.x; pid < p1; pid += UPD_NT)
-        upd_pencil<PREC, N, GATHER>(m, w, r, z, dinv, alpha, pid, artr, arho);
-    __shared__ TS red[32];
-    TS v[2];
-    v[0] = block_sum<TS>(artr.value(), red);
-    v[1] = block_sum<TS>(arho.value(), red);
-    TS tot[2];
-    if (grid_reduce<TS, 2>(v, rw, tot) && threadIdx.x == 0) {
-        const TS trtr = tot[0], trho = tot[1];
-        const int it = scal->iter + 1;
-        const double res = sqrt((double)trtr / scal->rtr0);
-        hist[it] = res;
-        int done = 0;
-        if (!isfinite((double)trtr) || !isfinite((double)trho)) {
-            scal->status = NB_BROKEDOWN;
-            done = 1;
-        } else if (res <= scal->rtol || trtr == (TS)0) {
-            scal->status = NB_CONVERGED;
-            done = 1;
-        } else if (it >= scal->max_iter) {
-            scal->status = NB_MAXITER;
-            done = 1;
-        }
-        const TS rho_old = (TS)scal->rho;
-        scal->beta = (double)(trho / rho_old);
-        scal->rho = (double)trho;
-        scal->rtr = (double)trtr;
-        scal->iter = it;
-        scal->done = done;
-        if (done && use_cond) cudaGraphSetConditional(cond, 0);
-    }
-}
-
-template <int PREC, int N>
-__global__ void __launch_bounds__(UPD_NT)
-k_init(const MeshDev m, const typename Pol<PREC>::TV *__restrict__ bvec, typename Pol<PREC>::TV *__restrict__ x,
-       typename Pol<PREC>::TV *__restrict__ pv, typename Pol<PREC>::TV *__restrict__ r,
-       typename Pol<PREC>::TV *__restrict__ z, const typename Pol<PREC>::TJ *__restrict__ dinv,
-       Scal *__restrict__ scal, const RedWs rw, double *__restrict__ hist)
-{
-    using TS = typename Pol<PREC>::TS;
-    Acc<PREC> artr, arho;
-    const int64_t np = (int64_t)m.E * N * N;
-    const int64_t p0 = split(np, gridDim.x, blockIdx.x), p1 = split(np, gridDim.x, blockIdx.x + 1);
-    for (int64_t pid = p0 + threadIdx.x; pid < p1; pid += UPD_NT)
-        init_pencil<PREC, N>(m, bvec, x, pv, r, z, dinv, pid, artr, arho);
-    __shared__ TS red[32];
-    TS v[2];
-    v[0] = block_sum<TS>(artr.value(), red);
-    v[1] = block_sum<TS>(arho.value(), red);
-    TS tot[2];
-    if (grid_reduce<TS, 2>(v, rw, tot) && threadIdx.x == 0) {
-        const TS trtr = tot[0], trho = tot[1];
-        scal->rtr0 = (double)trtr;
-        scal->rtr = (double)trtr;
-        scal->rho = (double)trho;
-        scal->beta = 0.0;
-        scal->alpha = 0.0;
-        scal->pending = 0;
-        scal->iter = 0;
-        hist[0] = 1.0;
-        if (trtr == (TS)0) {
-            scal->status = NB_CONVERGED;
-            scal->done = 1;
-            hist[0] = 0.0;
-        } else if (!isfinite((double)trtr)) {
-            scal->status = NB_BROKEDOWN;
-            scal->done = 1;
-        } else if (scal->max_iter <= 0) {
-            scal->status = NB_MAXITER;
-            scal->done = 1;
-        }
-    }
-}
-
-// the deferred x += alpha p of the last iteration
-template <int PREC>
-__global__ void __launch_bounds__(256)
-k_fin(int64_t n, typename Pol<PREC>::TV *__restrict__ x, const typename Pol<PREC>::TV *__restrict__ pv,
-      Scal *__restrict__ scal)
-{
-    using TV = typename Pol<PREC>::TV;
-    using TS = typename Pol<PREC>::TS;
-    if (!scal->pending) return;
-    const TV alpha = (TV)(TS)scal->alpha;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        x[i] = fma(alpha, pv[i], x[i]);
 }
 
 // ===========================================================================
 // launchers
 // ===========================================================================
-template <typename K>
-static int occupancy(K kern, int nt, int smem)
-{
-    int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, nt, smem);
-    return o > 0 ? o : 1;
-}
+// Per-device cache of a kernel's residency (the function attributes it depends on are
+// per device: set them and query once on every device that launches the kernel).
+struct DevCache {
+    int v[NB_MAX_DEVICES];
+    DevCache() { for (int i = 0; i < NB_MAX_DEVICES; i++) v[i] = -1; }
+    int &here()
+    {
+        int d = 0;
+        cudaGetDevice(&d);
+        return v[(d >= 0 && d < NB_MAX_DEVICES) ? d : 0];
+    }
+};
 
-template <int PREC, int N, int MODE>
+template <int PREC, int N>
 static int ax_grid_t(const nb_handle *h)
 {
     using TV = typename Pol<PREC>::TV;
     using C = AxCfg<TV, N>;
-    static int occ = -1;
+    static DevCache cache;
+    int &occ = cache.here();
     if (occ < 0) {
-        cudaFuncSetAttribute(k_ax<PREC, N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        occ = occupancy(k_ax<PREC, N, MODE>, C::NT, C::SMEM);
+        cudaFuncSetAttribute(k_ax<PREC, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_ax<PREC, N>, C::NT, C::SMEM);
+        occ = o > 0 ? o : 1;
     }
     const int64_t ngroups = (h->E + C::EPB - 1) / C::EPB;
     int64_t grid = (int64_t)h->sm_count * occ;
@@ -1299,107 +1165,30 @@ static int ax_grid_t(const nb_handle *h)
     return (int)(grid < 1 ? 1 : grid);
 }
 
-template <int PREC, int N, int MODE>
-static cudaError_t ax_launch_t(const nb_handle *h, const void *in, void *pv, void *xv, void *w, int apply_mask,
-                               Scal *scal, const RedWs &rw, cudaStream_t st)
+template <int PREC, int N>
+static cudaError_t ax_launch_t(const nb_handle *h, const void *in, void *w, int apply_mask, cudaStream_t st)
 {
     using TV = typename Pol<PREC>::TV;
     using C = AxCfg<TV, N>;
-    const int grid = ax_grid_t<PREC, N, MODE>(h);
+    const int grid = ax_grid_t<PREC, N>(h);
     const TV *g = (const TV *)(sizeof(TV) == 8 ? (const void *)h->g64 : (const void *)h->g32);
-    k_ax<PREC, N, MODE><<<grid, C::NT, C::SMEM, st>>>(h->md(), make_dmat<TV, N>(h->D), (const TV *)in, (TV *)pv,
-                                                      (TV *)xv, g, (TV *)w, apply_mask, scal, rw);
+    k_ax<PREC, N><<<grid, C::NT, C::SMEM, st>>>(h->md(), make_dmat<TV, N>(h->D), (const TV *)in, g, (TV *)w,
+                                                apply_mask);
     return cudaGetLastError();
 }
 
 template <int PREC>
 cudaError_t launch_ax_local(const nb_handle *h, const void *u, void *w, bool mask, cudaStream_t st)
 {
-    RedWs none = {nullptr, nullptr, nullptr};
-    NB_DISPATCH_N(h->n, return (ax_launch_t<PREC, NN, 0>(h, u, nullptr, nullptr, w, mask ? 1 : 0, nullptr, none, st)))
-}
-
-template <int PREC>
-int grid_k1(const nb_handle *h)
-{
-    NB_DISPATCH_N(h->n, return (ax_grid_t<PREC, NN, 1>(h) > ax_grid_t<PREC, NN, 2>(h) ? ax_grid_t<PREC, NN, 1>(h)
-                                                                                         : ax_grid_t<PREC, NN, 2>(h)))
-}
-template <int PREC>
-int grid_k2(const nb_handle *h)
-{
-    const int64_t np = h->E * h->n * h->n;
-    return grid_for(np, UPD_NT, h->sm_count, 4);
-}
-
-template <int PREC>
-cudaError_t launch_cg_init(const nb_handle *h, Workspace &ws, const void *b, cudaStream_t st)
-{
-    using TV = typename Pol<PREC>::TV;
-    using TJ = typename Pol<PREC>::TJ;
-    const TJ *dinv = (const TJ *)(sizeof(TJ) == 4 ? (const void *)h->dinv32 : (const void *)h->dinv64);
-    const int grid = grid_k2<PREC>(h);
-    NB_DISPATCH_N(h->n, (k_init<PREC, NN><<<grid, UPD_NT, 0, st>>>(h->md(), (const TV *)b, (TV *)ws.x, (TV *)ws.p,
-                                                                   (TV *)ws.r, (TV *)ws.z, dinv, ws.scal, ws.red,
-                                                                   ws.hist));
-                 break)
-    return cudaGetLastError();
-}
-
-template <int PREC>
-cudaError_t launch_cg_k1(const nb_handle *h, Workspace &ws, bool with_pap, cudaStream_t st)
-{
-    if (with_pap) {
-        NB_DISPATCH_N(h->n, return (ax_launch_t<PREC, NN, 1>(h, ws.z, ws.p, ws.x, ws.w, 1, ws.scal, ws.red, st)))
-    }
-    NB_DISPATCH_N(h->n, return (ax_launch_t<PREC, NN, 2>(h, ws.z, ws.p, ws.x, ws.w, 1, ws.scal, ws.red, st)))
-}
-
-template <int PREC>
-cudaError_t launch_cg_k2(const nb_handle *h, Workspace &ws, bool gather, cudaStream_t st,
-                         cudaGraphConditionalHandle cond, bool use_cond)
-{
-    using TV = typename Pol<PREC>::TV;
-    using TJ = typename Pol<PREC>::TJ;
-    const TJ *dinv = (const TJ *)(sizeof(TJ) == 4 ? (const void *)h->dinv32 : (const void *)h->dinv64);
-    const int grid = grid_k2<PREC>(h);
-    const int uc = use_cond ? 1 : 0;
-    if (gather) {
-        NB_DISPATCH_N(h->n, (k_upd<PREC, NN, 1><<<grid, UPD_NT, 0, st>>>(h->md(), (const TV *)ws.w, (TV *)ws.r,
-                                                                         (TV *)ws.z, dinv, ws.scal, ws.red, ws.hist,
-                                                                         cond, uc));
-                     break)
-    } else {
-        NB_DISPATCH_N(h->n, (k_upd<PREC, NN, 0><<<grid, UPD_NT, 0, st>>>(h->md(), (const TV *)ws.w, (TV *)ws.r,
-                                                                         (TV *)ws.z, dinv, ws.scal, ws.red, ws.hist,
-                                                                         cond, uc));
-                     break)
-    }
-    return cudaGetLastError();
-}
-
-template <int PREC>
-cudaError_t launch_cg_fin(const nb_handle *h, Workspace &ws, cudaStream_t st)
-{
-    using TV = typename Pol<PREC>::TV;
-    const int grid = grid_for(h->NL, 256, h->sm_count, 8);
-    k_fin<PREC><<<grid, 256, 0, st>>>(h->NL, (TV *)ws.x, (const TV *)ws.p, ws.scal);
-    return cudaGetLastError();
+    NB_DISPATCH_N(h->n, return (ax_launch_t<PREC, NN>(h, u, w, mask ? 1 : 0, st)))
 }
 
 #define NB_INSTANTIATE_CG(P)                                                                                  \
     extern template int grid_mega_var<P, 1>(const nb_handle *);                                               \
     extern template cudaError_t launch_cg_mega_var<P, 1>(const nb_handle *, const MegaArgs &, bool, cudaStream_t); \
     template cudaError_t launch_ax_local<P>(const nb_handle *, const void *, void *, bool, cudaStream_t);      \
-    template int grid_k1<P>(const nb_handle *);                                                               \
-    template int grid_k2<P>(const nb_handle *);                                                               \
     template int grid_mega<P>(const nb_handle *);                                                             \
     template int grid_mega_var<P, 0>(const nb_handle *);                                                      \
-    template cudaError_t launch_cg_init<P>(const nb_handle *, Workspace &, const void *, cudaStream_t);        \
-    template cudaError_t launch_cg_k1<P>(const nb_handle *, Workspace &, bool, cudaStream_t);                 \
-    template cudaError_t launch_cg_k2<P>(const nb_handle *, Workspace &, bool, cudaStream_t,                  \
-                                         cudaGraphConditionalHandle, bool);                                   \
-    template cudaError_t launch_cg_fin<P>(const nb_handle *, Workspace &, cudaStream_t);                      \
     template cudaError_t launch_cg_mega<P>(const nb_handle *, Workspace &, const void *, int, int, double,    \
                                            int, int, unsigned long long *, cudaStream_t);                     \
     template cudaError_t launch_cg_mega_var<P, 0>(const nb_handle *, const MegaArgs &, bool, cudaStream_t);

@@ -335,61 +335,6 @@ __device__ __forceinline__ T block_sum(T v, T *sh)
     return r;
 }
 
-// Two-level deterministic grid reduction of K values (H4 of SURVEY.md §7): block partials
-// -> per-chunk (256 blocks) partial, reduced by the chunk's last block to finish -> total,
-// reduced by the last chunk reducer.  Every sum runs in a fixed index order, so results are
-// bit-reproducible; no floating-point atomics.  Counters self-reset.  Call from every
-// thread of every block; v valid in thread 0.  Returns true in all threads of the single
-// block that holds the total (valid in thread 0).
-constexpr int RED_CHUNK = 256;
-template <typename TS, int K>
-__device__ __forceinline__ bool grid_reduce(const TS (&v)[K], const RedWs &rw, TS (&tot)[K])
-{
-    __shared__ TS sh[32];
-    __shared__ int flag;
-    const int nblk = gridDim.x;
-    const int b = blockIdx.x;
-    const int chunk = b / RED_CHUNK;
-    const int nchunk = (nblk + RED_CHUNK - 1) / RED_CHUNK;
-    const int csz = min(RED_CHUNK, nblk - chunk * RED_CHUNK);
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int k = 0; k < K; k++) rw.part[(size_t)b * K + k] = (double)v[k];
-        __threadfence();
-        const uint32_t prev = atomicAdd(&rw.cnt[1 + chunk], 1u);
-        flag = (prev == (uint32_t)(csz - 1));
-    }
-    __syncthreads();
-    if (!flag) return false;
-    __threadfence();
-    TS c[K];
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        TS s = 0;
-        for (int i = threadIdx.x; i < csz; i += blockDim.x) s += (TS)__ldcg(rw.part + (size_t)(chunk * RED_CHUNK + i) * K + k);
-        c[k] = block_sum<TS>(s, sh);
-    }
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int k = 0; k < K; k++) rw.part2[(size_t)chunk * K + k] = (double)c[k];
-        rw.cnt[1 + chunk] = 0;
-        __threadfence();
-        const uint32_t prev = atomicAdd(&rw.cnt[0], 1u);
-        flag = (prev == (uint32_t)(nchunk - 1));
-    }
-    __syncthreads();
-    if (!flag) return false;
-    __threadfence();
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        TS s = 0;
-        for (int i = threadIdx.x; i < nchunk; i += blockDim.x) s += (TS)__ldcg(rw.part2 + (size_t)i * K + k);
-        tot[k] = block_sum<TS>(s, sh);
-    }
-    if (threadIdx.x == 0) rw.cnt[0] = 0;
-    return true;
-}
-
 // ---------------------------------------------------------------------------
 // counter-based SplitMix64; the CUDA path's own implementation
 // ---------------------------------------------------------------------------

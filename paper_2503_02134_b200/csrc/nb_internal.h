@@ -28,6 +28,7 @@ struct Scal {
 
 // Multi-rank (z-slab) solves: ranks per solve, slabs per launch (one GPU)
 constexpr int NB_MAX_RANKS = 8;
+constexpr int NB_MAX_DEVICES = 64;   // per-device caches of kernel residency
 constexpr int NB_MAX_LOCAL = 4;
 // per-rank control block (peer-visible): arrival flag, then rank-partial slots
 // [2 parities][NB_MAX_RANKS][4 doubles] (K <= 2 accumulators x W <= 2 doubles)
@@ -41,13 +42,6 @@ struct PeerState {
     uint32_t epoch = 0;                // cross-rank barrier epochs completed by earlier solves
     void *opened[NB_MAX_RANKS + 2] = {};   // IPC mappings to close
     int nopened = 0;
-};
-
-// Scratch of the deterministic two-level grid reductions (nb_common.cuh grid_reduce).
-struct RedWs {
-    double *part;      // [max_blocks * 2]
-    double *part2;     // [max_chunks * 2]
-    uint32_t *cnt;     // [1 + max_chunks], zero, self-resetting
 };
 
 // Geometry needed by kernels, passed by value.
@@ -72,6 +66,7 @@ struct MegaArgs {
     int32_t max_iter;
     double rtol;
     double *hist;           // [max_iter + 1]
+    double *shist;          // nullable: [3 * max_iter] rho_k, alpha_k, beta_k (block 0)
     unsigned long long *tim;  // nullable: [3 * (max_iter + 1)] globaltimer stamps (block 0)
     double *partA, *partS, *partB;   // per-block partials, [G], [G], [2G] (x Acc::W)
     int32_t pc;             // nb_precond (z aliases r for the identity)
@@ -108,18 +103,16 @@ struct Workspace {          // per-policy CG workspace (lazily allocated)
     double *xd = nullptr;       // x accumulated in double (x_fp64 option), lazily allocated
     unsigned char *ctl = nullptr;   // multi-rank control block (NB_CTL_BYTES), lazily allocated
     PeerState peer;
-    RedWs red = {nullptr, nullptr, nullptr};
+    double *part = nullptr;     // megakernel per-block partials
     Scal *scal = nullptr;       // device scalars
     Scal *scal_host = nullptr;  // pinned mirror
     double *hist = nullptr;     // device history, capacity hist_cap
+    double *shist = nullptr;    // device scalar history [3 * hist_cap] (rho, alpha, beta)
     int32_t hist_cap = 0;
     // megakernel: grid size, barrier words [2], globaltimer stamps [3 * hist_cap]
     int32_t mega_G = 0;
     unsigned int *bar = nullptr;
     unsigned long long *tim = nullptr;
-    // conditional-while graph cache (one per gs order)
-    cudaGraph_t graph[2] = {nullptr, nullptr};
-    cudaGraphExec_t exec[2] = {nullptr, nullptr};
 };
 
 }  // namespace nb
@@ -146,9 +139,8 @@ struct nb_handle {
     int32_t *gs_off = nullptr;  // [nseg+1]
     int32_t *gs_idx = nullptr;  // [ncopies]
     int32_t *flag = nullptr;    // device error flags for setup checks
-    cudaStream_t cap_stream = nullptr;   // private stream used for graph capture / setup
+    cudaStream_t cap_stream = nullptr;   // private stream used for setup
     int cg_csr = 0;             // 1: consistent-order CG also through the CSR dssum kernel (A/B)
-    int cg_graph = 0;           // 1: per-phase kernels in a CUDA graph instead of the megakernel
     nb::Workspace ws[4];   // one per nb_policy
     nb::MeshDev md() const {
         nb::MeshDev m;
@@ -177,21 +169,9 @@ cudaError_t launch_rhs(const nb_handle *h, int kind, double noise, uint64_t seed
 // ---- CSR gather-scatter (nb_gs.cu) ----
 int grid_gs(const nb_handle *h);
 cudaError_t launch_dssum(const nb_handle *h, int prec, int order, void *u, cudaStream_t st);
-// CG K2 (per-copy path, or consistent with cg_csr): w <- QQ^T w, pap partials, alpha finalize
-cudaError_t launch_cg_gs(const nb_handle *h, int prec, int order, Workspace &ws, cudaStream_t st);
 
 // ---- Ax + CG kernels, one translation unit per policy (nb_cg_<policy>.cu) ----
 template <int PREC> cudaError_t launch_ax_local(const nb_handle *h, const void *u, void *w, bool mask, cudaStream_t st);
-template <int PREC> int grid_k1(const nb_handle *h);
-template <int PREC> int grid_k2(const nb_handle *h);
-template <int PREC> cudaError_t launch_cg_init(const nb_handle *h, Workspace &ws, const void *b, cudaStream_t st);
-// K1: p = z + beta p; x += alpha_prev p_old; w = mask A_L p; (with_pap) pap + alpha finalize
-template <int PREC> cudaError_t launch_cg_k1(const nb_handle *h, Workspace &ws, bool with_pap, cudaStream_t st);
-// K2': (gather) w <- QQ^T w on the fly; r -= alpha w; z = M^-1 r; rtr, rho; beta/status finalize
-template <int PREC> cudaError_t launch_cg_k2(const nb_handle *h, Workspace &ws, bool gather, cudaStream_t st,
-                                            cudaGraphConditionalHandle cond, bool use_cond);
-// deferred x += alpha p of the last iteration
-template <int PREC> cudaError_t launch_cg_fin(const nb_handle *h, Workspace &ws, cudaStream_t st);
 // the whole solve as one persistent cooperative kernel (grid size: grid_mega)
 template <int PREC> int grid_mega(const nb_handle *h);
 struct MegaArgs;

@@ -13,7 +13,7 @@ namespace nb {
 
 // Shared-memory carve-out: just what the resident blocks need, the rest of the 256 KB stays L1
 // (phase B's neighbour-copy loads hit in L1).  NB_CARVEOUT=0 leaves the driver's choice.
-static void set_carveout(const void *fn, int occ, int smem)
+static void set_carveout(const void *fn, int occ, int smem)   // called once per device and kernel
 {
     static int mode = -1;
     if (mode < 0) {
@@ -32,7 +32,8 @@ static int mega_grid_t(const nb_handle *h)
 {
     using C = AxCfg<typename Pol<PREC>::TV, N>;
     const void *fn = (const void *)k_cg_mega<PREC, N, FUSED, VAR>;
-    static int occ = -1;
+    static DevCache cache;   // the attributes and the residency are per device
+    int &occ = cache.here();
     if (occ < 0) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         int o = 0;
@@ -124,10 +125,10 @@ void fill_mega_args(const nb_handle *h, Workspace &ws, const void *b, int order,
                                                                                   : (const void *)h->dinv64;
     A.gs_off = h->gs_off; A.gs_idx = h->gs_idx; A.nseg = (int32_t)h->nseg;
     A.order = order; A.max_iter = max_iter; A.rtol = rtol;
-    A.hist = ws.hist; A.tim = tim;
+    A.hist = ws.hist; A.shist = ws.shist; A.tim = tim;
     // per-block partials: W doubles per accumulator (2 for the Dot2 expansions)
     const size_t W = (size_t)Acc<PREC>::W;
-    A.partA = ws.red.part; A.partS = ws.red.part + W * ws.mega_G; A.partB = ws.red.part + 2 * W * ws.mega_G;
+    A.partA = ws.part; A.partS = ws.part + W * ws.mega_G; A.partB = ws.part + 2 * W * ws.mega_G;
     A.bar = ws.bar;
     A.scal = ws.scal;
     A.wlo = ws.peer.wlo;
@@ -153,7 +154,8 @@ template <int PREC, int N>
 static int mr_occupancy()
 {
     using C = AxCfg<typename Pol<PREC>::TV, N>;
-    static int occ = -1;
+    static DevCache cache;
+    int &occ = cache.here();
     if (occ < 0) {
         const void *fn = (const void *)k_cg_mega_mr<PREC, N>;
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);

@@ -184,14 +184,16 @@ def test_cg_stagnation_per_copy(box8):
     assert rm.status == nb.NB_CONVERGED and abs(rm.iterations - r64.iterations) <= 0.05 * r64.iterations
 
 
-def test_cg_timed_mode_matches_graph_mode(box8):
+def test_cg_repeat_is_bit_identical_and_phase_timed(box8):
+    """Two solves of the same system give bit-identical x (fixed-order reductions) and the
+    megakernel's per-phase globaltimer stamps are reported."""
     g, o, ref = box8
     b = g.rhs(nb.NB_MIXED, seed=0)
     x1, r1 = g.cg(b, nb.NB_MIXED, max_iter=1200, rtol=1e-8)
-    x2, r2 = g.cg(b, nb.NB_MIXED, max_iter=1200, rtol=1e-8, time_kernels=True)
+    x2, r2 = g.cg(b, nb.NB_MIXED, max_iter=1200, rtol=1e-8)
     assert r1.iterations == r2.iterations
     assert torch.equal(x1, x2)                             # deterministic reductions
-    assert r2.k_ax_ms > 0 and r2.k_upd_ms > 0
+    assert r2.k_ax_ms > 0 and r2.k_upd_ms > 0 and r2.kernel_launches == 1
 
 
 def test_cg_host_buffers(box8):
@@ -218,9 +220,8 @@ def test_cg_csr_path_matches_fused(box8, monkeypatch):
         assert r1.status == r2.status == nb.NB_CONVERGED
         assert abs(r1.iterations - r2.iterations) <= 2
         assert rel_l2(x1.cpu().numpy(), x2.cpu().numpy()) <= (1e-9 if pol == nb.NB_FP64 else 1e-6)
-        # megakernel driver: one launch per solve; graph driver: init + per-iteration kernels + fin
-        assert r2.kernel_launches in (1, 1 + 3 * r2.iterations + 1)
-        assert r1.kernel_launches in (1, 1 + 2 * r1.iterations + 1)
+        # one megakernel launch per solve (the CSR path runs as an in-kernel phase)
+        assert r1.kernel_launches == 1 and r2.kernel_launches == 1
     gc.close()
 
 

@@ -28,7 +28,7 @@ order = nb.NB_GS_CONSISTENT if a.gs == "consistent" else nb.NB_GS_PER_COPY
 m = nb.Mesh(*a.nel, a.p, deform=a.deform)
 b = m.rhs(pol, seed=0)
 x = m.empty(pol)
-rep, _ = nb.nb_cg(m.h, b, x, pol, a.iters, 0.0, gs_order=order, time_kernels=True)
+rep, _ = nb.nb_cg(m.h, b, x, pol, a.iters, 0.0, gs_order=order)
 print(f"iters={rep.iterations} k1={1e3 * rep.k_ax_ms / rep.iterations:.2f}us gs={1e3 * rep.k_gs_ms / rep.iterations:.2f}us "
       f"k2={1e3 * rep.k_upd_ms / rep.iterations:.2f}us")
 w = m.empty(pol)
