@@ -31,15 +31,16 @@ template <int PREC, int N, int FUSED, int VAR>
 static int mega_grid_t(const nb_handle *h)
 {
     using C = AxCfg<typename Pol<PREC>::TV, N>;
+    constexpr int SMEM_MEGA = StageB<PREC, N>::MEGA_SMEM;
     const void *fn = (const void *)k_cg_mega<PREC, N, FUSED, VAR>;
     static DevCache cache;   // the attributes and the residency are per device
     int &occ = cache.here();
     if (occ < 0) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MEGA);
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, C::NT, C::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, C::NT, SMEM_MEGA);
         occ = o > 0 ? o : 1;
-        set_carveout(fn, occ, C::SMEM);
+        set_carveout(fn, occ, SMEM_MEGA);
     }
     return h->sm_count * occ;
 }
@@ -79,6 +80,7 @@ static cudaError_t mega_launch_t(const nb_handle *h, const MegaArgs &args, cudaS
 {
     using TV = typename Pol<PREC>::TV;
     using C = AxCfg<TV, N>;
+    constexpr int SMEM_MEGA = StageB<PREC, N>::MEGA_SMEM;
     DMat<TV, N> D = make_dmat<TV, N>(h->D);
     void *params[2] = {(void *)&args, (void *)&D};
     int grid = mega_grid_t<PREC, N, FUSED, VAR>(h);
@@ -100,7 +102,7 @@ static cudaError_t mega_launch_t(const nb_handle *h, const MegaArgs &args, cudaS
             grid = (int)g;
     }
     return cudaLaunchCooperativeKernel((const void *)k_cg_mega<PREC, N, FUSED, VAR>, dim3(grid), dim3(C::NT), params,
-                                       (size_t)C::SMEM, st);
+                                       (size_t)SMEM_MEGA, st);
 }
 
 template <int PREC, int VAR>
@@ -154,13 +156,14 @@ template <int PREC, int N>
 static int mr_occupancy()
 {
     using C = AxCfg<typename Pol<PREC>::TV, N>;
+    constexpr int SMEM_MEGA = StageB<PREC, N>::MEGA_SMEM;
     static DevCache cache;
     int &occ = cache.here();
     if (occ < 0) {
         const void *fn = (const void *)k_cg_mega_mr<PREC, N>;
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MEGA);
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, C::NT, C::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, C::NT, SMEM_MEGA);
         occ = o > 0 ? o : 1;
     }
     return occ;
@@ -177,11 +180,12 @@ static cudaError_t mr_launch_t(const nb_handle *h, const MultiArgs &M, cudaStrea
 {
     using TV = typename Pol<PREC>::TV;
     using C = AxCfg<TV, N>;
+    constexpr int SMEM_MEGA = StageB<PREC, N>::MEGA_SMEM;
     DMat<TV, N> D = make_dmat<TV, N>(h->D);
     void *params[2] = {(void *)&M, (void *)&D};
     (void)mr_occupancy<PREC, N>();
     return cudaLaunchCooperativeKernel((const void *)k_cg_mega_mr<PREC, N>, dim3(M.mr.nloc * M.mr.Gr), dim3(C::NT),
-                                       params, (size_t)C::SMEM, st);
+                                       params, (size_t)SMEM_MEGA, st);
 }
 
 template <int PREC>
