@@ -47,6 +47,7 @@ SJ = {0: 8, 1: 4, 2: 8}          # dinv entry
 K1_BYTES = {p: 3 * SV[p] + 6 * SV[p] + 3 * SV[p] for p in SV}
 K2_BYTES = {p: 2 * SV[p] + SJ[p] + 2 * SV[p] for p in SV}
 AX_BYTES = {p: 2 * SV[p] + 6 * SV[p] for p in SV}     # standalone local Ax: u + 6 g -> w
+ROOF_ITERS = 200                                       # fixed iterations of the configs[2] roofline launch
 
 
 def load_peaks():
@@ -274,8 +275,6 @@ def time_launches(fn, n, stream):
     """Device time (ms) of one fn() launch, median over n.  Each launch is bracketed by CUDA
     events queued behind a short GPU sleep, so the host work of the ctypes call (argument checks,
     pointer queries) is absorbed by the sleep and the events time the kernel alone."""
-    import statistics
-
     import torch
     fn()
     torch.cuda.synchronize()
@@ -291,6 +290,155 @@ def time_launches(fn, n, stream):
     return statistics.median(ts)
 
 
+def survey_bytes(pol, info):
+    """SURVEY.md §8(d) algorithmic bytes per local DOF and CG iteration of the fused iteration
+    K1 + K2 + K3 (every vector, g and dinv entry at its policy precision, c as a vector, int32 CSR
+    indices for the shared copies), evaluated with the mesh's own shared fractions."""
+    sv, sj = SV[pol], SJ[pol]
+    NL = info.n_local
+    f_sh, f_g = info.n_shared_copies / NL, info.n_shared_global / NL
+    k1 = 2 * sv + sj + 6 * sv + 2 * sv          # K1: r, dinv, p_old, 6 g -> p, w          (88 / 48 / 44)
+    k2 = f_sh * (2 * sv + 4) + f_g * 4 + f_g * sv   # K2: dssum (copies + int32 idx + offsets) + shared pap
+    k3 = 6 * sv + sj + sv                       # K3: x, p, r, w, dinv, c -> x, r          (64 / 36 / 32)
+    return k1 + k2 + k3
+
+
+def impl_bytes(pol):
+    """Bytes per local DOF and iteration this implementation moves: phase A
+    z, p_old, x, 6 g -> p, x, w; phase B w, r, dinv -> r, z; c and the mask are analytic."""
+    return K1_BYTES[pol] + K2_BYTES[pol]
+
+
+def roofline_point(nb, args, flush, dev, cfg_name="configs[2]"):
+    """The HBM-bound roofline measurement: the CG megakernel on configs[2] (32^3 deformed, p = 9,
+    32.8M local DOF, ~2.4 GB/iteration of mixed traffic: 19x the 126 MB L2), `ROOF_ITERS` fixed
+    iterations in one launch, timed with CUDA events on the launching stream; per-phase time from
+    the kernel's own %globaltimer stamps.  DRAM traffic of the same launch from the committed ncu
+    capture (profiles/r2_ncu_roofline.json, tools/ncu_roofline.sh)."""
+    import torch
+    st = torch.cuda.current_stream()
+    m = nb.Mesh(32, 32, 32, 9, deform=0.1, seed=0, device=dev)
+    info, NL = m.info, m.n_local
+    peak, peak_src = load_peaks()
+    traffic = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_ncu_roofline.json")) as f:
+            traffic = json.load(f)
+    except Exception:
+        pass
+    out = {"workload": "configs[2]: box 32x32x32 deformed 0.1, p=9, uniform RHS seed 0, "
+                       f"{ROOF_ITERS} fixed CG iterations in one k_cg_mega launch", "n_local": NL,
+           "l2": "working set 19x the L2 (mixed); 256 MiB flush before each launch", "policies": {}}
+    for name in args.roof_policies:
+        pol = POLICIES[name]
+        b = m.rhs(pol, nb.NB_RHS_UNIFORM, seed=0)
+        x = m.empty(pol)
+        nb.nb_cg(m.h, b, x, pol, ROOF_ITERS, 0.0, history=False)      # warm-up (and the ncu target)
+        if args.roofline_only:
+            break
+        best = None
+        for _ in range(3):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            rep, _ = nb.nb_cg(m.h, b, x, pol, ROOF_ITERS, 0.0, history=False)
+            e1.record(st)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            if best is None or ms < best[0]:
+                best = (ms, rep)
+        ms, rep = best
+        it = rep.iterations
+        sb, ib = survey_bytes(pol, info), impl_bytes(pol)
+        a_us, b_us = 1e3 * rep.k_ax_ms / it, 1e3 * rep.k_upd_ms / it
+        tr = traffic.get(f"configs2_{name}")
+        rec = {"launch_ms": ms, "iterations": it, "dof_iter_per_s": NL * it / (ms * 1e-3),
+               "survey_bytes_per_dof_iter": sb, "impl_bytes_per_dof_iter": ib,
+               "achieved_GBps": sb * NL * it / (ms * 1e-3) / 1e9,
+               "achieved_impl_GBps": ib * NL * it / (ms * 1e-3) / 1e9,
+               "phaseA_us": a_us, "phaseB_us": b_us,
+               "phaseA_GBps": K1_BYTES[pol] * NL / (a_us * 1e-6) / 1e9,
+               "phaseB_GBps": K2_BYTES[pol] * NL / (b_us * 1e-6) / 1e9}
+        rec["phaseA_frac"] = rec["phaseA_GBps"] / peak
+        rec["phaseB_frac"] = rec["phaseB_GBps"] / peak
+        if tr:
+            rec["ncu_dram_bytes_per_iteration"] = tr.get("dram_bytes_per_iteration")
+            rec["ncu_dram_bytes_per_launch"] = tr.get("dram_bytes_per_iteration", 0) * it
+            rec["ncu_dram_GBps_at_this_launch_time"] = rec["ncu_dram_bytes_per_launch"] / (ms * 1e-3) / 1e9
+            for ph in ("A", "B"):
+                if tr.get(f"phase{ph}_dram_bytes_per_iteration"):
+                    rec[f"ncu_phase{ph}_dram_bytes_per_iteration"] = tr[f"phase{ph}_dram_bytes_per_iteration"]
+                    us = a_us if ph == "A" else b_us
+                    rec[f"ncu_phase{ph}_dram_frac"] = tr[f"phase{ph}_dram_bytes_per_iteration"] / (us * 1e-6) / 1e9 / peak
+            rec["ncu_source"] = tr.get("source")
+        # standalone operators at this HBM-bound size (the metric's "Ax/dssum HBM GB/s")
+        u = m.rhs(pol, nb.NB_RHS_UNIFORM, seed=5)
+        w = m.empty(pol)
+        ax_ms = time_launches(lambda: nb.nb_ax(m.h, pol, u, w, nb.NB_AX_LOCAL), 10, st)
+        gs_ms = time_launches(lambda: nb.nb_dssum(m.h, pol, nb.NB_GS_CONSISTENT, w), 10, st)
+        gs_bytes = info.n_shared_copies * (2 * SV[pol] + 4) + (info.n_shared_global + 1) * 4
+        rec["nb_ax_local"] = {"us": 1e3 * ax_ms, "alg_bytes": AX_BYTES[pol] * NL,
+                              "GBps": AX_BYTES[pol] * NL / (ax_ms * 1e-3) / 1e9,
+                              "frac": AX_BYTES[pol] * NL / (ax_ms * 1e-3) / 1e9 / peak}
+        rec["nb_dssum"] = {"us": 1e3 * gs_ms, "alg_bytes": gs_bytes, "GBps": gs_bytes / (gs_ms * 1e-3) / 1e9,
+                           "frac": gs_bytes / (gs_ms * 1e-3) / 1e9 / peak}
+        out["policies"][name] = rec
+        del b, x, u, w
+    m.close()
+    torch.cuda.empty_cache()
+    return out, peak, peak_src
+
+
+def spawn(args):
+    """--gpus N without a torchrun environment: relaunch this script under torch.distributed.run
+    with N local ranks (127.0.0.1 rendezvous) and pass its output through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """--dry-run: the multi-rank plumbing only (CPU, gloo): every rank joins, rank 0 prints the
+    line's shape with n_gpus = world size.  Used by the CPU tests of --gpus N spawning."""
+    import torch.distributed as dist
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        dist.init_process_group("gloo")
+        dist.barrier()
+    mode = args.mode or ("slab" if world > 1 else "single")
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "mode": mode,
+                          "parallelism": parallelism(mode, world, 0)}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def parallelism(mode, world, nslab_local):
+    if mode == "slab" and world > 1:
+        return f"z-slabs over {world} GPUs (NVLink peer memory, in-kernel exchange)"
+    if nslab_local:
+        return f"{nslab_local} z-slabs in one launch on one GPU"
+    if world > 1:
+        return f"replicas over {world} GPUs"
+    return "single GPU"
+
+
+def ae_mae(h_m, h_d):
+    """PAPER.md:489-497 (Sec. 5.1.1): AE_i = |r_m,i - r_d,i| of the residual histories of the mixed
+    and the double-precision solve, MAE = mean over the common iterations."""
+    import numpy as np
+    n = min(len(h_m), len(h_d))
+    ae = np.abs(np.asarray(h_m[1:n]) - np.asarray(h_d[1:n]))
+    return {"iterations_compared": int(n - 1), "MAE": float(ae.mean()) if ae.size else 0.0,
+            "AE_max": float(ae.max()) if ae.size else 0.0, "AE_final": float(ae[-1]) if ae.size else 0.0,
+            "AE_at": {str(k): float(ae[k - 1]) for k in (1, 10, 100, 300) if k <= ae.size}}
+
+
 def run_ours(args):
     import torch
     import paper_2503_02134_b200 as nb
@@ -300,10 +448,13 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     pol = POLICIES[args.policy]
     nel, p = list(WORKLOAD["nel"]), WORKLOAD["p"]
-    slab = args.mode == "slab"
+    mode = args.mode or ("slab" if world > 1 else "single")
     group = []
-    if slab:
-        args.quick = True        # the per-policy table / companion run on rank 0 alone
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+    if args.roofline_only:
+        roofline_point(nb, args, flush, dev)
+        return 0
+    if mode == "slab":
         if world > 1:
             nel[2] = WORKLOAD["nel"][2] * world          # configs[1] per GPU, stacked along z
             mesh = nb.Mesh(*nel, p, deform=0.0, seed=0, device=dev, slab=nb.slab_bounds(nel[2], world, rank))
@@ -316,12 +467,10 @@ def run_ours(args):
     else:
         mesh = nb.Mesh(*nel, p, deform=0.0, seed=0, device=dev)
     NL = sum(m.n_local for m in group) if group else mesh.n_local
-    info = mesh.info
     b = mesh.rhs(pol, nb.NB_RHS_UNIFORM, seed=0)
     x = mesh.empty(pol)
     gb = [m.rhs(pol, nb.NB_RHS_UNIFORM, seed=0) for m in group]
     gx = [m.empty(pol) for m in group]
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
     max_iter = 4000
     st = torch.cuda.current_stream()
 
@@ -354,30 +503,9 @@ def run_ours(args):
     step_ms = [a.elapsed_time(b2) for a, b2 in ev]
     t_local = sum(step_ms) / 1e3
     value, t_max = aggregate(NL * sum(iters), t_local, world)
-
-    # per-phase device time of the same solve: the megakernel's block 0 stamps %globaltimer after
-    # every grid barrier (nb_cg_report k_ax_ms / k_upd_ms)
-    kt = [solve() for _ in range(max(1, min(args.steps, 3)))]
-    it_k = sum(r.iterations for r in kt)
-    k1_ms = sum(r.k_ax_ms for r in kt) / it_k
-    k2_ms = sum(r.k_upd_ms for r in kt) / it_k
-    peak, peak_src = load_peaks()
-    vs = SV[pol]
-    k1_bytes = K1_BYTES[pol] * NL
-    k2_bytes = K2_BYTES[pol] * NL
-    # standalone operator pieces (the metric's "Ax/dssum HBM GB/s"): local Ax and the CSR dssum
-    u = mesh.rhs(pol, nb.NB_RHS_UNIFORM, seed=5)
-    wv = mesh.empty(pol)
-    ax_ms = time_launches(lambda: nb.nb_ax(mesh.h, pol, u, wv, nb.NB_AX_LOCAL), 50, st)
-    gs_ms = time_launches(lambda: nb.nb_dssum(mesh.h, pol, nb.NB_GS_CONSISTENT, wv), 50, st)
-    gs_bytes = info.n_shared_copies * (2 * vs + 4) + (info.n_shared_global + 1) * 4
-    # DRAM traffic of the solve kernel from the committed ncu capture (profiles/), per iteration
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(f"{args.policy}_configs1_dram_bytes_per_iteration")
-    except Exception:
-        pass
+    # per-phase device time of the timed solve (block 0's %globaltimer stamps after each barrier)
+    kt = solve()
+    k1_us, k2_us = 1e3 * kt.k_ax_ms / kt.iterations, 1e3 * kt.k_upd_ms / kt.iterations
 
     # e2e: the public host-buffer call, pinned host b/x, copies inside the timed region
     e2e = None
@@ -397,50 +525,33 @@ def run_ours(args):
         e2e_val = sum_over_ranks(float(NL * e2e_it), world) / e2e_t
         e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": NL * SV[pol], "d2h_bytes_per_step": NL * SV[pol]}
 
-    # time-to-1e-8 for every policy (reported next to the headline; not the timed region)
+    # time-to-1e-8 for every policy on the headline workload, and AE/MAE
     ttr = {}
-    if rank == 0 and not args.quick:
+    companions = rank == 0 and world == 1 and not group and not args.quick
+    if companions:
+        hists = {}
         for name, pp in POLICIES.items():
             bb = mesh.rhs(pp, nb.NB_RHS_UNIFORM, seed=0)
             xx = mesh.empty(pp)
             reps = []
             for _ in range(3):
                 flush.zero_()
-                r, _ = nb.nb_cg(mesh.h, bb, xx, pp, max_iter, WORKLOAD["rtol"], history=False)
+                r, hh = nb.nb_cg(mesh.h, bb, xx, pp, max_iter, WORKLOAD["rtol"], history=True)
                 reps.append(r)
-            rk, _ = nb.nb_cg(mesh.h, bb, xx, pp, max_iter, WORKLOAD["rtol"], history=False)
-            n_it = rk.iterations
+            hists[name] = hh
             tmed = statistics.median(r.solve_ms for r in reps)
-            ttr[name] = {"iterations": reps[-1].iterations, "status": reps[-1].status, "time_ms": tmed,
-                         "dof_iter_per_s": NL * reps[-1].iterations / (tmed * 1e-3),
-                         "k1_us": 1e3 * rk.k_ax_ms / n_it, "k2_us": 1e3 * rk.k_upd_ms / n_it,
-                         "k1_alg_GBps": K1_BYTES[pp] * NL / (rk.k_ax_ms * 1e-3 / n_it) / 1e9,
-                         "k2_alg_GBps": K2_BYTES[pp] * NL / (rk.k_upd_ms * 1e-3 / n_it) / 1e9}
+            rk = reps[-1]
+            ttr[name] = {"iterations": rk.iterations, "status": rk.status, "time_ms": tmed,
+                         "dof_iter_per_s": NL * rk.iterations / (tmed * 1e-3),
+                         "phaseA_us": 1e3 * rk.k_ax_ms / rk.iterations, "phaseB_us": 1e3 * rk.k_upd_ms / rk.iterations}
         ttr["speedup_fp64_over_mixed_time"] = ttr["fp64"]["time_ms"] / ttr["mixed"]["time_ms"]
+        ttr["accuracy_AE_MAE_mixed_vs_fp64"] = ae_mae(hists["mixed"], hists["fp64"])
+        ttr["accuracy_AE_MAE_fp32_vs_fp64"] = ae_mae(hists["fp32"], hists["fp64"])
 
-    # HBM-bound companion point: configs[1]'s working set (~100 MB mixed) fits in the 126 MB L2,
-    # so its phase GB/s are not an HBM measurement.  configs[2] (32^3, p=9, deformed, 32.8M DOF,
-    # ~1.6 GB per mixed iteration) is: fixed 100 iterations, phase times from the same stamps.
-    large = None
-    if rank == 0 and not args.quick and not args.no_large:
-        lm = nb.Mesh(32, 32, 32, 9, deform=0.1, seed=0, device=dev)
-        lnl = lm.n_local
-        large = {"workload": "configs[2]: box 32x32x32 deformed 0.1, p=9, uniform RHS seed 0, 100 fixed iterations"}
-        for name, pp in (("mixed", POLICIES["mixed"]), ("fp64", POLICIES["fp64"])):
-            lb = lm.rhs(pp, nb.NB_RHS_UNIFORM, seed=0)
-            lx = lm.empty(pp)
-            nb.nb_cg(lm.h, lb, lx, pp, 100, 0.0, history=False)
-            flush.zero_()
-            r, _ = nb.nb_cg(lm.h, lb, lx, pp, 100, 0.0, history=False)
-            a_us, b_us = 1e3 * r.k_ax_ms / r.iterations, 1e3 * r.k_upd_ms / r.iterations
-            large[name] = {"us_per_iteration": 1e3 * r.solve_ms / r.iterations,
-                           "dof_iter_per_s": lnl * r.iterations / (r.solve_ms * 1e-3),
-                           "phaseA_us": a_us, "phaseA_GBps": K1_BYTES[pp] * lnl / (a_us * 1e-6) / 1e9,
-                           "phaseA_frac": K1_BYTES[pp] * lnl / (a_us * 1e-6) / 1e9 / load_peaks()[0],
-                           "phaseB_us": b_us, "phaseB_GBps": K2_BYTES[pp] * lnl / (b_us * 1e-6) / 1e9,
-                           "phaseB_frac": K2_BYTES[pp] * lnl / (b_us * 1e-6) / 1e9 / load_peaks()[0]}
-            del lb, lx
-        lm.close()
+    # the HBM roofline point (configs[2]); configs[1] above is L2-resident
+    roof, peak, peak_src = None, None, None
+    if companions and not args.no_large:
+        roof, peak, peak_src = roofline_point(nb, args, flush, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -451,44 +562,40 @@ def run_ours(args):
 
     if rank == 0:
         ms_per_step = 1e3 * t_max / args.steps
-        k1_ach = k1_bytes / (k1_ms * 1e-3) / 1e9
-        k2_ach = k2_bytes / (k2_ms * 1e-3) / 1e9
+        roofline = None
+        if roof:
+            r = roof["policies"][args.policy if args.policy in roof["policies"] else "mixed"]
+            roofline = {"bound": "hbm", "kernel": "k_cg_mega (the whole CG solve: phase A p-update + x + local Ax "
+                                                   "+ pap, phase B gather-scatter + r/z update + dots)",
+                        "workload": roof["workload"], "policy": args.policy,
+                        "achieved": r["achieved_GBps"], "peak": peak, "unit": "GB/s",
+                        "frac": r["achieved_GBps"] / peak,
+                        "traffic": r.get("ncu_dram_bytes_per_launch"),
+                        "achieved_note": "SURVEY.md §8(d) fused-iteration bytes per DOF "
+                                         f"({r['survey_bytes_per_dof_iter']:.1f} B at this mesh's shared fractions) x "
+                                         f"n_local x iterations / launch time (CUDA events on the launching stream)",
+                        "achieved_impl_bytes": r["achieved_impl_GBps"], "frac_impl_bytes": r["achieved_impl_GBps"] / peak,
+                        "ncu_dram_GBps": r.get("ncu_dram_GBps_at_this_launch_time"),
+                        "ncu_dram_frac": (r["ncu_dram_GBps_at_this_launch_time"] / peak
+                                          if r.get("ncu_dram_GBps_at_this_launch_time") else None),
+                        "alg_bytes_per_launch": r["survey_bytes_per_dof_iter"] * roof["n_local"] * r["iterations"],
+                        "avg_launch_us": 1e3 * r["launch_ms"], "peak_source": peak_src,
+                        "ncu_source": r.get("ncu_source")}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": {0: "f64", 1: "f32", 2: "f32+f64 (mixed)"}[pol],
                 "data": "synthetic",
                 "config": dict(WORKLOAD, policy=args.policy, iterations=iters[0], status=sorted(statuses),
-                               n_local=NL, l2="256 MiB write between steps (outside the step events)",
-                               parallelism=(f"z-slabs over {world} GPUs (NVLink peer memory)" if slab and world > 1
-                                            else f"{len(group)} z-slabs in one launch on one GPU" if group
-                                            else "replicas" if world > 1 else "single GPU"),
-                               **({"nel": nel} if slab else {})),
+                               n_local=NL, l2="256 MiB write between steps (outside the step events); "
+                                              "configs[1]'s working set (~100 MB mixed) is L2-resident: "
+                                              "throughput and time only, the HBM roofline is taken on configs[2]",
+                               parallelism=parallelism(mode, world, len(group)), mode=mode,
+                               **({"nel": nel} if mode == "slab" else {})),
                 "time_to_rtol_ms": ms_per_step,
                 "step_ms": {"events_around_call": step_ms, "library_device_ms": lib_ms},
-                "roofline": {"bound": "hbm",
-                             "kernel": "k_cg_mega phase A (Jacobi p-update + deferred x update + local Ax + mask + pap), "
-                                       "per CG iteration",
-                             "achieved": k1_ach, "peak": peak, "unit": "GB/s", "frac": k1_ach / peak,
-                             "traffic": traffic, "traffic_note": "ncu dram read+write of the whole megakernel "
-                                                                 "(both phases) per iteration, profiles/",
-                             "alg_bytes_per_iteration": k1_bytes + k2_bytes, "peak_source": peak_src,
-                             "alg_bytes_per_launch": k1_bytes, "avg_launch_us": 1e3 * k1_ms,
-                             "share_of_iteration": k1_ms / (k1_ms + k2_ms)},
-                "kernels": {
-                    "phaseA_ax": {"avg_us": 1e3 * k1_ms, "alg_bytes": k1_bytes, "GBps": k1_ach, "frac": k1_ach / peak},
-                    "phaseB_gather_update": {"avg_us": 1e3 * k2_ms, "alg_bytes": k2_bytes, "GBps": k2_ach,
-                                             "frac": k2_ach / peak},
-                    "ax_local": {"avg_us": 1e3 * ax_ms, "alg_bytes": AX_BYTES[pol] * NL,
-                                 "GBps": AX_BYTES[pol] * NL / (ax_ms * 1e-3) / 1e9,
-                                 "frac": AX_BYTES[pol] * NL / (ax_ms * 1e-3) / 1e9 / peak},
-                    "dssum_csr": {"note": "standalone nb_dssum (CSR segments; setup/API kernel, not on the solve "
-                                          "path: the solve gathers in phase B)",
-                                  "avg_us": 1e3 * gs_ms, "alg_bytes": gs_bytes,
-                                  "GBps": gs_bytes / (gs_ms * 1e-3) / 1e9,
-                                  "frac": gs_bytes / (gs_ms * 1e-3) / 1e9 / peak}},
-                "e2e": e2e,
-                "gpu_launches": launches, "clocks": ck, "cpu_baseline": cpu, "policies": ttr,
-                "hbm_bound_companion": large}
+                "phases_us": {"A": k1_us, "B": k2_us},
+                "roofline": roofline, "hbm_roofline_point": roof,
+                "e2e": e2e, "gpu_launches": launches, "clocks": ck, "cpu_baseline": cpu, "policies": ttr}
         print(json.dumps(line), flush=True)
     for m in group or [mesh]:
         m.close()
@@ -508,15 +615,23 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=60)
     ap.add_argument("--ref-iters", type=int, default=20)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--quick", action="store_true", help="skip the per-policy table and the large companion")
-    ap.add_argument("--no-large", action="store_true", help="skip the HBM-bound configs[2] companion point")
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "slab"],
-                    help="N>1: independent replicas, or one box split in z-slabs over the GPUs")
+    ap.add_argument("--quick", action="store_true", help="skip the per-policy table and the roofline point")
+    ap.add_argument("--no-large", action="store_true", help="skip the HBM-bound configs[2] roofline point")
+    ap.add_argument("--roofline-only", action="store_true",
+                    help="one configs[2] megakernel launch per --roof-policies entry (the ncu target), nothing else")
+    ap.add_argument("--roof-policies", nargs="+", default=["mixed", "fp64"], choices=list(POLICIES))
+    ap.add_argument("--mode", default=None, choices=["single", "replicas", "slab"],
+                    help="N>1 default: slab (one box split in z-slabs over the GPUs); replicas: independent solves")
     ap.add_argument("--slabs", type=int, default=2, help="--mode slab on one GPU: slabs in the launch")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only (gloo, no GPU work)")
     ap.add_argument("--oracle-timing", action="store_true",
                     help="instead of the bench line: time the CPU oracle per config (SURVEY §8(d))")
     ap.add_argument("--oracle-max-dof", type=float, default=0, help="--oracle-timing: skip larger configs")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
+    if args.dry_run:
+        return run_dry(args)
     if args.oracle_timing:
         return run_oracle_timing(args)
     if args.impl == "reference":

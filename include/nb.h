@@ -74,7 +74,11 @@ typedef enum {
     NB_ECUDA = 3,       /* CUDA runtime error; message in nb_last_error() */
     NB_EGEOM = 4,       /* non-positive Jacobian or Jacobi diagonal at setup */
     NB_EBREAKDOWN = 5,  /* pap <= 0 with rtr > 0, or a non-finite scalar */
-    NB_ESTATE = 6       /* handle destroyed / used from the wrong device */
+    NB_ESTATE = 6,      /* handle destroyed / used from the wrong device; a peer-attached handle
+                           whose last multi-rank solve aborted (nb_peer_detach + attach again) */
+    NB_ETIMEOUT = 7     /* multi-rank solve: a peer rank did not arrive within NB_PEER_TIMEOUT_MS
+                           (default 20000 ms) or another rank gave up; the solve stopped on every
+                           rank (no hang) and the attachment must be renewed */
 } nb_status;
 
 /* nb_cg_report.status (stagnation is NB_OK with status NB_STAGNATED) */

@@ -29,7 +29,7 @@ NB_PC_JACOBI, NB_PC_IDENTITY, NB_PC_JACOBI_F32 = 0, 1, 2
 NB_RHS_UNIFORM, NB_RHS_MANUFACTURED = 0, 1
 NB_AX_LOCAL = 1
 NB_CONVERGED, NB_MAXITER, NB_STAGNATED, NB_BROKEDOWN = 0, 1, 2, 3
-NB_OK, NB_EINVAL, NB_ENOMEM, NB_ECUDA, NB_EGEOM, NB_EBREAKDOWN, NB_ESTATE = range(7)
+NB_OK, NB_EINVAL, NB_ENOMEM, NB_ECUDA, NB_EGEOM, NB_EBREAKDOWN, NB_ESTATE, NB_ETIMEOUT = range(8)
 POLICY_NAMES = {NB_FP64: "fp64", NB_FP32: "fp32", NB_MIXED: "mixed", NB_FP32_DOT2: "fp32_dot2"}
 
 EXPORTED = ["nb_setup", "nb_setup_slab", "nb_destroy", "nb_query", "nb_rhs", "nb_ax", "nb_dssum", "nb_cg",

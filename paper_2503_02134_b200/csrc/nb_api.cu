@@ -261,6 +261,8 @@ static int setup_box(nb_handle *h, bool jacobi)
     {
         const char *gs = std::getenv("NB_CG_GS");
         h->cg_csr = (gs && std::strcmp(gs, "csr") == 0) ? 1 : 0;
+        const char *po = std::getenv("NB_PHASE_ONLY");   // measurement knob (tools/ncu_phases.sh)
+        h->phase_only = po ? (po[0] == 'A' ? 1 : po[0] == 'B' ? 2 : 0) : 0;
     }
     if ((e = cudaMalloc(&h->g64, sizeof(double) * 6 * NL)) != cudaSuccess) return fail(NB_ENOMEM, "cudaMalloc g64");
     if ((e = cudaMalloc(&h->B, sizeof(double) * NL)) != cudaSuccess) return fail(NB_ENOMEM, "cudaMalloc B");
@@ -530,15 +532,35 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
                 M.a[r].wlo = r > 0 ? (const void *)((const char *)hs[r - 1]->ws[prec].w + es * hs[r - 1]->E * n3) : nullptr;
                 M.a[r].whi = r + 1 < nh ? (const void *)((const char *)hs[r + 1]->ws[prec].w - es * hs[r]->E * n3) : nullptr;
                 M.mr.flag[r] = (unsigned int *)ws.ctl;
+                M.mr.abrt[r] = (unsigned int *)(ws.ctl + nb::NB_CTL_ABORT_OFF);
                 M.mr.slot[r] = (double *)(ws.ctl + nb::NB_CTL_FLAG_BYTES);
                 NB_CU(cudaMemsetAsync(ws.ctl, 0, nb::NB_CTL_BYTES, st), "memset ctl");
             }
             M.mr.nrank = nh; M.mr.rank0 = 0; M.mr.nloc = nh; M.mr.epoch0 = 0; M.mr.sys = 0;
+            // fault injection (tests only): a phantom extra rank that never arrives -- every
+            // cross-rank wait must give up after NB_PEER_TIMEOUT_MS and end the solve (no hang)
+            const char *ph = std::getenv("NB_FAULT_PHANTOM_RANK");
+            if (ph && ph[0] == '1' && nh < nb::NB_MAX_RANKS) {
+                unsigned char *c0 = hs[0]->ws[prec].ctl;
+                M.mr.flag[nh] = (unsigned int *)(c0 + 96);
+                M.mr.abrt[nh] = (unsigned int *)(c0 + 100);
+                M.mr.slot[nh] = (double *)(c0 + nb::NB_CTL_FLAG_BYTES);   // same values as rank 0's slots
+                M.mr.nrank = nh + 1;
+            }
         } else {
             const nb::PeerState &ps = ws0.peer;
-            for (int q = 0; q < ps.nrank; q++) { M.mr.flag[q] = ps.flag[q]; M.mr.slot[q] = ps.slot[q]; }
+            for (int q = 0; q < ps.nrank; q++) {
+                M.mr.flag[q] = ps.flag[q];
+                M.mr.abrt[q] = ps.abrt[q];
+                M.mr.slot[q] = ps.slot[q];
+            }
             M.mr.nrank = ps.nrank; M.mr.rank0 = ps.rank; M.mr.nloc = 1; M.mr.epoch0 = ps.epoch;
             M.mr.sys = ps.nrank > 1 ? 1 : 0;
+        }
+        {
+            const char *tm = std::getenv("NB_PEER_TIMEOUT_MS");
+            const double ms_to = tm ? std::atof(tm) : 20000.0;
+            M.mr.timeout_ns = (unsigned long long)((ms_to > 0 ? ms_to : 20000.0) * 1e6);
         }
         M.mr.Gr = NB_POL(prec, nb::grid_mega_mr, h0) / nh;
         if (M.mr.Gr < 1) return fail(NB_EINVAL, "too many slabs for one launch");
@@ -567,7 +589,17 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
         nb_handle *h = hs[r];
         nb::Workspace &ws = h->ws[prec];
         const nb::Scal s = *ws.scal_host;
-        if (multi && nh == 1) ws.peer.epoch += (uint32_t)s.epochs;   // flags are never reset
+        if (multi) {
+            // a bounded cross-rank wait gave up somewhere (this rank's abort word, or block 0's report)
+            uint32_t ab = 0;
+            NB_CU(cudaMemcpy(&ab, ws.ctl + nb::NB_CTL_ABORT_OFF, sizeof(ab), cudaMemcpyDeviceToHost), "copy abort");
+            if (ab || s.aborted) {
+                if (nh == 1) ws.peer.broken = true;   // flags and epochs are out of step: re-attach
+                ret = NB_ETIMEOUT;
+            } else if (nh == 1) {
+                ws.peer.epoch += (uint32_t)s.epochs;   // flags are never reset
+            }
+        }
         const int k = s.iter;
         std::vector<double> res(k + 1, 0.0);
         NB_CU(cudaMemcpy(res.data(), ws.hist, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost), "copy hist");
@@ -606,8 +638,10 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
             rep->k_gs_ms = km[1];
             rep->k_upd_ms = km[2];
         }
-        if (status == NB_BROKEDOWN) ret = NB_EBREAKDOWN;
+        if (status == NB_BROKEDOWN && ret == NB_OK) ret = NB_EBREAKDOWN;
     }
+    if (ret == NB_ETIMEOUT)
+        return fail(NB_ETIMEOUT, "multi-rank solve aborted: a peer rank did not arrive in time (re-attach before the next solve)");
     if (ret == NB_EBREAKDOWN) return fail(NB_EBREAKDOWN, "CG breakdown (pap <= 0 or non-finite scalar)");
     return NB_OK;
 }
@@ -642,6 +676,8 @@ static int cg_args(nb_handle *h, const nb_cg_opts *o)
 static int mr_args(const nb_handle *h, const nb_cg_opts *o)
 {
     if (o->gs_order != NB_GS_CONSISTENT) return fail(NB_EINVAL, "multi-rank solves use the consistent GS order");
+    if (h->ws[o->policy].peer.broken)
+        return fail(NB_ESTATE, "the last multi-rank solve aborted: nb_peer_detach and nb_peer_attach again");
     if (h->cg_csr) return fail(NB_EINVAL, "multi-rank solves run on the fused megakernel only");
     return NB_OK;
 }
@@ -821,6 +857,7 @@ int nb_peer_attach(nb_handle *h, nb_policy policy, int32_t nrank, int32_t rank, 
         if (q == rank) ctl = ws.ctl;
         else if ((rc = open(pb[q].ctl, (void **)&ctl))) return fail_close(rc);
         ps.flag[q] = (unsigned int *)ctl;
+        ps.abrt[q] = (unsigned int *)(ctl + nb::NB_CTL_ABORT_OFF);
         ps.slot[q] = (double *)(ctl + nb::NB_CTL_FLAG_BYTES);
     }
     if (rank > 0) {

@@ -40,7 +40,6 @@
 #pragma once
 #include "nb_common.cuh"
 #include "nb_gs.cuh"
-#include "nb_tma.cuh"
 
 namespace nb {
 
@@ -767,281 +766,6 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
     if (pc != NB_PC_IDENTITY) st_pencil<TV, N>(z + base, zz);
 }
 
-// ---------------------------------------------------------------------------
-// phase B, flat form: one thread per local node (consecutive threads on consecutive nodes), so
-// every vector access of a warp is one contiguous, fully coalesced segment (the pencil form
-// above touches 32 pencils = 32 x N x sizeof(TV) bytes per warp instruction: at p = 9 that is
-// 10 L1 wavefronts per 256 B).  Each copy of a shared node gathers all copies of its node in
-// ascending element order -- lexicographic (dz, dy, dx), negative offsets first -- i.e. the
-// CSR consistent order (C-8), so all copies get bit-identical sums (the same sums as upd_pencil;
-// only the order of the dot-product partials differs).  U nodes per thread per trip (stride NT) keep U x (w, r, dinv)
-// loads in flight per thread.  The element position of a thread's node advances by at most one
-// element per trip when NT <= N^3, so it is carried incrementally (no runtime divisions).
-// ---------------------------------------------------------------------------
-#ifndef NB_FLATB
-#define NB_FLATB 0   // measured 2-4x slower than upd_pencil (per-node neighbour round trips): off
-#endif
-#ifndef NB_FLATB_U
-#define NB_FLATB_U 4
-#endif
-struct FlatPos {
-    int32_t e, ex, ey, ez;   // element of the current node and its (global-layer) position
-};
-template <bool SLAB>
-__device__ __forceinline__ void flat_advance(const MeshDev &m, FlatPos &f, int32_t e)
-{
-    if (e == f.e) return;
-    if (e == f.e + 1) {
-        f.e = e;
-        if (++f.ex == m.nelx) {
-            f.ex = 0;
-            if (++f.ey == m.nely) { f.ey = 0; ++f.ez; }
-        }
-        return;
-    }
-    const ElemPos P = elem_pos<SLAB>(m, e);
-    f.e = e; f.ex = P.ex; f.ey = P.ey; f.ez = P.ez;
-}
-
-template <int PREC, int N, int GATHER, bool SLAB, int U>
-__device__ __forceinline__ void upd_flat(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ w,
-                                         typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
-                                         const void *__restrict__ dinv, typename Pol<PREC>::TV alpha, int32_t l0,
-                                         int32_t l1, int nt, Acc<PREC> &rtr, Acc<PREC> &rho, int pc,
-                                         const typename Pol<PREC>::TV *wlo, const typename Pol<PREC>::TV *whi)
-{
-    using TV = typename Pol<PREC>::TV;
-    using TG = typename Pol<PREC>::TG;
-    using TJ = typename Pol<PREC>::TJ;
-    using TS = typename Pol<PREC>::TS;
-    constexpr int N2 = N * N, N3 = N * N * N;
-    const int64_t ox = N3 - (N - 1);                                       // x-neighbour copy offset
-    const int64_t oy = (int64_t)m.nelx * N3 - (int64_t)(N - 1) * N;        // y
-    const int64_t oz = (int64_t)m.nelx * m.nely * N3 - (int64_t)(N - 1) * N2;   // z
-    FlatPos f;
-    f.e = -2;
-#pragma unroll 1
-    for (int32_t l = l0 + (int32_t)threadIdx.x; l < l1; l += U * nt) {
-        TV ww[U], rr[U];
-        TJ dd[U];
-        int xs[U], ys[U], zs[U];
-        bool zlo[U], zhi[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            const int32_t lu = l + u * nt;
-            xs[u] = ys[u] = zs[u] = 0;
-            zlo[u] = zhi[u] = false;
-            if (lu < l1) {
-                ww[u] = ldv<NB_WLD>(w + lu);
-                rr[u] = r[lu];
-                if (pc == NB_PC_IDENTITY) dd[u] = TJ(1);
-                else if (sizeof(TJ) == 8 && pc == NB_PC_JACOBI_F32) dd[u] = (TJ)__ldg((const float *)dinv + lu);
-                else dd[u] = __ldg((const TJ *)dinv + lu);
-                const int32_t e = lu / N3;
-                if constexpr (N3 >= 32 * ((AxCfg<TV, N>::NT + 31) / 32)) flat_advance<SLAB>(m, f, e);
-                else { const ElemPos P = elem_pos<SLAB>(m, e); f.e = e; f.ex = P.ex; f.ey = P.ey; f.ez = P.ez; }
-                const int q = lu - e * N3;
-                const int k = q / N2, j = (q / N) % N, i = q % N;
-                xs[u] = (i == 0 && f.ex > 0) ? -1 : ((i == N - 1 && f.ex < m.nelx - 1) ? 1 : 0);
-                ys[u] = (j == 0 && f.ey > 0) ? -1 : ((j == N - 1 && f.ey < m.nely - 1) ? 1 : 0);
-                zs[u] = (k == 0 && f.ez > 0) ? -1 : ((k == N - 1 && f.ez < m.nelz - 1) ? 1 : 0);
-                if (SLAB) {   // the z-neighbour layer may live in another slab (multi-rank)
-                    zlo[u] = zs[u] < 0 && f.ez == m.ez0;
-                    zhi[u] = zs[u] > 0 && f.ez == m.ez0 + m.nelzl - 1;
-                }
-            }
-        }
-        if (GATHER) {
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                const int32_t lu = l + u * nt;
-                if (lu < l1 && (xs[u] | ys[u] | zs[u])) {
-                    // copies (dz, dy, dx) in {lo, hi}^3 with lo = min(0, s), hi = max(0, s); the
-                    // combination with a zero offset on an axis without a neighbour appears once
-                    TV v[2][2][2];
-#pragma unroll
-                    for (int iz = 0; iz < 2; iz++)
-#pragma unroll
-                        for (int iy = 0; iy < 2; iy++)
-#pragma unroll
-                            for (int ix = 0; ix < 2; ix++) {
-                                const int dz = iz ? max(zs[u], 0) : min(zs[u], 0);
-                                const int dy = iy ? max(ys[u], 0) : min(ys[u], 0);
-                                const int dx = ix ? max(xs[u], 0) : min(xs[u], 0);
-                                const bool dup = (iz && !zs[u]) || (iy && !ys[u]) || (ix && !xs[u]);
-                                if (dup) continue;
-                                if (dz == 0 && dy == 0 && dx == 0) { v[iz][iy][ix] = ww[u]; continue; }
-                                const TV *base = w;
-                                if (SLAB && dz < 0 && zlo[u]) base = wlo;
-                                if (SLAB && dz > 0 && zhi[u]) base = whi;
-                                v[iz][iy][ix] = ldv<NB_WLD>(base + (lu + dz * oz + dy * oy + dx * ox));
-                            }
-                    TG s = 0;
-                    bool first = true;
-#pragma unroll
-                    for (int iz = 0; iz < 2; iz++)
-#pragma unroll
-                        for (int iy = 0; iy < 2; iy++)
-#pragma unroll
-                            for (int ix = 0; ix < 2; ix++) {
-                                const bool dup = (iz && !zs[u]) || (iy && !ys[u]) || (ix && !xs[u]);
-                                if (dup) continue;
-                                s = first ? (TG)v[iz][iy][ix] : s + (TG)v[iz][iy][ix];
-                                first = false;
-                            }
-                    ww[u] = (TV)s;
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            const int32_t lu = l + u * nt;
-            if (lu < l1) {
-                const TV rn = fma(-alpha, ww[u], rr[u]);                 // add2s2(r, w, -alpha)
-                const TV zn = solve_m<PREC>(rn, dd[u], pc);              // solveM
-                const int sh = (xs[u] != 0) + (ys[u] != 0) + (zs[u] != 0);
-                const TS c = sh == 0 ? (TS)1 : sh == 1 ? (TS)0.5 : sh == 2 ? (TS)0.25 : (TS)0.125;   // 1/mult
-                const TS rs = (TS)rn;
-                rtr.add(rs * c, rs);                                     // glsc3(r, c, r)
-                rho.add(rs * c, (TS)zn);                                 // glsc3(r, c, z)
-                r[lu] = rn;
-                if (pc != NB_PC_IDENTITY) z[lu] = zn;
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// phase B, staged form (default for even N): the block's elements are processed in groups of
-// EPB elements (phase A's grouping); each group's w, r and Jacobi diagonal -- three contiguous
-// ranges -- arrive in shared memory by 1-D TMA bulk copies on an mbarrier, double-buffered (the
-// next group's copies fly while this one is computed), and r, z leave by bulk stores.  The
-// per-thread work is upd_pencil's, on shared-memory pencils: the x-partner copies of the group's
-// own elements come from shared memory, the y/z-neighbour copies from global memory (L2).  No
-// vector operand is held in registers while in flight, so the block keeps ~2 stages (tens of KB)
-// of HBM traffic outstanding instead of one strided pencil per thread.  The buffers reuse (and
-// extend) phase A's dynamic shared memory.
-// ---------------------------------------------------------------------------
-#ifndef NB_STAGEB
-#define NB_STAGEB 0   // measured slower than upd_pencil: opt-in
-#endif
-template <int PREC, int N> struct StageB {
-    using TV = typename Pol<PREC>::TV;
-    using TJ = typename Pol<PREC>::TJ;
-    using C = AxCfg<TV, N>;
-    // bulk copies need 16-byte multiples: N^3 * 4 bytes is one for even N
-    static constexpr bool ON = NB_STAGEB && (N % 2 == 0);
-    static constexpr int CNT = C::EPB * N * N * N;                          // values per array per stage
-    static constexpr int BYTES = CNT * (2 * (int)sizeof(TV) + (int)sizeof(TJ));   // w, r, dinv
-    static constexpr int SMEM = ON ? 2 * BYTES : 0;
-    static constexpr int MEGA_SMEM = C::SMEM > SMEM ? C::SMEM : SMEM;     // dynamic smem of the megakernel
-};
-
-template <int PREC, int N, int GATHER, bool SLAB>
-__device__ __forceinline__ void upd_staged(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ w,
-                                           typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
-                                           const void *__restrict__ dinv, typename Pol<PREC>::TV alpha, int32_t e0,
-                                           int32_t e1, Acc<PREC> &rtr, Acc<PREC> &rho, int pc,
-                                           const typename Pol<PREC>::TV *wlo, const typename Pol<PREC>::TV *whi,
-                                           unsigned char *smem, uint64_t *bar, uint32_t &bph)
-{
-    using TV = typename Pol<PREC>::TV;
-    using TJ = typename Pol<PREC>::TJ;
-    using TS = typename Pol<PREC>::TS;
-    using SB = StageB<PREC, N>;
-    using C = AxCfg<TV, N>;
-    constexpr int N2 = N * N, N3 = N * N * N, EPB = C::EPB;
-    const int tid = threadIdx.x;
-    const bool ident = pc == NB_PC_IDENTITY;
-    const bool jf32 = sizeof(TJ) == 8 && pc == NB_PC_JACOBI_F32;   // mixed with Neko's fp32 diagonal
-    const int dsz = jf32 ? 4 : (int)sizeof(TJ);
-    auto stage = [&](int s) { return smem + (size_t)s * SB::BYTES; };
-    auto issue = [&](int32_t eg, int s) {   // thread 0: the group's three ranges -> stage s
-        const int ne = min(EPB, e1 - eg);
-        const size_t off = (size_t)eg * N3;
-        const uint32_t cnt = (uint32_t)ne * N3;
-        unsigned char *st = stage(s);
-        fence_proxy_async();
-        mbar_arrive_expect_tx(bar + s, cnt * (2 * (uint32_t)sizeof(TV) + (ident ? 0u : (uint32_t)dsz)));
-        bulk_g2s(st, w + off, cnt * (uint32_t)sizeof(TV), bar + s);
-        bulk_g2s(st + SB::CNT * sizeof(TV), r + off, cnt * (uint32_t)sizeof(TV), bar + s);
-        if (!ident) bulk_g2s(st + 2 * SB::CNT * sizeof(TV), (const unsigned char *)dinv + off * dsz, cnt * (uint32_t)dsz, bar + s);
-    };
-    const int32_t ngr = e1 > e0 ? (e1 - e0 + EPB - 1) / EPB : 0;
-    fence_proxy_async();   // phase A's shared-memory accesses before the bulk copies overwrite them
-    __syncthreads();
-    if (tid == 0 && ngr > 0) issue(e0, 0);
-#pragma unroll 1
-    for (int32_t t = 0; t < ngr; t++) {
-        const int s = t & 1;
-        const int32_t eg = e0 + t * EPB;
-        const int ne = min(EPB, e1 - eg);
-        if (tid == 0 && t + 1 < ngr) {
-            bulk_wait_read0();   // stage s^1's previous bulk stores have read their data
-            issue(eg + EPB, s ^ 1);
-        }
-        mbar_wait(bar + s, (bph >> s) & 1u);
-        bph ^= 1u << s;
-        unsigned char *st = stage(s);
-        TV *sw = reinterpret_cast<TV *>(st);
-        TV *sr = sw + SB::CNT;
-        const TJ *sd = reinterpret_cast<const TJ *>(sr + SB::CNT);
-        const bool act = tid < ne * N2;
-        const int el = tid / N2, q = tid - el * N2;
-        const int lb = el * N3 + q * N;   // this thread's pencil in the stage
-        TV z0 = 0, zn1 = 0;
-        if (act) {
-            const int a = q % N, b = q / N;
-            const int e = eg + el;
-            TV ww[N];
-#pragma unroll
-            for (int i = 0; i < N; i++) ww[i] = sw[lb + i];
-            const ElemPos P = elem_pos<SLAB>(m, e);
-            if (GATHER) {
-                const size_t gb = (size_t)e * N3 + (size_t)q * N;   // pencil in global memory
-                const TV ol = P.ex > 0 ? (el > 0 ? sw[lb - N3 + (N - 1)] : ldv<NB_WLD>(w + gb - N3 + (N - 1))) : TV(0);
-                const TV orr = P.ex < m.nelx - 1 ? (el + 1 < ne ? sw[lb + N3] : ldv<NB_WLD>(w + gb + N3)) : TV(0);
-                gather_pencil<PREC, N>(m, w, e, P, a, b, ww, ol, orr, wlo, whi);
-            }
-            const int mjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz);
-            // streamed node by node from shared memory: r -> sr at once (read by this thread only);
-            // z -> sw, except the pencil ends, which other threads read as x-partners until the barrier
-#pragma unroll
-            for (int i = 0; i < N; i++) {
-                const TJ d = ident ? TJ(1) : jf32 ? (TJ)reinterpret_cast<const float *>(sd)[lb + i] : sd[lb + i];
-                const TV rn = fma(-alpha, ww[i], sr[lb + i]);          // add2s2(r, w, -alpha)
-                const TV zv = solve_m<PREC>(rn, d, pc);                // solveM
-                const TS c = (TS)1 / (TS)(mjk * axis_mult(i, N, P.ex, m.nelx));
-                const TS rs = (TS)rn;
-                rtr.add(rs * c, rs);                                   // glsc3(r, c, r)
-                rho.add(rs * c, (TS)zv);                               // glsc3(r, c, z)
-                sr[lb + i] = rn;
-                if (i == 0) z0 = zv;
-                else if (i == N - 1) zn1 = zv;
-                else if (!ident) sw[lb + i] = zv;
-            }
-        }
-        __syncthreads();   // every x-partner read of sw is done: the pencil ends of z -> sw
-        if (act && !ident) {
-            sw[lb] = z0;
-            sw[lb + N - 1] = zn1;
-        }
-        fence_proxy_async();   // the shared-memory writes before the bulk stores read them
-        __syncthreads();
-        if (tid == 0) {
-            const size_t off = (size_t)eg * N3;
-            const uint32_t bytes = (uint32_t)(ne * N3) * (uint32_t)sizeof(TV);
-            bulk_s2g(r + off, sr, bytes);
-            if (!ident) bulk_s2g(z + off, sw, bytes);
-            bulk_commit();
-        }
-    }
-    if (tid == 0) {
-        bulk_wait0();          // r, z written before the grid barrier (and smem free for phase A)
-        fence_proxy_async();
-    }
-}
-
 // CG prologue for one pencil: r = b, x = 0, p = 0, z = M^-1 r; rtr0 and rho_1 partials.
 template <int PREC, int N, bool SLAB = false>
 __device__ __forceinline__ void init_pencil(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ bvec,
@@ -1280,8 +1004,24 @@ __device__ __forceinline__ unsigned int ld_acquire_sys_u32(const unsigned int *p
 // every rank's slot array and bumps every rank's flag -> every block waits until its rank's flag
 // counts all R pushes and merges the R rank partials in rank order (bit-identical in every block
 // of every rank).  One local barrier, one push, one flag wait per reduction.
+// Every wait of the multi-rank solve is bounded: it gives up when its rank's abort word is set
+// (another block or rank gave up) or after mr.timeout_ns, and then sets every rank's abort word.
+// A dead or mismatched peer (not launched, other options) thus ends the solve with the
+// `aborted` status instead of hanging every GPU (the host then requires a re-attach).
+__device__ __forceinline__ bool mr_give_up(const MrArgs &mr, int me, unsigned long long t0)
+{
+    const unsigned int ab = mr.sys ? ld_acquire_sys_u32(mr.abrt[me]) : ld_acquire_u32(mr.abrt[me]);
+    if (ab) return true;
+    if (globaltimer() - t0 < mr.timeout_ns) return false;
+    for (int q = 0; q < mr.nrank; q++) {
+        if (mr.sys) asm volatile("st.release.sys.global.u32 [%0], 1;" ::"l"(mr.abrt[q]) : "memory");
+        else asm volatile("st.release.gpu.global.u32 [%0], 1;" ::"l"(mr.abrt[q]) : "memory");
+    }
+    return true;
+}
+
 template <int PREC, int K>
-__device__ __forceinline__ void mr_reduce(const MegaArgs &A, const MrArgs &mr, int vr, int bid, int G,
+__device__ __forceinline__ bool mr_reduce(const MegaArgs &A, const MrArgs &mr, int vr, int bid, int G,
                                           Acc<PREC> (&vals)[K], double *part, unsigned int &tgt, unsigned int ep,
                                           typename Pol<PREC>::TS (&tot)[K], Acc<PREC> *acc_sh)
 {
@@ -1290,12 +1030,20 @@ __device__ __forceinline__ void mr_reduce(const MegaArgs &A, const MrArgs &mr, i
     const int tid = threadIdx.x;
     const int R = mr.nrank, me = mr.rank0 + vr, par = ep & 1;
     __shared__ TS bc[K];
+    __shared__ int gave_up;
     if (tid < 32) {
         if (tid == 0) {
 #pragma unroll
             for (int k = 0; k < K; k++) vals[k].store(part + ((size_t)bid * K + k) * W);
             tgt += G;
-            grid_arrive_wait(A.bar, tgt);
+            gave_up = 0;
+            // rank-local grid barrier, bounded
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.bar) : "memory");
+            const unsigned long long t0 = globaltimer();
+            while ((int)(ld_acquire_u32(A.bar) - tgt) < 0) {
+                if (mr_give_up(mr, me, t0)) { gave_up = 1; break; }
+                __nanosleep(NB_POLL_NS);
+            }
         }
         __syncwarp();
         // warp 0: the rank partial (fixed order, the same value in every block of the rank)
@@ -1319,18 +1067,19 @@ __device__ __forceinline__ void mr_reduce(const MegaArgs &A, const MrArgs &mr, i
             }
             // the release orders the slot stores before the flag bumps; system scope only when
             // ranks live on other GPUs (peer memory), GPU scope when they share this launch
+            const unsigned long long t0 = globaltimer();
             if (mr.sys) {
                 if (bid == 0)
                     for (int q = 0; q < R; q++)
                         asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(mr.flag[q]) : "memory");
-                while ((int)(ld_acquire_sys_u32(mr.flag[me]) - want) < 0) {
-                }
+                while (!gave_up && (int)(ld_acquire_sys_u32(mr.flag[me]) - want) < 0)
+                    if (mr_give_up(mr, me, t0)) gave_up = 1;
             } else {
                 if (bid == 0)
                     for (int q = 0; q < R; q++)
                         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(mr.flag[q]) : "memory");
-                while ((int)(ld_acquire_u32(mr.flag[me]) - want) < 0) {
-                }
+                while (!gave_up && (int)(ld_acquire_u32(mr.flag[me]) - want) < 0)
+                    if (mr_give_up(mr, me, t0)) gave_up = 1;
             }
             Acc<PREC> t[K];
             const double *src = mr.slot[me] + (size_t)par * NB_MAX_RANKS * 4;
@@ -1346,6 +1095,7 @@ __device__ __forceinline__ void mr_reduce(const MegaArgs &A, const MrArgs &mr, i
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < K; k++) tot[k] = bc[k];
+    return gave_up != 0;
 }
 
 

@@ -24,21 +24,25 @@ struct Scal {
     int32_t status;    // NB_CONVERGED / NB_MAXITER / NB_BROKEDOWN (stagnation decided on host)
     int32_t pending;   // 1: x += alpha*p of the last iteration not yet applied (deferred x update)
     int32_t epochs;    // multi-rank megakernel: cross-rank barrier epochs used by the solve
+    int32_t aborted;   // multi-rank megakernel: a cross-rank wait timed out or a rank aborted
 };
 
 // Multi-rank (z-slab) solves: ranks per solve, slabs per launch (one GPU)
 constexpr int NB_MAX_RANKS = 8;
 constexpr int NB_MAX_DEVICES = 64;   // per-device caches of kernel residency
 constexpr int NB_MAX_LOCAL = 4;
-// per-rank control block (peer-visible): arrival flag, then rank-partial slots
-// [2 parities][NB_MAX_RANKS][4 doubles] (K <= 2 accumulators x W <= 2 doubles)
+// per-rank control block (peer-visible): arrival flag (offset 0), abort word (offset 64), then
+// rank-partial slots [2 parities][NB_MAX_RANKS][4 doubles] (K <= 2 accumulators x W <= 2 doubles)
 constexpr int NB_CTL_FLAG_BYTES = 128;
+constexpr int NB_CTL_ABORT_OFF = 64;
 constexpr int NB_CTL_BYTES = NB_CTL_FLAG_BYTES + 2 * NB_MAX_RANKS * 4 * 8;
 struct PeerState {
     int32_t nrank = 0, rank = 0;       // nrank 0: not attached
     const void *wlo = nullptr, *whi = nullptr;   // neighbours' w (below / above), rebased (nb_cg.cuh)
     unsigned int *flag[NB_MAX_RANKS] = {};
+    unsigned int *abrt[NB_MAX_RANKS] = {};
     double *slot[NB_MAX_RANKS] = {};
+    bool broken = false;               // a solve aborted: flags/epochs out of step, re-attach needed
     uint32_t epoch = 0;                // cross-rank barrier epochs completed by earlier solves
     void *opened[NB_MAX_RANKS + 2] = {};   // IPC mappings to close
     int nopened = 0;
@@ -71,6 +75,8 @@ struct MegaArgs {
     double *partA, *partS, *partB;   // per-block partials, [G], [G], [2G] (x Acc::W)
     int32_t pc;             // nb_precond (z aliases r for the identity)
     int32_t x64;            // NB_MIXED: x is double (x_fp64 option)
+    int32_t phase_only;     // measurement only (NB_PHASE_ONLY=A|B at setup): 1 = phase A alone,
+                            // 2 = phase B alone, max_iter iterations, no stop test (ncu traffic per phase)
     unsigned int *bar;      // [2] grid barrier: arrival count, generation
     Scal *scal;             // result scalars (written by block 0)
     // multi-rank (z-slab) solves only: the neighbour slabs' w, rebased so that the element
@@ -89,7 +95,9 @@ struct MrArgs {
     int32_t Gr;              // blocks per slab
     uint32_t epoch0;         // barrier epochs completed by earlier solves
     int32_t sys;             // 1: ranks on other GPUs (system-scope flags); 0: all in this launch
+    unsigned long long timeout_ns;   // bound of every cross-rank wait (NB_PEER_TIMEOUT_MS)
     unsigned int *flag[NB_MAX_RANKS];
+    unsigned int *abrt[NB_MAX_RANKS];   // abort words: a rank that gives up tells every rank
     double *slot[NB_MAX_RANKS];
 };
 struct MultiArgs {
@@ -141,6 +149,7 @@ struct nb_handle {
     int32_t *flag = nullptr;    // device error flags for setup checks
     cudaStream_t cap_stream = nullptr;   // private stream used for setup
     int cg_csr = 0;             // 1: consistent-order CG also through the CSR dssum kernel (A/B)
+    int phase_only = 0;         // NB_PHASE_ONLY=A (1) / B (2): measurement runs of one megakernel phase
     nb::Workspace ws[4];   // one per nb_policy
     nb::MeshDev md() const {
         nb::MeshDev m;

@@ -31,7 +31,7 @@ template <int PREC, int N, int FUSED, int VAR>
 static int mega_grid_t(const nb_handle *h)
 {
     using C = AxCfg<typename Pol<PREC>::TV, N>;
-    constexpr int SMEM_MEGA = StageB<PREC, N>::MEGA_SMEM;
+    constexpr int SMEM_MEGA = C::SMEM;
     const void *fn = (const void *)k_cg_mega<PREC, N, FUSED, VAR>;
     static DevCache cache;   // the attributes and the residency are per device
     int &occ = cache.here();
@@ -80,7 +80,7 @@ static cudaError_t mega_launch_t(const nb_handle *h, const MegaArgs &args, cudaS
 {
     using TV = typename Pol<PREC>::TV;
     using C = AxCfg<TV, N>;
-    constexpr int SMEM_MEGA = StageB<PREC, N>::MEGA_SMEM;
+    constexpr int SMEM_MEGA = C::SMEM;
     DMat<TV, N> D = make_dmat<TV, N>(h->D);
     void *params[2] = {(void *)&args, (void *)&D};
     int grid = mega_grid_t<PREC, N, FUSED, VAR>(h);
@@ -120,6 +120,7 @@ void fill_mega_args(const nb_handle *h, Workspace &ws, const void *b, int order,
     A.b = b;
     A.pc = precond;
     A.x64 = (PREC == NB_MIXED && x64) ? 1 : 0;
+    A.phase_only = h->phase_only;
     A.x = A.x64 ? (void *)ws.xd : ws.x; A.p = ws.p; A.r = ws.r; A.w = ws.w;
     A.z = precond == NB_PC_IDENTITY ? ws.r : ws.z;   // identity: z aliases r (never stored)
     A.g = (sizeof(typename Pol<PREC>::TV) == 8) ? (const void *)h->g64 : (const void *)h->g32;
@@ -156,7 +157,7 @@ template <int PREC, int N>
 static int mr_occupancy()
 {
     using C = AxCfg<typename Pol<PREC>::TV, N>;
-    constexpr int SMEM_MEGA = StageB<PREC, N>::MEGA_SMEM;
+    constexpr int SMEM_MEGA = C::SMEM;
     static DevCache cache;
     int &occ = cache.here();
     if (occ < 0) {
@@ -180,7 +181,7 @@ static cudaError_t mr_launch_t(const nb_handle *h, const MultiArgs &M, cudaStrea
 {
     using TV = typename Pol<PREC>::TV;
     using C = AxCfg<TV, N>;
-    constexpr int SMEM_MEGA = StageB<PREC, N>::MEGA_SMEM;
+    constexpr int SMEM_MEGA = C::SMEM;
     DMat<TV, N> D = make_dmat<TV, N>(h->D);
     void *params[2] = {(void *)&M, (void *)&D};
     (void)mr_occupancy<PREC, N>();

@@ -34,3 +34,30 @@ def test_oracle_timing_small():
     (c,) = d["cases"]
     assert c["config"] == "configs[0]" and c["n_local"] == 4096
     assert c["solve_fp64"]["iterations"] == 100 and c["solve_fp64"]["dof_iter_per_s"] > 0
+
+
+def test_gpus2_spawns_two_ranks_dry_run():
+    """--gpus N without a torchrun environment relaunches itself with N ranks (127.0.0.1
+    rendezvous); N > 1 defaults to the z-slab decomposition.  --dry-run: gloo plumbing only."""
+    env_clean = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=300, env=env_clean)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["mode"] == "slab" and "z-slabs over 2 GPUs" in d["parallelism"]
+
+
+def test_survey_bytes_and_ae_mae():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    class Info:
+        n_local, n_shared_copies, n_shared_global = 2097152, 1155960, 501705   # configs[1], SURVEY §8(a)
+
+    got = [round(bench.survey_bytes(p, Info), 1) for p in (0, 2, 1)]
+    assert got == [165.9, 92.5, 84.5]                                        # SURVEY.md §8(d) table
+    assert bench.impl_bytes(0) == 136 and bench.impl_bytes(2) == 72 and bench.impl_bytes(1) == 68
+    d = bench.ae_mae([1.0, 0.5, 0.25, 0.1], [1.0, 0.5, 0.2, 0.1, 0.05])
+    assert d["iterations_compared"] == 3 and abs(d["MAE"] - 0.05 / 3) < 1e-12 and abs(d["AE_max"] - 0.05) < 1e-12

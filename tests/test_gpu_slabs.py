@@ -240,3 +240,25 @@ def test_group_degenerate_cases():
     xs, rs = nb.cg_group(ms, bs, nb.NB_MIXED, max_iter=500, rtol=1e-8)
     assert rs[0].status == nb.NB_CONVERGED
     close_all(ms)
+
+
+def test_group_phantom_rank_times_out_instead_of_hanging(monkeypatch):
+    """A rank that never arrives (fault injection: a phantom extra rank) makes every bounded
+    cross-rank wait give up after NB_PEER_TIMEOUT_MS: the solve returns NB_ETIMEOUT on every slab
+    instead of hanging the GPU, and the next solve (fresh control blocks) is correct again."""
+    import time
+    ms = slabs((4, 4, 4), 5, 2)
+    bs = [m.rhs(nb.NB_MIXED, seed=0) for m in ms]
+    xs0, r0 = nb.cg_group(ms, bs, nb.NB_MIXED, max_iter=400, rtol=1e-8)
+    monkeypatch.setenv("NB_FAULT_PHANTOM_RANK", "1")
+    monkeypatch.setenv("NB_PEER_TIMEOUT_MS", "200")
+    t0 = time.time()
+    with pytest.raises(nb.NbError) as ei:
+        nb.cg_group(ms, bs, nb.NB_MIXED, max_iter=400, rtol=1e-8)
+    assert ei.value.code == nb.NB_ETIMEOUT
+    assert time.time() - t0 < 30.0
+    monkeypatch.delenv("NB_FAULT_PHANTOM_RANK")
+    xs1, r1 = nb.cg_group(ms, bs, nb.NB_MIXED, max_iter=400, rtol=1e-8)
+    assert r1[0].iterations == r0[0].iterations
+    assert all(torch.equal(a, b) for a, b in zip(xs0, xs1))
+    close_all(ms)
