@@ -58,8 +58,17 @@ typedef enum { NB_FP64 = 0, NB_FP32 = 1, NB_MIXED = 2, NB_FP32_DOT2 = 3 } nb_pol
  *   NB_GS_CONSISTENT: one sum per shared global node, copies ascending, written to all copies.
  *   NB_GS_PER_COPY  : copy l receives w_l + sum_{m != l, ascending} w_m, emulating the
  *                     pairwise exchange mode whose fp32 stagnation the paper reports
- *                     (Table 3). */
-typedef enum { NB_GS_CONSISTENT = 0, NB_GS_PER_COPY = 1 } nb_gs_order;
+ *                     (Table 3) with every element its own rank.
+ *   NB_GS_PAIRWISE / NB_GS_ALLREDUCE: the gather-scatter of a run whose
+ *                     elements are split over px x py x pz ranks (contiguous blocks as even as
+ *                     possible: block b of an axis holds elements [b nel/P, (b+1) nel/P)).  Each
+ *                     rank sums its own copies of a node (ascending local index) into a partial P_q
+ *                     in the GS precision; PAIRWISE: a copy on rank r receives P_r + sum over the
+ *                     other ranks q ascending of P_q (gslib's pairwise exchange: each rank adds its
+ *                     neighbours' contributions to its own); ALLREDUCE: every copy receives
+ *                     sum over q ascending of P_q (one global reduction).  PAPER.md:339-341, Table 3.
+ *                     Emulated in one launch on one GPU (the partition is logical). */
+typedef enum { NB_GS_CONSISTENT = 0, NB_GS_PER_COPY = 1, NB_GS_PAIRWISE = 2, NB_GS_ALLREDUCE = 3 } nb_gs_order;
 
 /* Right-hand sides, generated in fp64 and cast once:
  *   NB_RHS_UNIFORM     : b_l = mask_l * U(seed, 1, gid_l), U the counter SplitMix64 in [-1,1).
@@ -118,6 +127,7 @@ typedef struct {
                                   [3(k-1) + 0..2] = rho_k, alpha_k, beta_k of Table 2
                                   as the policy computes them: binary64 under NB_FP64 / NB_MIXED,
                                   binary32 (widened exactly) under NB_FP32 / NB_FP32_DOT2 (C-10 table) */
+    int32_t ranks[3];          /* px, py, pz of gs_order NB_GS_PAIRWISE / NB_GS_ALLREDUCE (0 = 1) */
 } nb_cg_opts;
 
 typedef struct {
@@ -164,8 +174,13 @@ int nb_rhs(nb_handle *h, nb_rhs_kind kind, double noise_amp, uint64_t seed, nb_p
  * PAPER.md:163 ("call ax(w,p,g,ur,us,ut,wk,n)"), :147. */
 int nb_ax(nb_handle *h, nb_policy prec, const void *u, void *w, uint32_t flags, void *stream);
 
-/* In place u = QQ^T u over the shared-node segments (no mask).  Async.  PAPER.md:309, :404. */
+/* In place u = QQ^T u over the shared-node segments (no mask).  Async.  PAPER.md:309, :404.
+ * order NB_GS_PAIRWISE / NB_GS_ALLREDUCE need a partition: nb_dssum_ranked. */
 int nb_dssum(nb_handle *h, nb_policy prec, nb_gs_order order, void *u, void *stream);
+/* Same with the rank partition px x py x pz of the NB_GS_PAIRWISE / NB_GS_ALLREDUCE orders
+ * (NB_EINVAL unless 1 <= p_a <= nel_a; the handle must hold the whole box). */
+int nb_dssum_ranked(nb_handle *h, nb_policy prec, nb_gs_order order, int32_t px, int32_t py, int32_t pz,
+                    void *u, void *stream);
 
 /* Jacobi-PCG (Table 2 order) from x0 = 0.  b, x: device vectors in the
  * policy precision (x: double when o->x_fp64); b must be continuous and masked (e.g. from

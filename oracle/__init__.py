@@ -26,7 +26,7 @@ _LIB = os.path.join(_HERE, "libnb_oracle.so")
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c99", "-Wall"]
 
 FP64, FP32, MIXED, FP32_DOT2 = 0, 1, 2, 3
-GS_CONSISTENT, GS_PER_COPY = 0, 1
+GS_CONSISTENT, GS_PER_COPY, GS_PAIRWISE, GS_ALLREDUCE = 0, 1, 2, 3
 PC_JACOBI, PC_IDENTITY, PC_JACOBI_F32 = 0, 1, 2   # or_cg precond
 RHS_UNIFORM, RHS_MANUFACTURED = 0, 1
 CONVERGED, MAXITER, STAGNATED, BREAKDOWN = 0, 1, 2, 3
@@ -63,6 +63,7 @@ def lib():
         L.or_mesh_new.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64]
         L.or_mesh_free.argtypes = [P]
         L.or_mesh_info.argtypes = [P, P]
+        L.or_set_ranks.argtypes = [P, C.c_int, C.c_int, C.c_int]
         L.or_export_maps.argtypes = [P, P, P, P, P]
         L.or_export_geom.argtypes = [P, P, P, P, P, P, P]
         L.or_splitmix64.restype = C.c_uint64
@@ -157,6 +158,12 @@ class Mesh:
         if getattr(self, "_h", None):
             lib().or_mesh_free(self._h)
             self._h = None
+
+    def set_ranks(self, px: int, py: int, pz: int):
+        """Rank partition of the GS_PAIRWISE / GS_ALLREDUCE gather-scatter orders (NEXT-2)."""
+        if lib().or_set_ranks(self._h, px, py, pz):
+            raise ValueError("bad rank partition")
+        self.ranks = (px, py, pz)
 
     # exports -------------------------------------------------------------
     def maps(self):

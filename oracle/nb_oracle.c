@@ -47,6 +47,7 @@ struct or_mesh {
     int32_t *off, *idx;            /* GS CSR */
     double *dinv;                  /* NL fp64 */
     float *dinvf;                  /* one-time float cast */
+    int px, py, pz;                /* rank partition of the ranked gather-scatter orders (or_set_ranks) */
 };
 
 /* ------------------------------------------------------------------ */
@@ -195,6 +196,7 @@ or_mesh *or_mesh_new(int nelx, int nely, int nelz, int p, double deform_amp, uin
     if (nelx < 1 || nely < 1 || nelz < 1 || p < 1 || p > 15) return NULL;
     or_mesh *m = (or_mesh *)calloc(1, sizeof(or_mesh));
     m->nelx = nelx; m->nely = nely; m->nelz = nelz; m->p = p; m->n = p + 1;
+    m->px = m->py = m->pz = 1;
     const int n = m->n;
     const int64_t n3 = (int64_t)n * n * n;
     m->E = (int64_t)nelx * nely * nelz;
@@ -523,8 +525,79 @@ void or_ax_local_f(const or_mesh *m, const float *u, float *w)
 /* C-8: gather-scatter QQ^T over the CSR segments                      */
 /* ------------------------------------------------------------------ */
 
+/* Rank of element e in a px x py x pz partition of the element box:
+ * contiguous blocks as even as possible, block b of an axis with nel elements and P parts
+ * holding elements [floor(b nel / P), floor((b+1) nel / P)). */
+int or_set_ranks(or_mesh *m, int px, int py, int pz)
+{
+    if (px < 1 || py < 1 || pz < 1 || px > m->nelx || py > m->nely || pz > m->nelz) return 1;
+    m->px = px; m->py = py; m->pz = pz;
+    return 0;
+}
+static int block_of(int i, int nel, int P)
+{
+    int b = 0;
+    while (b + 1 < P && (int64_t)(b + 1) * nel / P <= i) b++;
+    return b;
+}
+static int elem_rank(const or_mesh *m, int64_t e)
+{
+    int ex, ey, ez;
+    element_xyz(m, e, &ex, &ey, &ez);
+    return block_of(ex, m->nelx, m->px) + m->px * (block_of(ey, m->nely, m->py) + m->py * block_of(ez, m->nelz, m->pz));
+}
+
+/* The gather-scatter of a rank-partitioned run (Table 3: gslib's pairwise and
+ * allreduce modes).  Each rank first sums its own copies of a node in ascending local index (the
+ * local gather, GS precision TG); the rank partials P_q are then exchanged in TG:
+ *   OR_GS_PAIRWISE : a copy on rank r receives P_r + sum_{q != r, ascending q} P_q -- each rank
+ *                    adds its neighbours' contributions to its own;
+ *   OR_GS_ALLREDUCE: every copy receives sum_{ascending q} P_q -- one reduction, the same value on
+ *                    every rank.
+ * Copies of a node on one rank always agree; copies on different ranks agree under pairwise only
+ * when at most two ranks share the node (a + b = b + a), so a 1-D partition stays consistent. */
+#define OR_DSSUM_RANKED(NAME, TVX, TGX)                                                        \
+    static void NAME(const or_mesh *m, int order, TVX *u)                                     \
+    {                                                                                          \
+        const int64_t n3 = (int64_t)m->n * m->n * m->n;                                        \
+        for (int32_t s = 0; s < m->nseg; s++) {                                                \
+            const int32_t a = m->off[s], cnt = m->off[s + 1] - a;                              \
+            TVX v[8];                                                                          \
+            int rk[8];                                                                         \
+            TGX part[8];                                                                       \
+            for (int q = 0; q < cnt; q++) {                                                    \
+                v[q] = u[m->idx[a + q]];                                                       \
+                rk[q] = elem_rank(m, m->idx[a + q] / n3);                                      \
+            }                                                                                  \
+            for (int q = 0; q < cnt; q++) {          /* local gather: P of copy q's rank */    \
+                TGX t = 0;                                                                     \
+                for (int q2 = 0; q2 < cnt; q2++)                                               \
+                    if (rk[q2] == rk[q]) t += (TGX)v[q2];                                      \
+                part[q] = t;                                                                   \
+            }                                                                                  \
+            for (int q = 0; q < cnt; q++) {                                                    \
+                TGX t = (order == OR_GS_PAIRWISE) ? part[q] : (TGX)0;                          \
+                int prev = -1;                                                                 \
+                for (;;) {                           /* ranks in ascending order */            \
+                    int best = -1;                                                             \
+                    for (int q2 = 0; q2 < cnt; q2++)                                           \
+                        if (rk[q2] > prev && (best < 0 || rk[q2] < rk[best])) best = q2;       \
+                    if (best < 0) break;                                                       \
+                    prev = rk[best];                                                           \
+                    if (order == OR_GS_PAIRWISE && rk[best] == rk[q]) continue;                \
+                    t += part[best];                                                           \
+                }                                                                              \
+                u[m->idx[a + q]] = (TVX)t;                                                     \
+            }                                                                                  \
+        }                                                                                      \
+    }
+OR_DSSUM_RANKED(dssum_ranked_d, double, double)
+OR_DSSUM_RANKED(dssum_ranked_f, float, float)
+OR_DSSUM_RANKED(dssum_ranked_fd, float, double)
+
 void or_dssum_d(const or_mesh *m, int order, double *u)
 {
+    if (order == OR_GS_PAIRWISE || order == OR_GS_ALLREDUCE) { dssum_ranked_d(m, order, u); return; }
     double vals[8];
     for (int32_t s = 0; s < m->nseg; s++) {
         int32_t a = m->off[s], cnt = m->off[s + 1] - a;
@@ -546,6 +619,7 @@ void or_dssum_d(const or_mesh *m, int order, double *u)
 
 void or_dssum_f(const or_mesh *m, int order, float *u)
 {
+    if (order == OR_GS_PAIRWISE || order == OR_GS_ALLREDUCE) { dssum_ranked_f(m, order, u); return; }
     float vals[8];
     for (int32_t s = 0; s < m->nseg; s++) {
         int32_t a = m->off[s], cnt = m->off[s + 1] - a;
@@ -567,6 +641,7 @@ void or_dssum_f(const or_mesh *m, int order, float *u)
 
 void or_dssum_fd(const or_mesh *m, int order, float *u)
 {
+    if (order == OR_GS_PAIRWISE || order == OR_GS_ALLREDUCE) { dssum_ranked_fd(m, order, u); return; }
     float vals[8];
     for (int32_t s = 0; s < m->nseg; s++) {
         int32_t a = m->off[s], cnt = m->off[s + 1] - a;

@@ -23,7 +23,9 @@ extern "C" {
 /* OR_FP32_DOT2: the fp32 policy with every glsc3 computed by the
  * compensated Dot2 in binary32. */
 enum { OR_FP64 = 0, OR_FP32 = 1, OR_MIXED = 2, OR_FP32_DOT2 = 3 };
-enum { OR_GS_CONSISTENT = 0, OR_GS_PER_COPY = 1 };
+/* OR_GS_PAIRWISE / OR_GS_ALLREDUCE: the gather-scatter of a rank-partitioned
+ * run (partition set by or_set_ranks; Table 3). */
+enum { OR_GS_CONSISTENT = 0, OR_GS_PER_COPY = 1, OR_GS_PAIRWISE = 2, OR_GS_ALLREDUCE = 3 };
 enum { OR_RHS_UNIFORM = 0, OR_RHS_MANUFACTURED = 1 };
 enum { OR_CONVERGED = 0, OR_MAXITER = 1, OR_STAGNATED = 2, OR_BREAKDOWN = 3 };
 
@@ -44,6 +46,9 @@ or_mesh *or_mesh_new(int nelx, int nely, int nelz, int p, double deform_amp, uin
 void or_mesh_free(or_mesh *m);
 /* info[0..7] = E, n_local, n_global, n_unmasked, n_shared_global, n_shared_copies, p, min J sign ok */
 void or_mesh_info(const or_mesh *m, int64_t *info);
+/* rank partition px x py x pz of the element box for OR_GS_PAIRWISE / OR_GS_ALLREDUCE (default 1x1x1);
+ * returns 1 unless 1 <= p_a <= nel_a. */
+int or_set_ranks(or_mesh *m, int px, int py, int pz);
 void or_export_maps(const or_mesh *m, int64_t *gid, uint8_t *mask, int32_t *gs_off, int32_t *gs_idx);
 /* g6: 6*n_local factor-major (g1..g6), B, dinv, c (=1/mult), xyz: 3*n_local (x,y,z factor-major), jac: n_local */
 void or_export_geom(const or_mesh *m, double *g6, double *B, double *dinv, double *c, double *xyz, double *jac);

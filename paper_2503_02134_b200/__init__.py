@@ -24,7 +24,7 @@ import numpy as np
 from ._build import LIB, build as _build_lib
 
 NB_FP64, NB_FP32, NB_MIXED, NB_FP32_DOT2 = 0, 1, 2, 3
-NB_GS_CONSISTENT, NB_GS_PER_COPY = 0, 1
+NB_GS_CONSISTENT, NB_GS_PER_COPY, NB_GS_PAIRWISE, NB_GS_ALLREDUCE = 0, 1, 2, 3
 NB_PC_JACOBI, NB_PC_IDENTITY, NB_PC_JACOBI_F32 = 0, 1, 2
 NB_RHS_UNIFORM, NB_RHS_MANUFACTURED = 0, 1
 NB_AX_LOCAL = 1
@@ -32,7 +32,7 @@ NB_CONVERGED, NB_MAXITER, NB_STAGNATED, NB_BROKEDOWN = 0, 1, 2, 3
 NB_OK, NB_EINVAL, NB_ENOMEM, NB_ECUDA, NB_EGEOM, NB_EBREAKDOWN, NB_ESTATE, NB_ETIMEOUT = range(8)
 POLICY_NAMES = {NB_FP64: "fp64", NB_FP32: "fp32", NB_MIXED: "mixed", NB_FP32_DOT2: "fp32_dot2"}
 
-EXPORTED = ["nb_setup", "nb_setup_slab", "nb_destroy", "nb_query", "nb_rhs", "nb_ax", "nb_dssum", "nb_cg",
+EXPORTED = ["nb_setup", "nb_setup_slab", "nb_destroy", "nb_query", "nb_rhs", "nb_ax", "nb_dssum", "nb_dssum_ranked", "nb_cg",
             "nb_cg_host", "nb_cg_group", "nb_peer_export", "nb_peer_attach", "nb_peer_detach", "nb_export_maps",
             "nb_export_geom", "nb_export_basis", "nb_last_error", "nb_version"]
 NB_PEER_BLOB_BYTES = 256
@@ -55,7 +55,8 @@ class nb_info(C.Structure):
 class nb_cg_opts(C.Structure):
     _fields_ = [("policy", C.c_int), ("max_iter", C.c_int32), ("rtol", C.c_double), ("gs_order", C.c_int),
                 ("stag_window", C.c_int32), ("reserved0", C.c_int32), ("rel_res_history", C.c_void_p),
-                ("precond", C.c_int), ("x_fp64", C.c_int32), ("scal_history", C.c_void_p)]
+                ("precond", C.c_int), ("x_fp64", C.c_int32), ("scal_history", C.c_void_p),
+                ("ranks", C.c_int32 * 3)]
 
 
 class nb_cg_report(C.Structure):
@@ -93,6 +94,7 @@ def lib(auto_build: bool = True):
     L.nb_rhs.argtypes = [P, I, D, U64, I, P, P]
     L.nb_ax.argtypes = [P, I, P, P, C.c_uint32, P]
     L.nb_dssum.argtypes = [P, I, I, P, P]
+    L.nb_dssum_ranked.argtypes = [P, I, I, C.c_int32, C.c_int32, C.c_int32, P, P]
     L.nb_cg.argtypes = [P, C.POINTER(nb_cg_opts), P, P, C.POINTER(nb_cg_report), P]
     L.nb_cg_host.argtypes = [P, C.POINTER(nb_cg_opts), P, P, C.POINTER(nb_cg_report), P]
     L.nb_export_maps.argtypes = [P, P, P, P, P]
@@ -241,8 +243,16 @@ def nb_dssum(h, prec: int, order: int, u, stream=None):
     _check(lib().nb_dssum(h, prec, order, _dptr(u, policy_dtype(prec)), _stream(stream)))
 
 
-def _opts(policy, max_iter, rtol, gs_order, stag_window, hist, precond=NB_PC_JACOBI, x64=False, scal=None):
+def nb_dssum_ranked(h, prec: int, order: int, ranks, u, stream=None):
+    px, py, pz = ranks
+    _check(lib().nb_dssum_ranked(h, prec, order, px, py, pz, _dptr(u, policy_dtype(prec)), _stream(stream)))
+
+
+def _opts(policy, max_iter, rtol, gs_order, stag_window, hist, precond=NB_PC_JACOBI, x64=False, scal=None,
+          ranks=None):
     o = nb_cg_opts()
+    if ranks is not None:
+        o.ranks[0], o.ranks[1], o.ranks[2] = ranks
     o.policy, o.max_iter, o.rtol, o.gs_order = policy, max_iter, rtol, gs_order
     o.stag_window, o.reserved0 = stag_window, 0
     o.precond, o.x_fp64 = precond, int(x64)
@@ -256,13 +266,14 @@ def _opts(policy, max_iter, rtol, gs_order, stag_window, hist, precond=NB_PC_JAC
 def nb_cg(h, b, x, policy: int = NB_MIXED, max_iter: int = 1000, rtol: float = 1e-8,
           gs_order: int = NB_GS_CONSISTENT, stag_window: int = 200,
           history: bool = True, stream=None, allow_breakdown: bool = True, precond: int = NB_PC_JACOBI,
-          x64: bool = False, scal_out: np.ndarray | None = None):
+          x64: bool = False, scal_out: np.ndarray | None = None, ranks=None):
     """PCG from x0 = 0; returns (report, rel_res_history).  x is float64 when x64.
-    scal_out (float64, >= 3*max_iter): receives rho_k, alpha_k, beta_k per iteration."""
+    scal_out (float64, >= 3*max_iter): receives rho_k, alpha_k, beta_k per iteration.
+    ranks (px, py, pz): partition of gs_order NB_GS_PAIRWISE / NB_GS_ALLREDUCE."""
     import torch
     dt = policy_dtype(policy)
     hist = np.zeros(max_iter + 1) if history else None
-    o = _opts(policy, max_iter, rtol, gs_order, stag_window, hist, precond, x64, scal_out)
+    o = _opts(policy, max_iter, rtol, gs_order, stag_window, hist, precond, x64, scal_out, ranks)
     rep = nb_cg_report()
     rc = lib().nb_cg(h, C.byref(o), _dptr(b, dt), _dptr(x, torch.float64 if x64 else dt), C.byref(rep),
                      _stream(stream))
@@ -385,17 +396,20 @@ class Mesh:
         nb_ax(self.h, policy, u, w, NB_AX_LOCAL if local else 0)
         return w
 
-    def dssum(self, u, policy, order=NB_GS_CONSISTENT):
+    def dssum(self, u, policy, order=NB_GS_CONSISTENT, ranks=None):
         v = u.clone()
-        nb_dssum(self.h, policy, order, v)
+        if ranks is None:
+            nb_dssum(self.h, policy, order, v)
+        else:
+            nb_dssum_ranked(self.h, policy, order, ranks, v)
         return v
 
     def cg(self, b, policy=NB_MIXED, max_iter=1000, rtol=1e-8, gs_order=NB_GS_CONSISTENT, stag_window=200,
-           precond=NB_PC_JACOBI, x64=False, scalars=False):
+           precond=NB_PC_JACOBI, x64=False, scalars=False, ranks=None):
         x = self.empty(NB_FP64 if x64 else policy)
         sc = np.zeros(3 * max(max_iter, 1)) if scalars else None
         rep, hist = nb_cg(self.h, b, x, policy, max_iter, rtol, gs_order, stag_window,
-                          precond=precond, x64=x64, scal_out=sc)
+                          precond=precond, x64=x64, scal_out=sc, ranks=ranks)
         r = CgResult(rep.iterations, rep.status, rep.rtr0, rep.rel_res_final, rep.rel_res_min, rep.solve_ms,
                      rep.kernel_launches, rep.k_ax_ms, rep.k_gs_ms, rep.k_upd_ms, hist,
                      sc[: 3 * rep.iterations].reshape(-1, 3) if sc is not None else None)

@@ -439,17 +439,29 @@ int nb_ax(nb_handle *h, nb_policy prec, const void *u, void *w, uint32_t flags, 
     return NB_OK;
 }
 
-int nb_dssum(nb_handle *h, nb_policy prec, nb_gs_order order, void *u, void *stream)
+int nb_dssum_ranked(nb_handle *h, nb_policy prec, nb_gs_order order, int32_t px, int32_t py, int32_t pz, void *u,
+                    void *stream)
 {
     if (!h) return fail(NB_EINVAL, "NULL handle");
     if (prec < NB_FP64 || prec > NB_FP32_DOT2) return fail(NB_EINVAL, "bad policy");
     if (prec == NB_FP32_DOT2) prec = NB_FP32;
-    if (order != NB_GS_CONSISTENT && order != NB_GS_PER_COPY) return fail(NB_EINVAL, "bad gs order");
+    if (order < NB_GS_CONSISTENT || order > NB_GS_ALLREDUCE) return fail(NB_EINVAL, "bad gs order");
+    if (px < 1 || py < 1 || pz < 1 || px > h->nelx || py > h->nely || pz > h->nelz)
+        return fail(NB_EINVAL, "rank partition must satisfy 1 <= p_a <= nel_a");
+    if ((order == NB_GS_PAIRWISE || order == NB_GS_ALLREDUCE) && h->nelzl != h->nelz)
+        return fail(NB_EINVAL, "ranked gather-scatter orders need the whole box");
     NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
     int rc = check_dev_ptr(h, u, "u");
     if (rc) return rc;
-    NB_CU(nb::launch_dssum(h, prec, order, u, (cudaStream_t)stream), "dssum");
+    NB_CU(nb::launch_dssum(h, prec, order, u, (cudaStream_t)stream, nb::RankPart{px, py, pz}), "dssum");
     return NB_OK;
+}
+
+int nb_dssum(nb_handle *h, nb_policy prec, nb_gs_order order, void *u, void *stream)
+{
+    if (h && (order == NB_GS_PAIRWISE || order == NB_GS_ALLREDUCE))
+        return fail(NB_EINVAL, "NB_GS_PAIRWISE / NB_GS_ALLREDUCE need a partition: nb_dssum_ranked");
+    return nb_dssum_ranked(h, prec, order, 1, 1, 1, u, stream);
 }
 
 // CUDA events released on every return path
@@ -567,8 +579,10 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
         NB_CU(NB_POL(prec, nb::launch_cg_mr, h0, M, st), "cg multi-rank megakernel");
         launches = 1;
     } else {
+        const nb::RankPart rp{o->ranks[0] > 0 ? o->ranks[0] : 1, o->ranks[1] > 0 ? o->ranks[1] : 1,
+                              o->ranks[2] > 0 ? o->ranks[2] : 1};
         NB_CU(NB_POL(prec, nb::launch_cg_mega, h0, ws0, bdev[0], order, o->max_iter, o->rtol, (int)o->precond,
-                     (int)o->x_fp64, ws0.tim, st),
+                     (int)o->x_fp64, ws0.tim, st, rp),
               "cg megakernel");
         launches = 1;
     }
@@ -665,7 +679,14 @@ static int cg_args(nb_handle *h, const nb_cg_opts *o)
     if (o->x_fp64 != 0 && o->x_fp64 != 1) return fail(NB_EINVAL, "x_fp64 must be 0 or 1");
     if (o->reserved0 != 0) return fail(NB_EINVAL, "nb_cg_opts.reserved0 must be 0");
     if (o->x_fp64 && o->policy != NB_MIXED) return fail(NB_EINVAL, "x_fp64 applies to NB_MIXED only");
-    if (o->gs_order != NB_GS_CONSISTENT && o->gs_order != NB_GS_PER_COPY) return fail(NB_EINVAL, "bad gs order");
+    if (o->gs_order < NB_GS_CONSISTENT || o->gs_order > NB_GS_ALLREDUCE) return fail(NB_EINVAL, "bad gs order");
+    if (o->gs_order == NB_GS_PAIRWISE || o->gs_order == NB_GS_ALLREDUCE) {
+        const int32_t nel[3] = {h->nelx, h->nely, h->nelz};
+        for (int a = 0; a < 3; a++)
+            if (o->ranks[a] < 0 || o->ranks[a] > nel[a])
+                return fail(NB_EINVAL, "ranks[a] must be in [1, nel_a] (0 = 1)");
+        if (h->nelzl != h->nelz) return fail(NB_EINVAL, "ranked gather-scatter orders need the whole box");
+    }
     if (o->max_iter < 0 || !(o->rtol >= 0.0)) return fail(NB_EINVAL, "bad max_iter/rtol");
     if (h->n_unmasked == 0) return fail(NB_EINVAL, "the mesh has no unknowns (every node is on the Dirichlet boundary)");
     NB_CU(cudaSetDevice(h->device), "cudaSetDevice");

@@ -1223,7 +1223,7 @@ cudaError_t launch_ax_local(const nb_handle *h, const void *u, void *w, bool mas
     template int grid_mega<P>(const nb_handle *);                                                             \
     template int grid_mega_var<P, 0>(const nb_handle *);                                                      \
     template cudaError_t launch_cg_mega<P>(const nb_handle *, Workspace &, const void *, int, int, double,    \
-                                           int, int, unsigned long long *, cudaStream_t);                     \
+                                           int, int, unsigned long long *, cudaStream_t, RankPart);           \
     template cudaError_t launch_cg_mega_var<P, 0>(const nb_handle *, const MegaArgs &, bool, cudaStream_t);
 // the variant (VAR = 1) megakernels: their own translation units (parallel build)
 #define NB_INSTANTIATE_CG_VAR(P)                                                                              \

@@ -48,6 +48,11 @@ struct PeerState {
     int nopened = 0;
 };
 
+// Rank partition of the NB_GS_PAIRWISE / NB_GS_ALLREDUCE gather-scatter orders (NEXT-2)
+struct RankPart {
+    int32_t px, py, pz;
+};
+
 // Geometry needed by kernels, passed by value.
 struct MeshDev {
     int32_t nelx, nely, nelz, p, n;   // the whole box (nelz: global layer count)
@@ -66,7 +71,8 @@ struct MegaArgs {
     const void *g, *dinv;
     const int32_t *gs_off, *gs_idx;
     int32_t nseg;
-    int32_t order;          // NB_GS_CONSISTENT / NB_GS_PER_COPY
+    int32_t order;          // NB_GS_CONSISTENT / NB_GS_PER_COPY / NB_GS_PAIRWISE / NB_GS_ALLREDUCE
+    RankPart rp;            // partition of the ranked orders
     int32_t max_iter;
     double rtol;
     double *hist;           // [max_iter + 1]
@@ -177,7 +183,8 @@ cudaError_t launch_rhs(const nb_handle *h, int kind, double noise, uint64_t seed
 
 // ---- CSR gather-scatter (nb_gs.cu) ----
 int grid_gs(const nb_handle *h);
-cudaError_t launch_dssum(const nb_handle *h, int prec, int order, void *u, cudaStream_t st);
+cudaError_t launch_dssum(const nb_handle *h, int prec, int order, void *u, cudaStream_t st,
+                         RankPart rp = RankPart{1, 1, 1});
 
 // ---- Ax + CG kernels, one translation unit per policy (nb_cg_<policy>.cu) ----
 template <int PREC> cudaError_t launch_ax_local(const nb_handle *h, const void *u, void *w, bool mask, cudaStream_t st);
@@ -196,6 +203,6 @@ template <int PREC, int VAR>
 cudaError_t launch_cg_mega_var(const nb_handle *h, const MegaArgs &A, bool fused, cudaStream_t st);
 template <int PREC> cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int order,
                                               int max_iter, double rtol, int precond, int x64,
-                                              unsigned long long *tim, cudaStream_t st);
+                                              unsigned long long *tim, cudaStream_t st, RankPart rp);
 
 }  // namespace nb

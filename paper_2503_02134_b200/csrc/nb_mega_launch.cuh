@@ -128,6 +128,7 @@ void fill_mega_args(const nb_handle *h, Workspace &ws, const void *b, int order,
                                                                                   : (const void *)h->dinv64;
     A.gs_off = h->gs_off; A.gs_idx = h->gs_idx; A.nseg = (int32_t)h->nseg;
     A.order = order; A.max_iter = max_iter; A.rtol = rtol;
+    A.rp = RankPart{1, 1, 1};
     A.hist = ws.hist; A.shist = ws.shist; A.tim = tim;
     // per-block partials: W doubles per accumulator (2 for the Dot2 expansions)
     const size_t W = (size_t)Acc<PREC>::W;
@@ -140,11 +141,12 @@ void fill_mega_args(const nb_handle *h, Workspace &ws, const void *b, int order,
 
 template <int PREC>
 cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int order, int max_iter, double rtol,
-                           int precond, int x64, unsigned long long *tim, cudaStream_t st)
+                           int precond, int x64, unsigned long long *tim, cudaStream_t st, RankPart rp)
 {
     MegaArgs A;
     fill_mega_args<PREC>(h, ws, b, order, max_iter, rtol, precond, x64, tim, A);
     A.wlo = A.whi = nullptr;
+    A.rp = rp;
     const bool fused = order == NB_GS_CONSISTENT && !h->cg_csr;
     cudaError_t e = cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned int), st);   // barrier epoch 0
     if (e != cudaSuccess) return e;
