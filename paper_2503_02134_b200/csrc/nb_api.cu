@@ -263,6 +263,8 @@ static int setup_box(nb_handle *h, bool jacobi)
         h->cg_csr = (gs && std::strcmp(gs, "csr") == 0) ? 1 : 0;
         const char *po = std::getenv("NB_PHASE_ONLY");   // measurement knob (tools/ncu_phases.sh)
         h->phase_only = po ? (po[0] == 'A' ? 1 : po[0] == 'B' ? 2 : 0) : 0;
+        const char *dc = std::getenv("NB_DSSUM");         // consistent nb_dssum: structured (default) or CSR
+        h->dssum_csr = (dc && std::strcmp(dc, "csr") == 0) ? 1 : 0;
     }
     if ((e = cudaMalloc(&h->g64, sizeof(double) * 6 * NL)) != cudaSuccess) return fail(NB_ENOMEM, "cudaMalloc g64");
     if ((e = cudaMalloc(&h->B, sizeof(double) * NL)) != cudaSuccess) return fail(NB_ENOMEM, "cudaMalloc B");

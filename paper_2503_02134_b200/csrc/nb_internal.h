@@ -156,6 +156,7 @@ struct nb_handle {
     cudaStream_t cap_stream = nullptr;   // private stream used for setup
     int cg_csr = 0;             // 1: consistent-order CG also through the CSR dssum kernel (A/B)
     int phase_only = 0;         // NB_PHASE_ONLY=A (1) / B (2): measurement runs of one megakernel phase
+    int dssum_csr = 0;          // NB_DSSUM=csr: consistent nb_dssum through the CSR kernel (A/B, tests)
     nb::Workspace ws[4];   // one per nb_policy
     nb::MeshDev md() const {
         nb::MeshDev m;
