@@ -813,6 +813,62 @@ __device__ __forceinline__ void init_pencil(const MeshDev &m, const typename Pol
 // contiguous even split of [0, n) over `parts`
 __device__ __forceinline__ int64_t split(int64_t n, int parts, int i) { return n * i / parts; }
 
+// ---------------------------------------------------------------------------
+// L2 prefetch distances (l2_prefetch, nb_common.cuh): phase A prefetches the operands of the
+// element group NB_L2PF_A groups ahead (g, z, p_old, x: one contiguous range each), phase B the
+// w, r, dinv ranges of the pencil trip NB_L2PF_B trips ahead; each phase's first ranges are
+// prefetched before the grid barrier that precedes it (they are the block's own data, final
+// before that barrier).  0 = off.
+// ---------------------------------------------------------------------------
+#ifndef NB_L2PF_A
+#define NB_L2PF_A 0
+#endif
+#ifndef NB_L2PF_B
+#define NB_L2PF_B 0
+#endif
+#ifndef NB_L2PF_N8ONLY
+#define NB_L2PF_N8ONLY 0
+#endif
+#ifndef NB_L2PF_LEAD
+#define NB_L2PF_LEAD 1
+#endif
+// which phase-A ranges (bits: 1 g, 2 z, 4 p_old, 8 x)
+#ifndef NB_L2PF_MASK
+#define NB_L2PF_MASK 15
+#endif
+// the standalone operator k_ax (u and g, one group ahead)
+#ifndef NB_L2PF_AX
+#define NB_L2PF_AX 1
+#endif
+// group grp (EPB elements from grp*EPB, clipped to E): threads 0, 32, 64, 96 issue one range each
+template <typename TV, int N, int EPB, int MASK = NB_L2PF_MASK>
+__device__ __forceinline__ void pf_group(int64_t grp, int64_t gend, int E, const TV *g, const void *z, const void *p,
+                                         const void *x, int xsz)
+{
+    constexpr int64_t N3 = N * N * N;
+    const int t = threadIdx.x;
+    if ((t & 31) || t >= 128 || grp >= gend) return;
+    const int64_t e0 = grp * EPB;
+    if (e0 >= E) return;
+    const int64_t ne = min((int64_t)EPB, (int64_t)E - e0);
+    if (t == 0 && (MASK & 1)) l2_prefetch(g + e0 * 6 * N3, (size_t)(ne * 6 * N3) * sizeof(TV));
+    else if (t == 32 && z && (MASK & 2)) l2_prefetch((const TV *)z + e0 * N3, (size_t)(ne * N3) * sizeof(TV));
+    else if (t == 64 && p && (MASK & 4)) l2_prefetch((const TV *)p + e0 * N3, (size_t)(ne * N3) * sizeof(TV));
+    else if (t == 96 && x && (MASK & 8)) l2_prefetch((const char *)x + e0 * N3 * xsz, (size_t)(ne * N3) * xsz);
+}
+// phase-B pencils [pb, min(pb + blockDim, pend)): w, r and the diagonal (dsz bytes per value, 0: none)
+template <typename TV, int N>
+__device__ __forceinline__ void pf_trip(int64_t pb, int64_t pend, const void *w, const void *r, const void *dinv,
+                                        int dsz)
+{
+    const int t = threadIdx.x;
+    if ((t & 31) || t >= 96 || pb >= pend) return;
+    const int64_t np = min((int64_t)blockDim.x, pend - pb);
+    if (t == 0) l2_prefetch((const TV *)w + pb * N, (size_t)(np * N) * sizeof(TV));
+    else if (t == 32) l2_prefetch((const TV *)r + pb * N, (size_t)(np * N) * sizeof(TV));
+    else if (dsz) l2_prefetch((const char *)dinv + pb * N * dsz, (size_t)(np * N) * dsz);
+}
+
 // ===========================================================================
 // persistent cooperative megakernel: the whole solve in one launch
 // ===========================================================================
@@ -1149,8 +1205,13 @@ k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
     TV *S0 = reinterpret_cast<TV *>(smraw) + (el < C::EPB ? el : 0) * C::NARR * C::ESZ;
     const int64_t ngroups = ((int64_t)m.E + C::EPB - 1) / C::EPB;
     const int64_t g0 = split(ngroups, gridDim.x, blockIdx.x), g1 = split(ngroups, gridDim.x, blockIdx.x + 1);
+    // u and g of the next group into L2 (measured at 32^3: mixed p9 323 -> 270 us, p11 587 -> 406 us,
+    // fp64 p9 721 -> 634 us; fp64 p7 slower, 226 -> 240 us, so not there)
+    constexpr bool PF = NB_L2PF_AX && !(sizeof(TV) == 8 && N == 8);
+    if (PF) pf_group<TV, N, C::EPB, 3>(g0, g1, m.E, g, in, nullptr, nullptr, 0);
 #pragma unroll 1
     for (int64_t gr = g0; gr < g1; gr++) {
+        if (PF) pf_group<TV, N, C::EPB, 3>(gr + 1, g1, m.E, g, in, nullptr, nullptr, 0);
         const int e = (int)(gr * C::EPB) + el;
         const bool active = el < C::EPB && (C::N2P == C::N2 || C::HALF || q < C::N2) && e < m.E;
         // the handle may be a z-slab (global mask layers): SLAB = true
