@@ -28,6 +28,7 @@ CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-st
 FP64, FP32, MIXED, FP32_DOT2 = 0, 1, 2, 3
 GS_CONSISTENT, GS_PER_COPY, GS_PAIRWISE, GS_ALLREDUCE = 0, 1, 2, 3
 PC_JACOBI, PC_IDENTITY, PC_JACOBI_F32 = 0, 1, 2   # or_cg precond
+PC_SCHWARZ = 3                                    # two-level Schwarz
 RHS_UNIFORM, RHS_MANUFACTURED = 0, 1
 CONVERGED, MAXITER, STAGNATED, BREAKDOWN = 0, 1, 2, 3
 
@@ -90,6 +91,9 @@ def lib():
         L.or_glsc3_f_dot2.argtypes = [P, P, P, C.c_int64]
         L.or_two_sum_f.argtypes = [C.c_float, C.c_float, P, P]
         L.or_two_prod_f.argtypes = [C.c_float, C.c_float, P, P]
+        L.or_schwarz_apply_d.argtypes = [P, P, P]
+        L.or_schwarz_apply_f.argtypes = [P, C.c_int, P, P]
+        L.or_schwarz_tables.argtypes = [P, C.c_int, C.c_int, P, P, P, P, P, P]
         L.or_cg.argtypes = [P, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                             C.c_int, P, P, P, P, C.POINTER(_Report)]
         _lib = L
@@ -220,6 +224,31 @@ class Mesh:
             w = np.zeros_like(u)
             lib().or_ax_f(self._h, policy, order, _p(u), _p(w))
         return w
+
+    def schwarz(self, r: np.ndarray, policy: int = FP64) -> np.ndarray:
+        """NEXT-4: z = M^-1 r of the two-level Schwarz preconditioner under a policy."""
+        if policy == FP64:
+            r = np.ascontiguousarray(r, dtype=np.float64)
+            z = np.zeros_like(r)
+            lib().or_schwarz_apply_d(self._h, _p(r), _p(z))
+        else:
+            r = np.ascontiguousarray(r, dtype=np.float32)
+            z = np.zeros_like(r)
+            if lib().or_schwarz_apply_f(self._h, policy, _p(r), _p(z)):
+                raise ValueError("or_schwarz_apply_f: bad arguments")
+        return z
+
+    def schwarz_tables(self, axis: int, ex: int):
+        """(t0, nt, S, lam, S0, lam0) of the fast-diagonalisation tables (axis 0/1/2, element position ex)."""
+        p3 = self.p + 3
+        nv = self.dims[axis] - 1
+        t0, nt = C.c_int(0), C.c_int(0)
+        S, lam = np.zeros((p3, p3)), np.zeros(p3)
+        S0, lam0 = np.zeros((max(nv, 1), max(nv, 1))), np.zeros(max(nv, 1))
+        if lib().or_schwarz_tables(self._h, axis, ex, C.byref(t0), C.byref(nt), _p(S), _p(lam), _p(S0), _p(lam0)):
+            raise ValueError("or_schwarz_tables: bad arguments")
+        k = t0.value, nt.value
+        return k[0], k[1], S[: k[1], : k[1]], lam[: k[1]], S0[:nv, :nv], lam0[:nv]
 
     def cg(self, b64: np.ndarray, policy: int = FP64, max_iter: int = 100, rtol: float = 0.0,
            gs_order: int = GS_CONSISTENT, stag_window: int = 200, seqdot: bool = False,

@@ -90,12 +90,28 @@ float or_glsc3_f_dot2(const float *a, const float *c, const float *b, int64_t n)
  * precond: OR_PC_JACOBI = the policy's Jacobi (C-10 table);
  *   OR_PC_IDENTITY = none, z = r ("CG with the identity ... preconditioner");
  *   OR_PC_JACOBI_F32 = Neko's single-precision copy of the Jacobi diagonal, z = r * (float)dinv in
- *   binary32 -- for fp32/dot2 the same as OR_PC_JACOBI; rejected for fp64.
+ *   binary32 -- for fp32/dot2 the same as OR_PC_JACOBI; rejected for fp64;
+ *   OR_PC_SCHWARZ = the NEXT-4 two-level Schwarz preconditioner below (the policy's variant).
  * scal: nullable, len 3*max_iter: scal[3(k-1) + 0..2] = rho_k, alpha_k, beta_k of iteration k (the
  *   policy's own scalar values widened to double: binary64 under fp64/mixed, binary32 under fp32).
  * Returns 0, or 1 on bad arguments.
  */
-enum { OR_PC_JACOBI = 0, OR_PC_IDENTITY = 1, OR_PC_JACOBI_F32 = 2 };
+enum { OR_PC_JACOBI = 0, OR_PC_IDENTITY = 1, OR_PC_JACOBI_F32 = 2, OR_PC_SCHWARZ = 3 };
+/*
+ * NEXT-4: two-level overlapping Schwarz preconditioner z = M^-1 r on the local
+ * copies (reading 28):
+ *   M^-1 = sum_e R_e^T W K_e^-1 W R_e + Phi A0^-1 Phi^T, W = diag(1/sqrt(overlap count)),
+ * K_e the 1-D Kronecker-sum operator of the element box extended by one GLL layer, A0 its
+ * Galerkin coarse operator on the interior element vertices; both by fast diagonalisation.
+ * _d: fp64.  _f: policy OR_MIXED (fp32 arithmetic, sqrt / weights and the sums over subdomains
+ * in fp64) or OR_FP32 / OR_FP32_DOT2 (all fp32).  Also or_cg(precond = OR_PC_SCHWARZ).
+ * or_schwarz_tables: the 1-D tables of axis a (0 x, 1 y, 2 z) at element position ex: first
+ * lattice index and size of the extended index set, S ((p+3) x (p+3), row-major) and lambda
+ * (p+3); the coarse S0 (nv x nv, nv = nel_a - 1) and lambda0 (nullable outputs).
+ */
+int or_schwarz_apply_d(or_mesh *m, const double *r, double *z);
+int or_schwarz_apply_f(or_mesh *m, int policy, const float *r, float *z);
+int or_schwarz_tables(or_mesh *m, int axis, int ex, int *t0, int *nt, double *S, double *lam, double *S0, double *lam0);
 int or_cg(const or_mesh *m, int policy, int max_iter, double rtol, int gs_order, int stag_window,
           int seqdot, int x64, int precond, const double *b64, double *x_out, double *hist, double *scal,
           or_report *rep);
