@@ -109,8 +109,18 @@ typedef struct {
  *   NB_PC_IDENTITY  : none, z = r -- "CG with the identity ... preconditioner".
  *   NB_PC_JACOBI_F32: Neko's "single precision copy of the preconditioner":
  *                     z = r * (float)dinv in binary32.  Same as NB_PC_JACOBI for NB_FP32 /
- *                     NB_FP32_DOT2; NB_EINVAL for NB_FP64. */
-typedef enum { NB_PC_JACOBI = 0, NB_PC_IDENTITY = 1, NB_PC_JACOBI_F32 = 2 } nb_precond;
+ *                     NB_FP32_DOT2; NB_EINVAL for NB_FP64.
+ *   NB_PC_SCHWARZ   : the two-level overlapping Schwarz preconditioner of SURVEY.md §8(f) NEXT-4
+ *                     (reading 28; Nekbone's multigrid-preconditioned CG, PAPER.md:160,
+ *                     :324-328, :537, :704-709): M^-1 = sum_e R_e^T W K_e^-1 W R_e + Phi A0^-1 Phi^T,
+ *                     local solves on the element boxes extended by one GLL layer by fast
+ *                     diagonalisation, weights W = 1/sqrt(overlap count) ("the square roots"),
+ *                     Galerkin coarse level on the interior element vertices.  Precision: the
+ *                     policy's vector type for the fast-diagonalisation arithmetic; square roots,
+ *                     weights and the sums over subdomains in the gather-scatter precision (fp64
+ *                     under NB_MIXED, the paper's "sqrt and GS in fp64").  Whole-box handles,
+ *                     consistent GS order only (NB_EINVAL otherwise). */
+typedef enum { NB_PC_JACOBI = 0, NB_PC_IDENTITY = 1, NB_PC_JACOBI_F32 = 2, NB_PC_SCHWARZ = 3 } nb_precond;
 
 typedef struct {
     nb_policy policy;
@@ -192,6 +202,12 @@ int nb_dssum_ranked(nb_handle *h, nb_policy prec, nb_gs_order order, int32_t px,
  * (report filled in either case); NB_EINVAL for bad options or a mesh without unknowns
  * (every node on the Dirichlet boundary, e.g. p = 1 with one element along an axis). */
 int nb_cg(nb_handle *h, const nb_cg_opts *o, const void *b, void *x, nb_cg_report *rep, void *stream);
+
+/* solveM alone (Table 2 line 2): z = M^-1 r for `pc` = NB_PC_SCHWARZ (the NEXT-4
+ * preconditioner of nb_cg, same arithmetic).  r, z: device, distinct, policy precision; r must be
+ * continuous and masked.  Builds the handle's Schwarz tables on first use (synchronizes then).
+ * One cooperative launch.  Errors: NB_EINVAL (other pc, slab handle, aliasing), NB_ECUDA. */
+int nb_precond_apply(nb_handle *h, nb_policy prec, nb_precond pc, const void *r, void *z, void *stream);
 
 /* Same solve with HOST buffers (pinned or pageable): copies b in and x out on `stream`. */
 int nb_cg_host(nb_handle *h, const nb_cg_opts *o, const void *b_host, void *x_host,

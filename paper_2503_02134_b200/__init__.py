@@ -25,14 +25,14 @@ from ._build import LIB, build as _build_lib
 
 NB_FP64, NB_FP32, NB_MIXED, NB_FP32_DOT2 = 0, 1, 2, 3
 NB_GS_CONSISTENT, NB_GS_PER_COPY, NB_GS_PAIRWISE, NB_GS_ALLREDUCE = 0, 1, 2, 3
-NB_PC_JACOBI, NB_PC_IDENTITY, NB_PC_JACOBI_F32 = 0, 1, 2
+NB_PC_JACOBI, NB_PC_IDENTITY, NB_PC_JACOBI_F32, NB_PC_SCHWARZ = 0, 1, 2, 3
 NB_RHS_UNIFORM, NB_RHS_MANUFACTURED = 0, 1
 NB_AX_LOCAL = 1
 NB_CONVERGED, NB_MAXITER, NB_STAGNATED, NB_BROKEDOWN = 0, 1, 2, 3
 NB_OK, NB_EINVAL, NB_ENOMEM, NB_ECUDA, NB_EGEOM, NB_EBREAKDOWN, NB_ESTATE, NB_ETIMEOUT = range(8)
 POLICY_NAMES = {NB_FP64: "fp64", NB_FP32: "fp32", NB_MIXED: "mixed", NB_FP32_DOT2: "fp32_dot2"}
 
-EXPORTED = ["nb_setup", "nb_setup_slab", "nb_destroy", "nb_query", "nb_rhs", "nb_ax", "nb_dssum", "nb_dssum_ranked", "nb_cg",
+EXPORTED = ["nb_setup", "nb_setup_slab", "nb_destroy", "nb_query", "nb_rhs", "nb_ax", "nb_dssum", "nb_dssum_ranked", "nb_precond_apply", "nb_cg",
             "nb_cg_host", "nb_cg_group", "nb_peer_export", "nb_peer_attach", "nb_peer_detach", "nb_export_maps",
             "nb_export_geom", "nb_export_basis", "nb_last_error", "nb_version"]
 NB_PEER_BLOB_BYTES = 256
@@ -95,6 +95,7 @@ def lib(auto_build: bool = True):
     L.nb_ax.argtypes = [P, I, P, P, C.c_uint32, P]
     L.nb_dssum.argtypes = [P, I, I, P, P]
     L.nb_dssum_ranked.argtypes = [P, I, I, C.c_int32, C.c_int32, C.c_int32, P, P]
+    L.nb_precond_apply.argtypes = [P, I, I, P, P, P]
     L.nb_cg.argtypes = [P, C.POINTER(nb_cg_opts), P, P, C.POINTER(nb_cg_report), P]
     L.nb_cg_host.argtypes = [P, C.POINTER(nb_cg_opts), P, P, C.POINTER(nb_cg_report), P]
     L.nb_export_maps.argtypes = [P, P, P, P, P]
@@ -241,6 +242,12 @@ def nb_ax(h, prec: int, u, w, flags: int = 0, stream=None):
 
 def nb_dssum(h, prec: int, order: int, u, stream=None):
     _check(lib().nb_dssum(h, prec, order, _dptr(u, policy_dtype(prec)), _stream(stream)))
+
+
+def nb_precond_apply(h, prec: int, pc: int, r, z, stream=None):
+    """solveM alone: z = M^-1 r (NB_PC_SCHWARZ; nb.h)."""
+    dt = policy_dtype(prec)
+    _check(lib().nb_precond_apply(h, prec, pc, _dptr(r, dt), _dptr(z, dt), _stream(stream)))
 
 
 def nb_dssum_ranked(h, prec: int, order: int, ranks, u, stream=None):
@@ -395,6 +402,11 @@ class Mesh:
         w = self.empty(policy)
         nb_ax(self.h, policy, u, w, NB_AX_LOCAL if local else 0)
         return w
+
+    def precond(self, r, policy, pc=NB_PC_SCHWARZ):
+        z = self.empty(policy)
+        nb_precond_apply(self.h, policy, pc, r, z)
+        return z
 
     def dssum(self, u, policy, order=NB_GS_CONSISTENT, ranks=None):
         v = u.clone()

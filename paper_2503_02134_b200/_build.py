@@ -16,9 +16,11 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.environ.get("NB_LIBPATH") or os.path.join(PKG, "libnb.so")
 UNITS = ("nb_api.cu", "nb_setup_k.cu", "nb_gs.cu", "nb_cg_fp64.cu", "nb_cg_fp32.cu", "nb_cg_mixed.cu",
-         "nb_cg_dot2.cu", "nb_cg_fp64_var.cu", "nb_cg_fp32_var.cu", "nb_cg_mixed_var.cu", "nb_cg_dot2_var.cu")
+         "nb_cg_dot2.cu", "nb_cg_fp64_var.cu", "nb_cg_fp32_var.cu", "nb_cg_mixed_var.cu", "nb_cg_dot2_var.cu",
+         "nb_cg_fp64_sw.cu", "nb_cg_fp32_sw.cu", "nb_cg_mixed_sw.cu", "nb_cg_dot2_sw.cu", "nb_sw_setup.cu")
 SOURCES = [os.path.join(CSRC, f) for f in UNITS]
-HEADERS = [os.path.join(CSRC, f) for f in ("nb_internal.h", "nb_common.cuh", "nb_cg.cuh", "nb_mega_body.inc", "nb_gs.cuh", "nb_mega_launch.cuh")] + [
+HEADERS = [os.path.join(CSRC, f) for f in ("nb_internal.h", "nb_common.cuh", "nb_cg.cuh", "nb_mega_body.inc", "nb_gs.cuh",
+                                           "nb_mega_launch.cuh", "nb_schwarz.cuh")] + [
     os.path.join(ROOT, "include", "nb.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -53,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lcusolver"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

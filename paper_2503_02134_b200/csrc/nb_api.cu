@@ -378,6 +378,7 @@ int nb_destroy(nb_handle *h)
     cudaSetDevice(h->device);
     if (h->ext) nb_destroy(h->ext);
     for (auto &ws : h->ws) free_ws(ws);
+    nb::sw_free(h);
     cudaFree(h->g64); cudaFree(h->g32); cudaFree(h->B); cudaFree(h->dinv64); cudaFree(h->dinv32);
     cudaFree(h->gs_off); cudaFree(h->gs_idx); cudaFree(h->flag);
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
@@ -498,6 +499,8 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
         nb_handle *h = hs[r];
         if (prec != NB_FP64 && (rc = ensure_f32(h))) return rc;
         if ((rc = ensure_ws(h, prec, o->max_iter))) return rc;
+        const char *swm = "";
+        if (o->precond == NB_PC_SCHWARZ && (rc = nb::sw_ensure(h, prec, &swm))) return fail(rc, swm);
         nb::Workspace &ws = h->ws[prec];
         if (o->x_fp64 && !ws.xd) NB_CU(cudaMalloc(&ws.xd, sizeof(double) * h->NL), "cudaMalloc xd");
     }
@@ -579,6 +582,17 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
         M.mr.Gr = NB_POL(prec, nb::grid_mega_mr, h0) / nh;
         if (M.mr.Gr < 1) return fail(NB_EINVAL, "too many slabs for one launch");
         NB_CU(NB_POL(prec, nb::launch_cg_mr, h0, M, st), "cg multi-rank megakernel");
+        launches = 1;
+    } else if (o->precond == NB_PC_SCHWARZ) {
+        // NEXT-4: the Schwarz-preconditioned megakernel (k_cg_sw)
+        nb::MegaArgs A;
+        memset(&A, 0, sizeof(A));
+        NB_POL(prec, nb::fill_mega_args, h0, ws0, bdev[0], order, o->max_iter, o->rtol, (int)o->precond,
+               (int)o->x_fp64, ws0.tim, A);
+        A.wlo = A.whi = nullptr;
+        nb::sw_fill(h0, prec, A.sw);
+        NB_CU(cudaMemsetAsync(ws0.bar, 0, 2 * sizeof(unsigned int), st), "memset bar");
+        NB_CU(NB_POL(prec, nb::launch_cg_sw, h0, A, ws0.mega_G, false, st), "cg Schwarz megakernel");
         launches = 1;
     } else {
         const nb::RankPart rp{o->ranks[0] > 0 ? o->ranks[0] : 1, o->ranks[1] > 0 ? o->ranks[1] : 1,
@@ -675,7 +689,12 @@ static int cg_args(nb_handle *h, const nb_cg_opts *o)
 {
     if (!h || !o) return fail(NB_EINVAL, "NULL argument");
     if (o->policy < NB_FP64 || o->policy > NB_FP32_DOT2) return fail(NB_EINVAL, "bad policy");
-    if (o->precond < NB_PC_JACOBI || o->precond > NB_PC_JACOBI_F32) return fail(NB_EINVAL, "bad precond");
+    if (o->precond < NB_PC_JACOBI || o->precond > NB_PC_SCHWARZ) return fail(NB_EINVAL, "bad precond");
+    if (o->precond == NB_PC_SCHWARZ) {
+        if (o->gs_order != NB_GS_CONSISTENT) return fail(NB_EINVAL, "NB_PC_SCHWARZ runs with the consistent GS order");
+        if (h->nelzl != h->nelz || h->ws[o->policy].peer.nrank > 0)
+            return fail(NB_EINVAL, "NB_PC_SCHWARZ needs a whole-box handle (no slabs, no peers)");
+    }
     if (o->precond == NB_PC_JACOBI_F32 && o->policy == NB_FP64)
         return fail(NB_EINVAL, "NB_PC_JACOBI_F32 is a single-precision variant (not for NB_FP64)");
     if (o->x_fp64 != 0 && o->x_fp64 != 1) return fail(NB_EINVAL, "x_fp64 must be 0 or 1");
@@ -715,6 +734,33 @@ int nb_cg(nb_handle *h, const nb_cg_opts *o, const void *b, void *x, nb_cg_repor
     if (h->ws[o->policy].peer.nrank > 0 && (rc = mr_args(h, o))) return rc;
     if ((rc = check_dev_ptr(h, b, "b")) || (rc = check_dev_ptr(h, x, "x"))) return rc;
     return cg_impl(h, o, b, false, x, false, rep, (cudaStream_t)stream);
+}
+
+int nb_precond_apply(nb_handle *h, nb_policy prec, nb_precond pc, const void *r, void *z, void *stream)
+{
+    if (!h) return fail(NB_EINVAL, "NULL handle");
+    if (prec < NB_FP64 || prec > NB_FP32_DOT2) return fail(NB_EINVAL, "bad policy");
+    if (pc != NB_PC_SCHWARZ) return fail(NB_EINVAL, "nb_precond_apply: only NB_PC_SCHWARZ has a standalone apply");
+    if (r == z) return fail(NB_EINVAL, "r and z must be distinct");
+    NB_CU(cudaSetDevice(h->device), "cudaSetDevice");
+    int rc;
+    if ((rc = check_dev_ptr(h, r, "r")) || (rc = check_dev_ptr(h, z, "z"))) return rc;
+    if (prec != NB_FP64 && (rc = ensure_f32(h))) return rc;
+    if ((rc = ensure_ws(h, prec, 0))) return rc;
+    const char *swm = "";
+    if ((rc = nb::sw_ensure(h, prec, &swm))) return fail(rc, swm);
+    nb::Workspace &ws = h->ws[prec];
+    nb::MegaArgs A;
+    memset(&A, 0, sizeof(A));
+    A.m = h->md();
+    A.r = const_cast<void *>(r);
+    A.z = z;
+    A.bar = ws.bar;
+    nb::sw_fill(h, prec, A.sw);
+    cudaStream_t st = (cudaStream_t)stream;
+    NB_CU(cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned int), st), "memset bar");
+    NB_CU(NB_POL(prec, nb::launch_cg_sw, h, A, ws.mega_G, true, st), "Schwarz apply");
+    return NB_OK;
 }
 
 int nb_cg_host(nb_handle *h, const nb_cg_opts *o, const void *b_host, void *x_host, nb_cg_report *rep, void *stream)

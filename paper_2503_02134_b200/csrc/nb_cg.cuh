@@ -40,6 +40,7 @@
 #pragma once
 #include "nb_common.cuh"
 #include "nb_gs.cuh"
+#include "nb_schwarz.cuh"
 
 namespace nb {
 
@@ -724,7 +725,7 @@ __device__ __forceinline__ typename Pol<PREC>::TV solve_m(typename Pol<PREC>::TV
     return (TV)((typename Pol<PREC>::TJ)r * d);
 }
 
-template <int PREC, int N, int GATHER, bool SLAB = false>
+template <int PREC, int N, int GATHER, bool SLAB = false, bool SW = false>
 __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ w,
                                            typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
                                            const void *__restrict__ dinv,
@@ -745,7 +746,7 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
     const ElemPos P = elem_pos<SLAB>(m, e);
     ld_pencil<TV, N, NB_WLD>(w + base, ww);
     ld_pencil<TV, N>(r + base, rr);
-    ld_dinv<TJ, N>(dinv, base, pc, dd);
+    if (!SW) ld_dinv<TJ, N>(dinv, base, pc, dd);
     if (GATHER) {
         constexpr int N3 = N * N * N;
         const TV ol = P.ex > 0 ? ldv<NB_WLD>(w + base - N3 + (N - 1)) : TV(0);
@@ -756,18 +757,20 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
 #pragma unroll
     for (int i = 0; i < N; i++) {
         rr[i] = fma(-alpha, ww[i], rr[i]);                   // add2s2(r, w, -alpha)
-        zz[i] = solve_m<PREC>(rr[i], dd[i], pc);              // solveM
         const TS c = (TS)1 / (TS)(mjk * axis_mult(i, N, P.ex, m.nelx));
         const TS rs = (TS)rr[i];
         rtr.add(rs * c, rs);                                 // glsc3(r, c, r)
-        rho.add(rs * c, (TS)zz[i]);                          // glsc3(r, c, z)
+        if (!SW) {                                           // (Schwarz: solveM is its own phase)
+            zz[i] = solve_m<PREC>(rr[i], dd[i], pc);          // solveM
+            rho.add(rs * c, (TS)zz[i]);                      // glsc3(r, c, z)
+        }
     }
     st_pencil<TV, N>(r + base, rr);
-    if (pc != NB_PC_IDENTITY) st_pencil<TV, N>(z + base, zz);
+    if (!SW && pc != NB_PC_IDENTITY) st_pencil<TV, N>(z + base, zz);
 }
 
 // CG prologue for one pencil: r = b, x = 0, p = 0, z = M^-1 r; rtr0 and rho_1 partials.
-template <int PREC, int N, bool SLAB = false>
+template <int PREC, int N, bool SLAB = false, bool SW = false>
 __device__ __forceinline__ void init_pencil(const MeshDev &m, const typename Pol<PREC>::TV *__restrict__ bvec,
                                             typename Pol<PREC>::TV *__restrict__ x, typename Pol<PREC>::TV *__restrict__ pv,
                                             typename Pol<PREC>::TV *__restrict__ r, typename Pol<PREC>::TV *__restrict__ z,
@@ -786,19 +789,21 @@ __device__ __forceinline__ void init_pencil(const MeshDev &m, const typename Pol
     TV rr[N], zz[N], zero[N];
     TD dd[N];
     ld_pencil<TV, N>(bvec + base, rr);
-    ld_dinv<TD, N>(dinv, base, pc, dd);
+    if (!SW) ld_dinv<TD, N>(dinv, base, pc, dd);
     const int mjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz);
 #pragma unroll
     for (int i = 0; i < N; i++) {
         zero[i] = TV(0);
-        zz[i] = solve_m<PREC>(rr[i], dd[i], pc);
         const TS c = (TS)1 / (TS)(mjk * axis_mult(i, N, P.ex, m.nelx));
         const TS rs = (TS)rr[i];
         rtr.add(rs * c, rs);
-        rho.add(rs * c, (TS)zz[i]);
+        if (!SW) {
+            zz[i] = solve_m<PREC>(rr[i], dd[i], pc);
+            rho.add(rs * c, (TS)zz[i]);
+        }
     }
     st_pencil<TV, N>(r + base, rr);
-    if (pc != NB_PC_IDENTITY) st_pencil<TV, N>(z + base, zz);
+    if (!SW && pc != NB_PC_IDENTITY) st_pencil<TV, N>(z + base, zz);
     if (PREC == NB_MIXED && x64) {
         double zd[N];
 #pragma unroll
@@ -1184,6 +1189,53 @@ k_cg_mega_mr(const __grid_constant__ MultiArgs M, const __grid_constant__ DMat<t
 #include "nb_mega_body.inc"
 }
 
+// Schwarz-preconditioned solve (NB_PC_SCHWARZ): the same body with the
+// preconditioner phases of nb_schwarz.cuh between phase B and the next phase A (VAR = 3).
+template <int PREC, int N>
+__global__ void NB_KERNEL_BOUNDS(AxCfg<typename Pol<PREC>::TV, N>)
+k_cg_sw(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D)
+{
+    constexpr int FUSED = 1, VAR = 3;
+    const MrArgs *const mr = nullptr;
+    const int vr = 0, bid = 0, G = 0;
+    (void)vr; (void)bid; (void)G; (void)mr;
+#include "nb_mega_body.inc"
+}
+
+// solveM alone (nb_precond_apply): z = M^-1 r with the Schwarz phases, one cooperative launch
+template <int PREC, int N>
+__global__ void NB_KERNEL_BOUNDS(AxCfg<typename Pol<PREC>::TV, N>)
+k_sw_apply(const __grid_constant__ MegaArgs A)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TG = typename Pol<PREC>::TG;
+    using C = AxCfg<TV, N>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    __shared__ TG sw_red[64], sw_w[28];
+    sw_weights_init(sw_w);
+    const int tid = threadIdx.x;
+    unsigned int tgt = 0;
+    int cur[3] = {-1, -1, -1};
+    const int64_t ng = ((int64_t)A.m.E + C::EPB - 1) / C::EPB;
+    const int64_t g0 = split(ng, gridDim.x, blockIdx.x), g1 = split(ng, gridDim.x, blockIdx.x + 1);
+    const int e0 = (int)min((int64_t)A.m.E, g0 * C::EPB), e1 = (int)min((int64_t)A.m.E, g1 * C::EPB);
+    for (int e = e0; e < e1; e++) sw_local<PREC, N>(A.m, A.sw, (const TV *)A.r, e, smraw, sw_red, cur, sw_w);
+    __syncthreads();
+    if (tid == 0) { tgt += gridDim.x; grid_arrive_wait(A.bar, tgt); }
+    __syncthreads();
+    if (A.sw.nv[0] > 0 && A.sw.nv[1] > 0 && A.sw.nv[2] > 0) {
+        for (int pass = 0; pass <= 6; pass++) {
+            sw_coarse<PREC>(A.m, A.sw, pass, (int64_t)blockIdx.x * blockDim.x + tid, (int64_t)gridDim.x * blockDim.x);
+            __syncthreads();
+            if (tid == 0) { tgt += gridDim.x; grid_arrive_wait(A.bar, tgt); }
+            __syncthreads();
+        }
+    }
+    Acc<PREC> rho;
+    for (int64_t pid = (int64_t)e0 * C::N2 + tid; pid < (int64_t)e1 * C::N2; pid += blockDim.x)
+        sw_gather_pencil<PREC, N>(A.m, A.sw, (const TV *)A.r, (TV *)A.z, pid, rho, sw_w);
+}
+
 // ===========================================================================
 // standalone operator (nb_ax): w = A_L u (+ dssum-free mask), one persistent kernel
 // ===========================================================================
@@ -1286,6 +1338,8 @@ cudaError_t launch_ax_local(const nb_handle *h, const void *u, void *w, bool mas
     template cudaError_t launch_cg_mega<P>(const nb_handle *, Workspace &, const void *, int, int, double,    \
                                            int, int, unsigned long long *, cudaStream_t, RankPart);           \
     template cudaError_t launch_cg_mega_var<P, 0>(const nb_handle *, const MegaArgs &, bool, cudaStream_t);
+#define NB_INSTANTIATE_CG_SW(P) \
+    template cudaError_t launch_cg_sw<P>(const nb_handle *, const MegaArgs &, int, bool, cudaStream_t);
 // the variant (VAR = 1) megakernels: their own translation units (parallel build)
 #define NB_INSTANTIATE_CG_VAR(P)                                                                              \
     template int grid_mega_var<P, 1>(const nb_handle *);                                                      \

@@ -1,0 +1,7 @@
+// nb_cg_mixed_sw.cu -- the mixed policy's Schwarz-preconditioned megakernel and solveM kernel
+// (NB_PC_SCHWARZ), in their own translation unit (parallel build).
+#include "nb_mega_launch.cuh"
+
+namespace nb {
+NB_INSTANTIATE_CG_SW(NB_MIXED)
+}  // namespace nb

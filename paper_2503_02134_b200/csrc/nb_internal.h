@@ -8,6 +8,8 @@
 
 namespace nb {
 
+struct SwState;   // NB_PC_SCHWARZ host state (nb_sw_setup.cu)
+
 // Device-resident CG scalars.  Values of the policy's scalar
 // precision (float under NB_FP32, double otherwise) are stored widened to double.
 struct Scal {
@@ -63,6 +65,23 @@ struct MeshDev {
     int64_t NZl, NGl;                 // the slab's own node lattice (its GS segments)
 };
 
+// Two-level Schwarz preconditioner (NEXT-4, nb_schwarz.cuh / nb_sw_setup.cu): device tables and
+// scratch of one handle and policy.  P3 = p + 3 points per axis of an extended element box.
+struct SwArgs {
+    int32_t on;                 // 1: tables valid (nb_cg with NB_PC_SCHWARZ, nb_precond_apply)
+    int32_t nv[3];              // interior element vertices per axis (nel_a - 1); coarse level iff all > 0
+    const uint8_t *cs[3];       // [nel_a]: case (1-D table) of each element position along axis a
+    const uint8_t *cnt[3];      // [nel_a][P3]: overlap count of the extended point (0: not an unknown)
+    const void *S[3];           // [ncase_a][P3][P3] (TV): fast-diagonalisation eigenvectors, row = point
+    const double *lam[3];       // [ncase_a][P3]: eigenvalues (padded modes: 1)
+    const void *S0[3];          // [nv_a][nv_a] (TV): coarse eigenvectors
+    const double *lam0[3];      // [nv_a]
+    const double *phL, *phR;    // [p+1]: (1 - xi_i)/2, (1 + xi_i)/2 at the GLL points
+    void *zext;                 // [E][P3^3] (TV): unweighted local solutions
+    void *cpart;                // [E][8] (TG): coarse restriction partials, element corners
+    void *c0, *c1;              // [V] (TV): coarse vectors (b0 / transforms; x0 ends in c0)
+};
+
 // Arguments of the persistent CG megakernel (nb_cg.cuh), one slab's (or the whole box's) solve
 struct MegaArgs {
     MeshDev m;
@@ -88,6 +107,7 @@ struct MegaArgs {
     // multi-rank (z-slab) solves only: the neighbour slabs' w, rebased so that the element
     // index of this slab addresses them (wlo + e*N3 for e < 0, whi + e*N3 for e >= E); else null
     const void *wlo, *whi;
+    SwArgs sw;              // NB_PC_SCHWARZ solves (k_cg_sw) only
 };
 
 // Multi-rank solve over z-slabs: every rank's block 0 pushes its rank partial
@@ -158,6 +178,7 @@ struct nb_handle {
     int phase_only = 0;         // NB_PHASE_ONLY=A (1) / B (2): measurement runs of one megakernel phase
     int dssum_csr = 0;          // NB_DSSUM=csr: consistent nb_dssum through the CSR kernel (A/B, tests)
     nb::Workspace ws[4];   // one per nb_policy
+    nb::SwState *sw = nullptr;      // NB_PC_SCHWARZ tables and scratch (nb_sw_setup.cu), lazily
     nb::MeshDev md() const {
         nb::MeshDev m;
         m.nelx = nelx; m.nely = nely; m.nelz = nelz; m.p = p; m.n = n;
@@ -199,6 +220,13 @@ template <int PREC>
 void fill_mega_args(const nb_handle *h, Workspace &ws, const void *b, int order, int max_iter, double rtol,
                     int precond, int x64, unsigned long long *tim, MegaArgs &A);
 template <int PREC> int grid_mega_mr(const nb_handle *h);
+// NB_PC_SCHWARZ: the Schwarz-preconditioned solve (k_cg_sw) or solveM alone (k_sw_apply)
+template <int PREC>
+cudaError_t launch_cg_sw(const nb_handle *h, const MegaArgs &A, int gmax, bool apply_only, cudaStream_t st);
+// Schwarz tables of the handle + the policy's scratch (nb_sw_setup.cu); fill / free
+int sw_ensure(nb_handle *h, int prec, const char **msg);   // NB_OK or an nb_status (msg set)
+void sw_fill(const nb_handle *h, int prec, SwArgs &a);
+void sw_free(nb_handle *h);
 template <int PREC> cudaError_t launch_cg_mr(const nb_handle *h0, const MultiArgs &M, cudaStream_t st);
 template <int PREC, int VAR>
 cudaError_t launch_cg_mega_var(const nb_handle *h, const MegaArgs &A, bool fused, cudaStream_t st);

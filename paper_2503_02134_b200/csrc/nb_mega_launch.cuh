@@ -154,6 +154,41 @@ cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int
     return var ? launch_cg_mega_var<PREC, 1>(h, A, fused, st) : launch_cg_mega_var<PREC, 0>(h, A, fused, st);
 }
 
+// ---- Schwarz-preconditioned solve (k_cg_sw) and solveM alone (k_sw_apply), NEXT-4 ----
+// Full occupancy grid (every block resident), at most `gmax` blocks (the workspace's partials).
+template <int PREC, int N, bool APPLY>
+static cudaError_t sw_launch_t(const nb_handle *h, const MegaArgs &A, int gmax, cudaStream_t st)
+{
+    using TV = typename Pol<PREC>::TV;
+    using C = AxCfg<TV, N>;
+    constexpr int SMEM = C::SMEM > SwCfg<TV, N>::SMEM ? C::SMEM : SwCfg<TV, N>::SMEM;
+    const void *fn = APPLY ? (const void *)k_sw_apply<PREC, N> : (const void *)k_cg_sw<PREC, N>;
+    static DevCache cache;
+    int &occ = cache.here();
+    if (occ < 0) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, C::NT, SMEM);
+        occ = o > 0 ? o : 1;
+        set_carveout(fn, occ, SMEM);
+    }
+    int grid = h->sm_count * occ;
+    if (gmax > 0 && grid > gmax) grid = gmax;
+    const long long ng = ((long long)h->E + C::EPB - 1) / C::EPB;
+    if (grid > ng) grid = (int)ng;
+    if (grid < 1) grid = 1;
+    DMat<TV, N> D = make_dmat<TV, N>(h->D);
+    void *params[2] = {(void *)&A, (void *)&D};
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(C::NT), params, (size_t)SMEM, st);
+}
+
+template <int PREC>
+cudaError_t launch_cg_sw(const nb_handle *h, const MegaArgs &A, int gmax, bool apply_only, cudaStream_t st)
+{
+    if (apply_only) { NB_DISPATCH_N(h->n, return (sw_launch_t<PREC, NN, true>(h, A, gmax, st))) }
+    NB_DISPATCH_N(h->n, return (sw_launch_t<PREC, NN, false>(h, A, gmax, st)))
+}
+
 // ---- multi-rank (z-slab) megakernel: consistent order, runtime options ----
 template <int PREC, int N>
 static int mr_occupancy()

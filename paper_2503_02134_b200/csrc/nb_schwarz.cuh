@@ -1,0 +1,361 @@
+// nb_schwarz.cuh -- the two-level overlapping Schwarz preconditioner z = M^-1 r (SURVEY.md §8(f)
+// NEXT-4; reading 28), as grid-wide phases of a persistent cooperative kernel:
+//
+//   M^-1 r = sum_e R_e^T W K_e^-1 W R_e r  +  Phi A0^-1 Phi^T r
+//
+//   S1 (sw_local, one element per block step): gather r on the element box extended by one GLL
+//      layer (the neighbours' copies, diagonal neighbours included), the coarse restriction
+//      partials of the element's 8 corners (Phi^T r), weights W = 1/sqrt(overlap count) -- the
+//      square roots of Nekbone's h1mg_schwarz_wt, in the gather-scatter precision
+//      TG: fp64 under NB_FP64 / NB_MIXED ("sqrt in fp64"), binary32 otherwise
+//      -- and the fast-diagonalisation solve (S_z S_y S_x) Lambda^-1 (S_z S_y S_x)^T in the vector
+//      precision TV: six 1-D contractions, one line of P3 values per thread through shared memory.
+//   C0..C6 (sw_coarse): the coarse vertex RHS assembled from the corner partials, then the six
+//      1-D passes of the coarse fast diagonalisation, one output per thread over the whole grid.
+//   S2 (sw_gather_pencil, one r-pencil per thread): z at every copy = the sum, in ascending
+//      element order, of the weighted local solutions of the (up to 8) extended boxes holding
+//      the node, accumulated in TG (the preconditioner's gather-scatter: fp64 under NB_MIXED),
+//      plus the trilinear interpolation of the coarse solution; glsc3(r, c, z) partial.
+// Grid barriers separate the phases (the caller passes the barrier counter and target).
+#pragma once
+#include "nb_common.cuh"
+
+namespace nb {
+
+template <typename TV, int N> struct SwCfg {
+    static constexpr int P3 = N + 2, P2 = P3 * P3, PV = P2 * P3;
+    // shared memory: F, T [PV] (TV); S_x, S_y, S_z and their transposes [P2] (TV); lambda_x,y,z [P3] (double)
+    static constexpr int OFF_S = 2 * PV * (int)sizeof(TV);
+    static constexpr int OFF_L = ((OFF_S + 6 * P2 * (int)sizeof(TV)) + 15) / 16 * 16;
+    static constexpr int SMEM = OFF_L + 3 * P3 * 8;
+};
+
+// W = 1/sqrt(count) in the gather-scatter precision (count 0: not an unknown)
+template <typename TG>
+__device__ __forceinline__ TG sw_weight(int c)
+{
+    if (c == 0) return TG(0);
+    if constexpr (sizeof(TG) == 8) return 1.0 / sqrt((double)c);
+    else return 1.0f / sqrtf((float)c);
+}
+
+// the weights of every possible count (1..27: up to 3 boxes per axis), in a block's shared memory
+template <typename TG>
+__device__ __forceinline__ void sw_weights_init(TG *wlut)
+{
+    if (threadIdx.x < 28) wlut[threadIdx.x] = sw_weight<TG>((int)threadIdx.x);
+    __syncthreads();
+}
+
+// one 1-D pass over the P3^3 box: axis 0 (x), 1 (y), 2 (z), one line per thread:
+// o[i] = sum_l M[l*P3 + i] in_l with M = S (S^T applied) or M = S^T (S applied), both stored
+// row-major in shared memory so a row of M is contiguous: single precision pairs the outputs in
+// packed FMAs (FFMA2) fed by 8-byte shared loads.  l outermost (unrolled by 2): one row of M live
+// at a time (all P3^2 coefficients hoisted into registers would spill at the megakernel's
+// register cap).  SCALE: multiply output (ti,tj,tk) by 1/(lx[ti] + ly[tj] + lz[tk]) (computed in
+// double, rounded once to TV).
+template <typename TV, int P3, int AXIS, bool SCALE>
+__device__ __forceinline__ void sw_pass(const TV *__restrict__ in, TV *__restrict__ out, const TV *__restrict__ M,
+                                        const double *__restrict__ lm)
+{
+    constexpr int P2 = P3 * P3;
+    constexpr bool PAIR = sizeof(TV) == 4 && P3 % 2 == 0 && NB_FFMA2;
+    for (int line = threadIdx.x; line < P2; line += blockDim.x) {
+        const int u = line % P3, w = line / P3;
+        // base index and stride of the line along AXIS
+        const int base = AXIS == 0 ? P3 * line : AXIS == 1 ? u + P2 * w : line;
+        constexpr int st = AXIS == 0 ? 1 : AXIS == 1 ? P3 : P2;
+        TV o[P3];
+        if constexpr (PAIR) {
+            unsigned long long acc[P3 / 2];
+#pragma unroll
+            for (int i = 0; i < P3 / 2; i++) acc[i] = 0ull;
+#pragma unroll 2
+            for (int l = 0; l < P3; l++) {
+                const float vl = (float)in[base + st * l];
+                const unsigned long long vv = pack2(vl, vl);
+                const unsigned long long *row = reinterpret_cast<const unsigned long long *>(M + l * P3);
+#pragma unroll
+                for (int i = 0; i < P3 / 2; i++) acc[i] = ffma2(row[i], vv, acc[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < P3 / 2; i++) { o[2 * i] = (TV)lo2(acc[i]); o[2 * i + 1] = (TV)hi2(acc[i]); }
+        } else {
+#pragma unroll
+            for (int i = 0; i < P3; i++) o[i] = TV(0);
+#pragma unroll 2
+            for (int l = 0; l < P3; l++) {
+                const TV vl = in[base + st * l];
+#pragma unroll
+                for (int i = 0; i < P3; i++) o[i] = fma(M[l * P3 + i], vl, o[i]);
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < P3; l++) {
+            TV val = o[l];
+            if (SCALE) {   // AXIS == 2: (ti, tj) = (u, w), tk = l
+                const double d = 1.0 / (lm[u] + lm[P3 + w] + lm[2 * P3 + l]);
+                val = val * (TV)d;
+            }
+            out[base + st * l] = val;
+        }
+    }
+}
+
+// S1: the local solve of element e (all threads of the block); writes S.zext[e] and S.cpart[e]
+template <int PREC, int N>
+__device__ __forceinline__ void sw_local(const MeshDev &m, const SwArgs &S, const typename Pol<PREC>::TV *__restrict__ r,
+                                         int e, unsigned char *smraw, typename Pol<PREC>::TG *red, int (&cur)[3],
+                                         const typename Pol<PREC>::TG *__restrict__ wlut)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TG = typename Pol<PREC>::TG;
+    using C = SwCfg<TV, N>;
+    constexpr int P3 = C::P3, P2 = C::P2, PV = C::PV, N3 = N * N * N;
+    TV *F = reinterpret_cast<TV *>(smraw);
+    TV *T = F + PV;
+    TV *Sm = reinterpret_cast<TV *>(smraw + C::OFF_S);
+    double *lm = reinterpret_cast<double *>(smraw + C::OFF_L);
+    const int tid = threadIdx.x;
+    const ElemPos P = elem_pos<false>(m, e);
+    const int pos[3] = {P.ex, P.ey, P.ez};
+    // the element's three 1-D tables (kept from the previous element of the block when the cases
+    // match: block-uniform test; the previous element's passes ended with a barrier)
+    const int cs0 = S.cs[0][pos[0]], cs1 = S.cs[1][pos[1]], cs2 = S.cs[2][pos[2]];
+    if (cs0 != cur[0] || cs1 != cur[1] || cs2 != cur[2]) {
+        for (int q = tid; q < 3 * P2; q += blockDim.x) {   // S_a at [a], S_a^T at [3 + a]
+            const int a = q / P2, k = q - a * P2;
+            const TV v = ((const TV *)S.S[a])[(size_t)S.cs[a][pos[a]] * P2 + k];
+            Sm[q] = v;
+            Sm[(3 + a) * P2 + (k % P3) * P3 + k / P3] = v;
+        }
+        for (int q = tid; q < 3 * P3; q += blockDim.x) {
+            const int a = q / P3, k = q - a * P3;
+            lm[q] = S.lam[a][(size_t)S.cs[a][pos[a]] * P3 + k];
+        }
+        cur[0] = cs0; cur[1] = cs1; cur[2] = cs2;
+    }
+    const uint8_t *cx = S.cnt[0] + (size_t)P.ex * P3, *cy = S.cnt[1] + (size_t)P.ey * P3, *cz = S.cnt[2] + (size_t)P.ez * P3;
+    // R_e r, its coarse restriction partials and W R_e r, one x-line (tj, tk) of the extended box
+    // per thread: the line is a row of the (y, z)-neighbour element's copy (N contiguous values)
+    // plus one value from each x-neighbour of that element
+    TG cp[8];
+#pragma unroll
+    for (int c = 0; c < 8; c++) cp[c] = TG(0);
+    const bool coarse = S.nv[0] > 0 && S.nv[1] > 0 && S.nv[2] > 0;
+    for (int line = tid; line < P2; line += blockDim.x) {
+        const int tj = line % P3, tk = line / P3;
+        const int cyz = cy[tj] * cz[tk];
+        TV v[P3];
+#pragma unroll
+        for (int t = 0; t < P3; t++) v[t] = TV(0);
+        if (cyz) {
+            const int dy = tj == 0 ? -1 : (tj == P3 - 1 ? 1 : 0);
+            const int dz = tk == 0 ? -1 : (tk == P3 - 1 ? 1 : 0);
+            const int lj = tj == 0 ? N - 2 : (tj == P3 - 1 ? 1 : tj - 1);
+            const int lk = tk == 0 ? N - 2 : (tk == P3 - 1 ? 1 : tk - 1);
+            const int64_t e2 = (int64_t)e + (int64_t)m.nelx * (dy + (int64_t)m.nely * dz);
+            const TV *row = r + e2 * N3 + N * (lj + N * lk);
+            TV own[N];
+            ld_pencil<TV, N>(row, own);
+            v[0] = cx[0] ? row[-N3 + N - 2] : TV(0);
+            v[P3 - 1] = cx[P3 - 1] ? row[N3 + 1] : TV(0);
+#pragma unroll
+            for (int i = 0; i < N; i++) v[i + 1] = cx[i + 1] ? own[i] : TV(0);
+            if (coarse && dy == 0 && dz == 0) {   // the element's own copies: c_l phi r per corner
+                const int j = tj - 1, k = tk - 1;
+                const double cjk = 1.0 / (double)(axis_mult(j, N, P.ey, m.nely) * axis_mult(k, N, P.ez, m.nelz));
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    const double cl = cjk / (double)axis_mult(i, N, P.ex, m.nelx);
+                    const TG vi = (TG)v[i + 1];
+#pragma unroll
+                    for (int c = 0; c < 8; c++) {
+                        const double ph = ((c & 1) ? S.phR[i] : S.phL[i]) * ((c & 2) ? S.phR[j] : S.phL[j]) *
+                                          ((c & 4) ? S.phR[k] : S.phL[k]);
+                        cp[c] += (TG)(ph * cl) * vi;
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < P3; t++) v[t] = (TV)((TG)v[t] * wlut[cx[t] * cyz]);
+        }
+#pragma unroll
+        for (int t = 0; t < P3; t++) F[P3 * line + t] = v[t];
+    }
+    if (coarse) {   // block sum of the 8 partials (fixed tree), stored by thread 0
+        const int lane = tid & 31, wid = tid >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+        for (int c = 0; c < 8; c++)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cp[c] += __shfl_down_sync(0xffffffffu, cp[c], o);
+        if (lane == 0)
+#pragma unroll
+            for (int c = 0; c < 8; c++) red[wid * 8 + c] = cp[c];
+        __syncthreads();
+        if (tid < 8) {
+            TG sacc = TG(0);
+            for (int w = 0; w < nw; w++) sacc += red[w * 8 + tid];
+            ((TG *)S.cpart)[(size_t)e * 8 + tid] = sacc;
+        }
+    } else {
+        __syncthreads();
+    }
+    // K_e^-1 by fast diagonalisation: S_x^T, S_y^T, S_z^T + Lambda^-1, S_z, S_y, S_x
+    sw_pass<TV, P3, 0, false>(F, T, Sm, lm);
+    __syncthreads();
+    sw_pass<TV, P3, 1, false>(T, F, Sm + P2, lm);
+    __syncthreads();
+    sw_pass<TV, P3, 2, true>(F, T, Sm + 2 * P2, lm);
+    __syncthreads();
+    sw_pass<TV, P3, 2, false>(T, F, Sm + 5 * P2, lm);
+    __syncthreads();
+    sw_pass<TV, P3, 1, false>(F, T, Sm + 4 * P2, lm);
+    __syncthreads();
+    sw_pass<TV, P3, 0, false>(T, (TV *)S.zext + (size_t)e * PV, Sm + 3 * P2, lm);
+    __syncthreads();   // smem reused by the next element
+}
+
+// coarse pass `pass` (0: assemble b0; 1..6: the fast-diagonalisation passes), thread gt of gn
+template <int PREC>
+__device__ __forceinline__ void sw_coarse(const MeshDev &m, const SwArgs &S, int pass, int64_t gt, int64_t gn)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TG = typename Pol<PREC>::TG;
+    const int nx = S.nv[0], ny = S.nv[1], nz = S.nv[2];
+    const int64_t V = (int64_t)nx * ny * nz;
+    TV *c0 = (TV *)S.c0, *c1 = (TV *)S.c1;
+    for (int64_t v = gt; v < V; v += gn) {
+        const int vx = (int)(v % nx), vy = (int)((v / nx) % ny), vz = (int)(v / ((int64_t)nx * ny));
+        if (pass == 0) {
+            // vertex (vx+1, vy+1, vz+1): corners of the elements around it, ascending element order
+            TG s = TG(0);
+            for (int dz = 0; dz < 2; dz++)
+                for (int dy = 0; dy < 2; dy++)
+                    for (int dx = 0; dx < 2; dx++) {
+                        const int ex = vx + dx, ey = vy + dy, ez = vz + dz;   // element; its corner (1-dx, 1-dy, 1-dz)
+                        const int64_t e = ex + (int64_t)m.nelx * (ey + (int64_t)m.nely * ez);
+                        const int c = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+                        s += __ldcg((const TG *)S.cpart + e * 8 + c);
+                    }
+            c0[v] = (TV)s;
+            continue;
+        }
+        // 1: Sx^T c0 -> c1; 2: Sy^T c1 -> c0; 3: Sz^T c0 * dl -> c1; 4: Sz c1 -> c0; 5: Sy c0 -> c1; 6: Sx c1 -> c0
+        const int ax = (pass == 1 || pass == 6) ? 0 : (pass == 2 || pass == 5) ? 1 : 2;
+        const bool tr = pass >= 4;
+        const TV *in = (pass & 1) ? c0 : c1;
+        TV *out = (pass & 1) ? c1 : c0;
+        const int n = S.nv[ax], idx = ax == 0 ? vx : ax == 1 ? vy : vz;
+        const int64_t st = ax == 0 ? 1 : ax == 1 ? nx : (int64_t)nx * ny;
+        const int64_t base = v - (int64_t)idx * st;
+        const TV *M = (const TV *)S.S0[ax];
+        TV s = TV(0);
+        for (int l = 0; l < n; l++) s = fma(tr ? M[idx * n + l] : M[l * n + idx], __ldcg(in + base + st * l), s);
+        if (pass == 3) s = s * (TV)(1.0 / (S.lam0[0][vx] + S.lam0[1][vy] + S.lam0[2][vz]));
+        out[v] = s;
+    }
+}
+
+// S2: z on the r-pencil (a, b) of element e = W (sum of the local solutions holding each node,
+// ascending element order, in TG) + the coarse interpolation; glsc3(r, c, z) partial.
+// Per candidate box row (iy, iz): the element's own box row (P3 contiguous values, 16-byte
+// loads) and, for the pencil's end nodes, the x-neighbours' boxes; the element's interior corner
+// values of the coarse solution are loaded once per pencil.
+template <int PREC, int N>
+__device__ __forceinline__ void sw_gather_pencil(const MeshDev &m, const SwArgs &S, const typename Pol<PREC>::TV *__restrict__ r,
+                                                 typename Pol<PREC>::TV *__restrict__ z, int64_t pid, Acc<PREC> &rho,
+                                                 const typename Pol<PREC>::TG *__restrict__ wlut)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TG = typename Pol<PREC>::TG;
+    using TS = typename Pol<PREC>::TS;
+    constexpr int N2 = N * N, P3 = N + 2, P2 = P3 * P3, PV = P2 * P3;
+    constexpr int VR = (P3 * sizeof(TV)) % 16 == 0 ? 16 / (int)sizeof(TV) : 1;   // row load width
+    const int e = (int)(pid / N2);
+    const int q = (int)(pid - (int64_t)e * N2);
+    const int a = q % N, b = q / N;
+    const ElemPos P = elem_pos<false>(m, e);
+    const TV *zx = (const TV *)S.zext;
+    const bool coarse = S.nv[0] > 0 && S.nv[1] > 0 && S.nv[2] > 0;
+    // candidate boxes along y and z (element offset d, index t in that element's box): the node at
+    // local a lies at box index a + 1 of its own element, a + N of the lower neighbour's (a <= 1)
+    // and a - N + 2 of the upper neighbour's (a >= N - 2); three boxes for p <= 2
+    int ny_ = 0, nz_ = 0, dy[3], ty[3], dz[3], tz[3];
+    if (a <= 1 && P.ey > 0) { dy[ny_] = -1; ty[ny_++] = a + N; }
+    dy[ny_] = 0; ty[ny_++] = a + 1;
+    if (a >= N - 2 && P.ey < m.nely - 1) { dy[ny_] = 1; ty[ny_++] = a - N + 2; }
+    if (b <= 1 && P.ez > 0) { dz[nz_] = -1; tz[nz_++] = b + N; }
+    dz[nz_] = 0; tz[nz_++] = b + 1;
+    if (b >= N - 2 && P.ez < m.nelz - 1) { dz[nz_] = 1; tz[nz_++] = b - N + 2; }
+    const bool xl = P.ex > 0, xr = P.ex < m.nelx - 1;
+    const int cyz = S.cnt[1][(size_t)P.ey * P3 + a + 1] * S.cnt[2][(size_t)P.ez * P3 + b + 1];
+    // sum of the local solutions at the node, then the node's weight (constant over its boxes)
+    TG acc[N];
+#pragma unroll
+    for (int i = 0; i < N; i++) acc[i] = TG(0);
+    if (cyz) {
+        for (int iz = 0; iz < nz_; iz++)
+            for (int iy = 0; iy < ny_; iy++) {
+                const int64_t eyz = (int64_t)e + (int64_t)m.nelx * (dy[iy] + (int64_t)m.nely * dz[iz]);
+                const TV *row = zx + eyz * PV + (int64_t)P3 * (ty[iy] + P3 * tz[iz]);
+                TV v[P3];
+#pragma unroll
+                for (int c = 0; c < P3 / VR; c++) {
+                    if constexpr (VR == 4) {
+                        const float4 t = __ldcg(reinterpret_cast<const float4 *>(row) + c);
+                        v[4 * c] = t.x; v[4 * c + 1] = t.y; v[4 * c + 2] = t.z; v[4 * c + 3] = t.w;
+                    } else if constexpr (VR == 2) {
+                        const double2 t = __ldcg(reinterpret_cast<const double2 *>(row) + c);
+                        v[2 * c] = t.x; v[2 * c + 1] = t.y;
+                    } else {
+                        v[c] = __ldcg(row + c);
+                    }
+                }
+                // x-neighbours' boxes: values at their indices N, N + 1 (nodes 0, 1) and 0, 1 (nodes N - 2, N - 1)
+                const TV l0 = xl ? __ldcg(row - PV + N) : TV(0), l1 = xl ? __ldcg(row - PV + N + 1) : TV(0);
+                const TV r0 = xr ? __ldcg(row + PV) : TV(0), r1 = xr ? __ldcg(row + PV + 1) : TV(0);
+#pragma unroll
+                for (int i = 0; i < N; i++) {
+                    if (i <= 1 && xl) acc[i] += (TG)(i == 0 ? l0 : l1);
+                    acc[i] += (TG)v[i + 1];
+                    if (i >= N - 2 && xr) acc[i] += (TG)(i == N - 2 ? r0 : r1);
+                }
+            }
+#pragma unroll
+        for (int i = 0; i < N; i++) acc[i] *= wlut[S.cnt[0][(size_t)P.ex * P3 + i + 1] * cyz];
+    }
+    if (coarse) {   // trilinear interpolation of x0 from the element's interior corner vertices:
+        // g[cx] = sum_{cz, cy} hz hy x0(corner) once per pencil, then per node hx0 g[0] + hx1 g[1]
+        // (corner values of boundary vertices are 0; the same arithmetic at every copy of a node)
+        const TV *x0 = (const TV *)S.c0;
+        const TV hy[2] = {(TV)S.phL[a], (TV)S.phR[a]}, hz[2] = {(TV)S.phL[b], (TV)S.phR[b]};
+        TV g[2] = {TV(0), TV(0)};
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            const int vx = P.ex + (c & 1), vy = P.ey + ((c >> 1) & 1), vz = P.ez + (c >> 2);
+            const bool in = vx >= 1 && vx <= S.nv[0] && vy >= 1 && vy <= S.nv[1] && vz >= 1 && vz <= S.nv[2];
+            const TV xcv = in ? __ldcg(x0 + (vx - 1) + (int64_t)S.nv[0] * ((vy - 1) + (int64_t)S.nv[1] * (vz - 1))) : TV(0);
+            g[c & 1] = fma(hz[c >> 2] * hy[(c >> 1) & 1], xcv, g[c & 1]);
+        }
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            if (!(cyz && S.cnt[0][(size_t)P.ex * P3 + i + 1])) continue;   // Dirichlet node
+            acc[i] += (TG)fma((TV)S.phL[i], g[0], (TV)S.phR[i] * g[1]);
+        }
+    }
+    TV rr[N], zz[N];
+    const size_t base = (size_t)pid * N;
+    ld_pencil<TV, N>(r + base, rr);
+    const int mjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz);
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+        zz[i] = (TV)acc[i];
+        const TS c = (TS)1 / (TS)(mjk * axis_mult(i, N, P.ex, m.nelx));
+        const TS rs = (TS)rr[i];
+        rho.add(rs * c, (TS)zz[i]);
+    }
+    st_pencil<TV, N>(z + base, zz);
+}
+
+}  // namespace nb

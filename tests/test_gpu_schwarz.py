@@ -1,0 +1,117 @@
+"""GPU parity of the two-level Schwarz preconditioner (NB_PC_SCHWARZ, SURVEY.md §8(f) NEXT-4,
+DESIGN.md reading 28) against the oracle's (pinned by tests/test_oracle_schwarz.py against the
+dense formula built from the independently assembled stiffness).
+
+- solveM alone (nb_precond_apply) vs oracle.schwarz on undeformed / deformed meshes, odd and even
+  p, meshes without a coarse level (one element along an axis), every policy: fp64 to 1e-11, the
+  single-precision policies to fp32 rounding; every copy of a node bit-identical, Dirichlet zero.
+- the Schwarz-preconditioned CG (nb_cg precond = NB_PC_SCHWARZ) vs the oracle's: iteration
+  counts within 5%, solutions within the policy's bar of the oracle fp64 solution.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+import paper_2503_02134_b200 as nb
+
+pytestmark = pytest.mark.gpu
+
+POL = {nb.NB_FP64: oracle.FP64, nb.NB_FP32: oracle.FP32, nb.NB_MIXED: oracle.MIXED, nb.NB_FP32_DOT2: oracle.FP32_DOT2}
+NAMES = {nb.NB_FP64: "fp64", nb.NB_FP32: "fp32", nb.NB_MIXED: "mixed", nb.NB_FP32_DOT2: "dot2"}
+
+MESHES = [((3, 2, 2), 3, 0.0), ((4, 3, 2), 5, 0.1), ((5, 4, 3), 7, 0.0), ((3, 3, 3), 9, 0.1), ((2, 2, 2), 1, 0.0),
+          ((1, 2, 3), 4, 0.0), ((3, 2, 2), 11, 0.1), ((2, 3, 2), 2, 0.0)]
+
+
+@pytest.mark.parametrize("nel,p,d", MESHES, ids=[f"{a}x{b}x{c}p{p}{'d' if d else ''}" for (a, b, c), p, d in MESHES])
+@pytest.mark.parametrize("policy", [nb.NB_FP64, nb.NB_MIXED, nb.NB_FP32, nb.NB_FP32_DOT2], ids=list(NAMES.values()))
+def test_schwarz_apply_vs_oracle(nel, p, d, policy):
+    o = oracle.Mesh(*nel, p, deform=d, seed=1)
+    g = nb.Mesh(*nel, p, deform=d, seed=1)
+    try:
+        r64 = o.rhs(seed=5)
+        gid, mask, _, _ = o.maps()
+        if policy == nb.NB_FP64:
+            zo = o.schwarz(r64, oracle.FP64)
+            r = torch.tensor(r64, device="cuda")
+        else:
+            r32 = r64.astype(np.float32)
+            zo = o.schwarz(r32, POL[policy]).astype(np.float64)
+            r = torch.tensor(r32, device="cuda")
+        z = g.precond(r, policy).cpu().numpy().astype(np.float64)
+        den = np.linalg.norm(zo)
+        assert den > 0
+        err = np.linalg.norm(z - zo) / den
+        assert err <= (1e-11 if policy == nb.NB_FP64 else 2e-6), err
+        assert np.max(np.abs(z - zo)) <= (1e-11 if policy == nb.NB_FP64 else 1e-5) * np.max(np.abs(zo))
+        # consistent: every copy of a global node holds the same bits; Dirichlet copies are zero
+        zg = np.full(o.n_global, np.nan)
+        zg[gid] = z
+        np.testing.assert_array_equal(z, zg[gid])
+        assert np.all(z[mask == 0] == 0.0)
+    finally:
+        g.close()
+
+
+def cgap(x, ref, c):
+    dd = x - ref
+    return float(np.sqrt(np.sum(c * dd * dd) / np.sum(c * ref * ref)))
+
+
+@pytest.fixture(scope="module", params=[((4, 4, 4), 7, 0.0), ((3, 3, 2), 5, 0.1)], ids=["4x4x4p7", "3x3x2p5d"])
+def pcg_mesh(request):
+    nel, p, d = request.param
+    g = nb.Mesh(*nel, p, deform=d)
+    o = oracle.Mesh(*nel, p, deform=d)
+    yield g, o, o.rhs(seed=0), {}
+    g.close()
+
+
+@pytest.mark.parametrize("policy", [nb.NB_FP64, nb.NB_MIXED, nb.NB_FP32, nb.NB_FP32_DOT2], ids=list(NAMES.values()))
+def test_schwarz_pcg_vs_oracle(pcg_mesh, policy):
+    g, o, bo, cache = pcg_mesh
+    if "fp64" not in cache:
+        cache["fp64"] = o.cg(bo, oracle.FP64, max_iter=500, rtol=1e-8, precond=oracle.PC_SCHWARZ)
+    x64o, h64, r64 = cache["fp64"]
+    xo, ho, ro = o.cg(bo, POL[policy], max_iter=500, rtol=1e-8, precond=oracle.PC_SCHWARZ)
+    b = g.rhs(policy, seed=0)
+    x, r = g.cg(b, policy, max_iter=500, rtol=1e-8, precond=nb.NB_PC_SCHWARZ)
+    assert r.status == nb.NB_CONVERGED and ro.status == oracle.CONVERGED
+    assert abs(r.iterations - ro.iterations) <= max(1, 0.05 * ro.iterations), (r.iterations, ro.iterations)
+    c = o.geom()["c"]
+    gap = cgap(x.cpu().numpy().astype(np.float64), x64o, c)
+    assert gap <= (1e-8 if policy == nb.NB_FP64 else 1e-6), gap
+    k = min(len(r.history), len(ho))
+    assert np.max(np.abs(np.log10(r.history[1:k]) - np.log10(ho[1:k]))) <= (1e-6 if policy == nb.NB_FP64 else 0.5)
+    # the Schwarz time is reported in the phase-S slot
+    assert r.k_gs_ms > 0
+
+
+def test_schwarz_pcg_configs1_fewer_iterations():
+    """configs[1] (16^3, p = 7, uniform RHS) under the mixed policy: the Schwarz PCG reaches 1e-8
+    in a small fraction of the Jacobi iterations (587), like the fp64 Schwarz PCG."""
+    g = nb.Mesh(16, 16, 16, 7)
+    try:
+        b = g.rhs(nb.NB_MIXED, seed=0)
+        _, rs = g.cg(b, nb.NB_MIXED, max_iter=1000, rtol=1e-8, precond=nb.NB_PC_SCHWARZ)
+        b64 = g.rhs(nb.NB_FP64, seed=0)
+        _, r64 = g.cg(b64, nb.NB_FP64, max_iter=1000, rtol=1e-8, precond=nb.NB_PC_SCHWARZ)
+        assert rs.status == nb.NB_CONVERGED and r64.status == nb.NB_CONVERGED
+        assert rs.iterations <= 587 // 5
+        assert abs(rs.iterations - r64.iterations) <= max(1, 0.05 * r64.iterations)
+    finally:
+        g.close()
+
+
+def test_schwarz_rejects_unsupported():
+    g = nb.Mesh(3, 3, 3, 3)
+    try:
+        b = g.rhs(nb.NB_MIXED)
+        with pytest.raises(nb.NbError):
+            g.cg(b, nb.NB_MIXED, max_iter=10, rtol=0.0, gs_order=nb.NB_GS_PER_COPY, precond=nb.NB_PC_SCHWARZ)
+        with pytest.raises(nb.NbError):
+            g.precond(b, nb.NB_MIXED, pc=nb.NB_PC_JACOBI)
+    finally:
+        g.close()
