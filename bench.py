@@ -547,6 +547,28 @@ def run_ours(args):
         ttr["speedup_fp64_over_mixed_time"] = ttr["fp64"]["time_ms"] / ttr["mixed"]["time_ms"]
         ttr["accuracy_AE_MAE_mixed_vs_fp64"] = ae_mae(hists["mixed"], hists["fp64"])
         ttr["accuracy_AE_MAE_fp32_vs_fp64"] = ae_mae(hists["fp32"], hists["fp64"])
+        # NEXT-4: the same workload with the two-level Schwarz preconditioner
+        # (Nekbone's multigrid-preconditioned CG) -- time to 1e-8 per policy
+        sw = {}
+        for name, pp in POLICIES.items():
+            bb = mesh.rhs(pp, nb.NB_RHS_UNIFORM, seed=0)
+            xx = mesh.empty(pp)
+            nb.nb_cg(mesh.h, bb, xx, pp, max_iter, WORKLOAD["rtol"], history=False, precond=nb.NB_PC_SCHWARZ)
+            reps = []
+            for _ in range(3):
+                flush.zero_()
+                r, _ = nb.nb_cg(mesh.h, bb, xx, pp, max_iter, WORKLOAD["rtol"], history=False,
+                                precond=nb.NB_PC_SCHWARZ)
+                reps.append(r)
+            tmed = statistics.median(r.solve_ms for r in reps)
+            rk = reps[-1]
+            it = max(rk.iterations, 1)
+            sw[name] = {"iterations": rk.iterations, "status": rk.status, "time_ms": tmed,
+                        "speedup_vs_jacobi": ttr[name]["time_ms"] / tmed,
+                        "phaseA_us": 1e3 * rk.k_ax_ms / it, "phaseB_us": 1e3 * rk.k_upd_ms / it,
+                        "solveM_us": 1e3 * rk.k_gs_ms / it}
+        sw["speedup_fp64_over_mixed_time"] = sw["fp64"]["time_ms"] / sw["mixed"]["time_ms"]
+        ttr["schwarz_pcg"] = sw
 
     # the HBM roofline point (configs[2]); configs[1] above is L2-resident
     roof, peak, peak_src = None, None, None

@@ -94,7 +94,7 @@ def test_bad_variants_rejected(small):
     with pytest.raises(ValueError):
         m.cg(b, oracle.FP32, max_iter=2, x64=True)
     with pytest.raises(ValueError):
-        m.cg(b, oracle.FP64, max_iter=2, precond=3)
+        m.cg(b, oracle.FP64, max_iter=2, precond=oracle.PC_SCHWARZ + 1)
 
 
 def test_fp32_jacobi_copy_is_fp32_jacobi(small):
