@@ -22,12 +22,18 @@
 
 namespace nb {
 
+#ifndef NB_SW_EB
+#define NB_SW_EB 2
+#endif
 template <typename TV, int N> struct SwCfg {
     static constexpr int P3 = N + 2, P2 = P3 * P3, PV = P2 * P3;
-    // shared memory: F, T [PV] (TV); S_x, S_y, S_z and their transposes [P2] (TV); lambda_x,y,z [P3] (double)
+    // one slot: F, T [PV] (TV); S_x, S_y, S_z and their transposes [P2] (TV); lambda_x,y,z [P3] (double)
     static constexpr int OFF_S = 2 * PV * (int)sizeof(TV);
     static constexpr int OFF_L = ((OFF_S + 6 * P2 * (int)sizeof(TV)) + 15) / 16 * 16;
-    static constexpr int SMEM = OFF_L + 3 * P3 * 8;
+    static constexpr int SLOT = ((OFF_L + 3 * P3 * 8) + 15) / 16 * 16;
+    // elements per S1 step (slots): NB_SW_EB while the slots fit in 110 KB, else 1
+    static constexpr int EB = (NB_SW_EB * SLOT <= 110 * 1024) ? NB_SW_EB : 1;
+    static constexpr int SMEM = EB * SLOT;
 };
 
 // W = 1/sqrt(count) in the gather-scatter precision (count 0: not an unknown)
@@ -47,20 +53,28 @@ __device__ __forceinline__ void sw_weights_init(TG *wlut)
     __syncthreads();
 }
 
-// one 1-D pass over the P3^3 box: axis 0 (x), 1 (y), 2 (z), one line per thread:
+// one 1-D pass over the P3^3 boxes of the ne slots: axis 0 (x), 1 (y), 2 (z), one line per thread:
 // o[i] = sum_l M[l*P3 + i] in_l with M = S (S^T applied) or M = S^T (S applied), both stored
-// row-major in shared memory so a row of M is contiguous: single precision pairs the outputs in
-// packed FMAs (FFMA2) fed by 8-byte shared loads.  l outermost (unrolled by 2): one row of M live
-// at a time (all P3^2 coefficients hoisted into registers would spill at the megakernel's
-// register cap).  SCALE: multiply output (ti,tj,tk) by 1/(lx[ti] + ly[tj] + lz[tk]) (computed in
-// double, rounded once to TV).
-template <typename TV, int P3, int AXIS, bool SCALE>
-__device__ __forceinline__ void sw_pass(const TV *__restrict__ in, TV *__restrict__ out, const TV *__restrict__ M,
-                                        const double *__restrict__ lm)
+// row-major in the slot's shared memory so a row of M is contiguous: single precision pairs the
+// outputs in packed FMAs (FFMA2) fed by 8-byte shared loads.  l outermost (unrolled by 2): one row
+// of M live at a time (all P3^2 coefficients hoisted into registers would spill at the
+// megakernel's register cap).  SCALE: multiply output (ti,tj,tk) by 1/(lx[ti] + ly[tj] + lz[tk])
+// (computed in double, rounded once to TV).  Byte offsets within a slot: IN, OUT (OUT < 0: the
+// global zext of the slot's element), M; the slot's lambdas at SwCfg::OFF_L.
+template <typename TV, int N, int AXIS, bool SCALE>
+__device__ __forceinline__ void sw_pass(unsigned char *smraw, int ne, int in_off, int out_off, int m_off,
+                                        TV *__restrict__ zext, int e0)
 {
-    constexpr int P2 = P3 * P3;
+    using C = SwCfg<TV, N>;
+    constexpr int P3 = C::P3, P2 = C::P2;
     constexpr bool PAIR = sizeof(TV) == 4 && P3 % 2 == 0 && NB_FFMA2;
-    for (int line = threadIdx.x; line < P2; line += blockDim.x) {
+    for (int L = threadIdx.x; L < ne * P2; L += blockDim.x) {
+        const int sl = L / P2, line = L - sl * P2;
+        unsigned char *slot = smraw + sl * C::SLOT;
+        const TV *in = reinterpret_cast<const TV *>(slot + in_off);
+        const TV *M = reinterpret_cast<const TV *>(slot + m_off);
+        const double *lm = reinterpret_cast<const double *>(slot + C::OFF_L);
+        TV *out = out_off >= 0 ? reinterpret_cast<TV *>(slot + out_off) : zext + (size_t)(e0 + sl) * C::PV;
         const int u = line % P3, w = line / P3;
         // base index and stride of the line along AXIS
         const int base = AXIS == 0 ? P3 * line : AXIS == 1 ? u + P2 * w : line;
@@ -74,7 +88,16 @@ __device__ __forceinline__ void sw_pass(const TV *__restrict__ in, TV *__restric
             for (int l = 0; l < P3; l++) {
                 const float vl = (float)in[base + st * l];
                 const unsigned long long vv = pack2(vl, vl);
-                const unsigned long long *row = reinterpret_cast<const unsigned long long *>(M + l * P3);
+                unsigned long long row[P3 / 2];
+                if constexpr (P3 % 4 == 0) {   // 16-byte shared loads of the M row (rows are 16-byte aligned)
+                    const ulonglong2 *r2 = reinterpret_cast<const ulonglong2 *>(M + l * P3);
+#pragma unroll
+                    for (int i = 0; i < P3 / 4; i++) { const ulonglong2 t = r2[i]; row[2 * i] = t.x; row[2 * i + 1] = t.y; }
+                } else {
+                    const unsigned long long *r1 = reinterpret_cast<const unsigned long long *>(M + l * P3);
+#pragma unroll
+                    for (int i = 0; i < P3 / 2; i++) row[i] = r1[i];
+                }
 #pragma unroll
                 for (int i = 0; i < P3 / 2; i++) acc[i] = ffma2(row[i], vv, acc[i]);
             }
@@ -86,8 +109,18 @@ __device__ __forceinline__ void sw_pass(const TV *__restrict__ in, TV *__restric
 #pragma unroll 2
             for (int l = 0; l < P3; l++) {
                 const TV vl = in[base + st * l];
+                if constexpr (sizeof(TV) == 8 && P3 % 2 == 0) {   // 16-byte shared loads of the M row
+                    const double2 *r2 = reinterpret_cast<const double2 *>(M + l * P3);
 #pragma unroll
-                for (int i = 0; i < P3; i++) o[i] = fma(M[l * P3 + i], vl, o[i]);
+                    for (int i = 0; i < P3 / 2; i++) {
+                        const double2 t = r2[i];
+                        o[2 * i] = fma((TV)t.x, vl, o[2 * i]);
+                        o[2 * i + 1] = fma((TV)t.y, vl, o[2 * i + 1]);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < P3; i++) o[i] = fma(M[l * P3 + i], vl, o[i]);
+                }
             }
         }
 #pragma unroll
@@ -102,118 +135,133 @@ __device__ __forceinline__ void sw_pass(const TV *__restrict__ in, TV *__restric
     }
 }
 
-// S1: the local solve of element e (all threads of the block); writes S.zext[e] and S.cpart[e]
+// S1: the local solves of elements e0 .. e0 + ne - 1 (ne <= SwCfg::EB, one shared-memory slot
+// each; all threads of the block); writes S.zext and S.cpart of those elements.  cur[sl]: the
+// cases of the tables the slot holds (kept across steps when they match: block-uniform test).
 template <int PREC, int N>
 __device__ __forceinline__ void sw_local(const MeshDev &m, const SwArgs &S, const typename Pol<PREC>::TV *__restrict__ r,
-                                         int e, unsigned char *smraw, typename Pol<PREC>::TG *red, int (&cur)[3],
+                                         int e0, int ne, unsigned char *smraw, typename Pol<PREC>::TG *red,
+                                         int (&cur)[SwCfg<typename Pol<PREC>::TV, N>::EB][3],
                                          const typename Pol<PREC>::TG *__restrict__ wlut)
 {
     using TV = typename Pol<PREC>::TV;
     using TG = typename Pol<PREC>::TG;
     using C = SwCfg<TV, N>;
-    constexpr int P3 = C::P3, P2 = C::P2, PV = C::PV, N3 = N * N * N;
-    TV *F = reinterpret_cast<TV *>(smraw);
-    TV *T = F + PV;
-    TV *Sm = reinterpret_cast<TV *>(smraw + C::OFF_S);
-    double *lm = reinterpret_cast<double *>(smraw + C::OFF_L);
+    constexpr int P3 = C::P3, P2 = C::P2, N3 = N * N * N, EB = C::EB;
     const int tid = threadIdx.x;
-    const ElemPos P = elem_pos<false>(m, e);
-    const int pos[3] = {P.ex, P.ey, P.ez};
-    // the element's three 1-D tables (kept from the previous element of the block when the cases
-    // match: block-uniform test; the previous element's passes ended with a barrier)
-    const int cs0 = S.cs[0][pos[0]], cs1 = S.cs[1][pos[1]], cs2 = S.cs[2][pos[2]];
-    if (cs0 != cur[0] || cs1 != cur[1] || cs2 != cur[2]) {
-        for (int q = tid; q < 3 * P2; q += blockDim.x) {   // S_a at [a], S_a^T at [3 + a]
-            const int a = q / P2, k = q - a * P2;
-            const TV v = ((const TV *)S.S[a])[(size_t)S.cs[a][pos[a]] * P2 + k];
-            Sm[q] = v;
-            Sm[(3 + a) * P2 + (k % P3) * P3 + k / P3] = v;
+    // the slots' 1-D tables: S_a at [a], S_a^T at [3 + a]
+#pragma unroll
+    for (int sl = 0; sl < EB; sl++) {
+        if (sl >= ne) break;
+        const ElemPos P = elem_pos<false>(m, e0 + sl);
+        const int pos[3] = {P.ex, P.ey, P.ez};
+        const int cs0 = S.cs[0][P.ex], cs1 = S.cs[1][P.ey], cs2 = S.cs[2][P.ez];
+        if (cs0 != cur[sl][0] || cs1 != cur[sl][1] || cs2 != cur[sl][2]) {
+            TV *Sm = reinterpret_cast<TV *>(smraw + sl * C::SLOT + C::OFF_S);
+            double *lm = reinterpret_cast<double *>(smraw + sl * C::SLOT + C::OFF_L);
+            for (int q = tid; q < 3 * P2; q += blockDim.x) {
+                const int a = q / P2, k = q - a * P2;
+                const TV v = ((const TV *)S.S[a])[(size_t)S.cs[a][pos[a]] * P2 + k];
+                Sm[q] = v;
+                Sm[(3 + a) * P2 + (k % P3) * P3 + k / P3] = v;
+            }
+            for (int q = tid; q < 3 * P3; q += blockDim.x) {
+                const int a = q / P3, k = q - a * P3;
+                lm[q] = S.lam[a][(size_t)S.cs[a][pos[a]] * P3 + k];
+            }
+            cur[sl][0] = cs0; cur[sl][1] = cs1; cur[sl][2] = cs2;
         }
-        for (int q = tid; q < 3 * P3; q += blockDim.x) {
-            const int a = q / P3, k = q - a * P3;
-            lm[q] = S.lam[a][(size_t)S.cs[a][pos[a]] * P3 + k];
-        }
-        cur[0] = cs0; cur[1] = cs1; cur[2] = cs2;
     }
-    const uint8_t *cx = S.cnt[0] + (size_t)P.ex * P3, *cy = S.cnt[1] + (size_t)P.ey * P3, *cz = S.cnt[2] + (size_t)P.ez * P3;
-    // R_e r, its coarse restriction partials and W R_e r, one x-line (tj, tk) of the extended box
+    // R_e r, its coarse restriction partials and W R_e r, one x-line (tj, tk) of an extended box
     // per thread: the line is a row of the (y, z)-neighbour element's copy (N contiguous values)
-    // plus one value from each x-neighbour of that element
+    // plus one value from each x-neighbour of that element.  Slot sl is served by the warps
+    // [sl TPS/32, (sl+1) TPS/32) so that every warp's partials belong to one element.
+    const int TPS = ((int)(blockDim.x >> 5) / EB) * 32;
+    const int sl = tid / TPS, lt = tid - sl * TPS;
     TG cp[8];
 #pragma unroll
     for (int c = 0; c < 8; c++) cp[c] = TG(0);
     const bool coarse = S.nv[0] > 0 && S.nv[1] > 0 && S.nv[2] > 0;
-    for (int line = tid; line < P2; line += blockDim.x) {
-        const int tj = line % P3, tk = line / P3;
-        const int cyz = cy[tj] * cz[tk];
-        TV v[P3];
+    if (sl < ne) {
+        const int e = e0 + sl;
+        const ElemPos P = elem_pos<false>(m, e);
+        const uint8_t *cx = S.cnt[0] + (size_t)P.ex * P3, *cy = S.cnt[1] + (size_t)P.ey * P3, *cz = S.cnt[2] + (size_t)P.ez * P3;
+        TV *F = reinterpret_cast<TV *>(smraw + sl * C::SLOT);
+        for (int line = lt; line < P2; line += TPS) {
+            const int tj = line % P3, tk = line / P3;
+            const int cyz = cy[tj] * cz[tk];
+            TV v[P3];
 #pragma unroll
-        for (int t = 0; t < P3; t++) v[t] = TV(0);
-        if (cyz) {
-            const int dy = tj == 0 ? -1 : (tj == P3 - 1 ? 1 : 0);
-            const int dz = tk == 0 ? -1 : (tk == P3 - 1 ? 1 : 0);
-            const int lj = tj == 0 ? N - 2 : (tj == P3 - 1 ? 1 : tj - 1);
-            const int lk = tk == 0 ? N - 2 : (tk == P3 - 1 ? 1 : tk - 1);
-            const int64_t e2 = (int64_t)e + (int64_t)m.nelx * (dy + (int64_t)m.nely * dz);
-            const TV *row = r + e2 * N3 + N * (lj + N * lk);
-            TV own[N];
-            ld_pencil<TV, N>(row, own);
-            v[0] = cx[0] ? row[-N3 + N - 2] : TV(0);
-            v[P3 - 1] = cx[P3 - 1] ? row[N3 + 1] : TV(0);
+            for (int t = 0; t < P3; t++) v[t] = TV(0);
+            if (cyz) {
+                const int dy = tj == 0 ? -1 : (tj == P3 - 1 ? 1 : 0);
+                const int dz = tk == 0 ? -1 : (tk == P3 - 1 ? 1 : 0);
+                const int lj = tj == 0 ? N - 2 : (tj == P3 - 1 ? 1 : tj - 1);
+                const int lk = tk == 0 ? N - 2 : (tk == P3 - 1 ? 1 : tk - 1);
+                const int64_t e2 = (int64_t)e + (int64_t)m.nelx * (dy + (int64_t)m.nely * dz);
+                const TV *row = r + e2 * N3 + N * (lj + N * lk);
+                TV own[N];
+                ld_pencil<TV, N>(row, own);
+                v[0] = cx[0] ? row[-N3 + N - 2] : TV(0);
+                v[P3 - 1] = cx[P3 - 1] ? row[N3 + 1] : TV(0);
 #pragma unroll
-            for (int i = 0; i < N; i++) v[i + 1] = cx[i + 1] ? own[i] : TV(0);
-            if (coarse && dy == 0 && dz == 0) {   // the element's own copies: c_l phi r per corner
-                const int j = tj - 1, k = tk - 1;
-                const double cjk = 1.0 / (double)(axis_mult(j, N, P.ey, m.nely) * axis_mult(k, N, P.ez, m.nelz));
+                for (int i = 0; i < N; i++) v[i + 1] = cx[i + 1] ? own[i] : TV(0);
+                if (coarse && dy == 0 && dz == 0) {   // the element's own copies: c_l phi r per corner
+                    const int j = tj - 1, k = tk - 1;
+                    const double cjk = 1.0 / (double)(axis_mult(j, N, P.ey, m.nely) * axis_mult(k, N, P.ez, m.nelz));
 #pragma unroll
-                for (int i = 0; i < N; i++) {
-                    const double cl = cjk / (double)axis_mult(i, N, P.ex, m.nelx);
-                    const TG vi = (TG)v[i + 1];
+                    for (int i = 0; i < N; i++) {
+                        const double cl = cjk / (double)axis_mult(i, N, P.ex, m.nelx);
+                        const TG vi = (TG)v[i + 1];
 #pragma unroll
-                    for (int c = 0; c < 8; c++) {
-                        const double ph = ((c & 1) ? S.phR[i] : S.phL[i]) * ((c & 2) ? S.phR[j] : S.phL[j]) *
-                                          ((c & 4) ? S.phR[k] : S.phL[k]);
-                        cp[c] += (TG)(ph * cl) * vi;
+                        for (int c = 0; c < 8; c++) {
+                            const double ph = ((c & 1) ? S.phR[i] : S.phL[i]) * ((c & 2) ? S.phR[j] : S.phL[j]) *
+                                              ((c & 4) ? S.phR[k] : S.phL[k]);
+                            cp[c] += (TG)(ph * cl) * vi;
+                        }
                     }
                 }
+#pragma unroll
+                for (int t = 0; t < P3; t++) v[t] = (TV)((TG)v[t] * wlut[cx[t] * cyz]);
             }
 #pragma unroll
-            for (int t = 0; t < P3; t++) v[t] = (TV)((TG)v[t] * wlut[cx[t] * cyz]);
+            for (int t = 0; t < P3; t++) F[P3 * line + t] = v[t];
         }
-#pragma unroll
-        for (int t = 0; t < P3; t++) F[P3 * line + t] = v[t];
     }
-    if (coarse) {   // block sum of the 8 partials (fixed tree), stored by thread 0
-        const int lane = tid & 31, wid = tid >> 5, nw = (blockDim.x + 31) >> 5;
+    if (coarse) {   // per slot: block sum of the 8 partials over its warps (fixed tree)
+        const int lane = tid & 31, wid = tid >> 5, wps = TPS >> 5;
 #pragma unroll
         for (int c = 0; c < 8; c++)
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) cp[c] += __shfl_down_sync(0xffffffffu, cp[c], o);
-        if (lane == 0)
+        if (lane == 0 && wid < EB * wps)
 #pragma unroll
             for (int c = 0; c < 8; c++) red[wid * 8 + c] = cp[c];
         __syncthreads();
-        if (tid < 8) {
+        if (tid < ne * 8) {
+            const int s2 = tid >> 3, c = tid & 7;
             TG sacc = TG(0);
-            for (int w = 0; w < nw; w++) sacc += red[w * 8 + tid];
-            ((TG *)S.cpart)[(size_t)e * 8 + tid] = sacc;
+            for (int w = s2 * wps; w < (s2 + 1) * wps; w++) sacc += red[w * 8 + c];
+            ((TG *)S.cpart)[(size_t)(e0 + s2) * 8 + c] = sacc;
         }
     } else {
         __syncthreads();
     }
     // K_e^-1 by fast diagonalisation: S_x^T, S_y^T, S_z^T + Lambda^-1, S_z, S_y, S_x
-    sw_pass<TV, P3, 0, false>(F, T, Sm, lm);
+    constexpr int oF = 0, oT = C::PV * (int)sizeof(TV), oS = C::OFF_S, P2B = P2 * (int)sizeof(TV);
+    TV *zx = (TV *)S.zext;
+    sw_pass<TV, N, 0, false>(smraw, ne, oF, oT, oS, zx, e0);
     __syncthreads();
-    sw_pass<TV, P3, 1, false>(T, F, Sm + P2, lm);
+    sw_pass<TV, N, 1, false>(smraw, ne, oT, oF, oS + P2B, zx, e0);
     __syncthreads();
-    sw_pass<TV, P3, 2, true>(F, T, Sm + 2 * P2, lm);
+    sw_pass<TV, N, 2, true>(smraw, ne, oF, oT, oS + 2 * P2B, zx, e0);
     __syncthreads();
-    sw_pass<TV, P3, 2, false>(T, F, Sm + 5 * P2, lm);
+    sw_pass<TV, N, 2, false>(smraw, ne, oT, oF, oS + 5 * P2B, zx, e0);
     __syncthreads();
-    sw_pass<TV, P3, 1, false>(F, T, Sm + 4 * P2, lm);
+    sw_pass<TV, N, 1, false>(smraw, ne, oF, oT, oS + 4 * P2B, zx, e0);
     __syncthreads();
-    sw_pass<TV, P3, 0, false>(T, (TV *)S.zext + (size_t)e * PV, Sm + 3 * P2, lm);
-    __syncthreads();   // smem reused by the next element
+    sw_pass<TV, N, 0, false>(smraw, ne, oT, -1, oS + 3 * P2B, zx, e0);
+    __syncthreads();   // smem reused by the next step
 }
 
 // coarse pass `pass` (0: assemble b0; 1..6: the fast-diagonalisation passes), thread gt of gn
@@ -290,63 +338,78 @@ __device__ __forceinline__ void sw_gather_pencil(const MeshDev &m, const SwArgs 
     if (b >= N - 2 && P.ez < m.nelz - 1) { dz[nz_] = 1; tz[nz_++] = b - N + 2; }
     const bool xl = P.ex > 0, xr = P.ex < m.nelx - 1;
     const int cyz = S.cnt[1][(size_t)P.ey * P3 + a + 1] * S.cnt[2][(size_t)P.ez * P3 + b + 1];
-    // sum of the local solutions at the node, then the node's weight (constant over its boxes)
+    // independent loads first: r (for rho) and the element's interior corner values of x0
+    TV rr[N];
+    const size_t base = (size_t)pid * N;
+    ld_pencil<TV, N>(r + base, rr);
+    TV xc[8];
+#pragma unroll
+    for (int c = 0; c < 8; c++) {
+        const int vx = P.ex + (c & 1), vy = P.ey + ((c >> 1) & 1), vz = P.ez + (c >> 2);
+        const bool in = coarse && vx >= 1 && vx <= S.nv[0] && vy >= 1 && vy <= S.nv[1] && vz >= 1 && vz <= S.nv[2];
+        xc[c] = in ? __ldcg((const TV *)S.c0 + (vx - 1) + (int64_t)S.nv[0] * ((vy - 1) + (int64_t)S.nv[1] * (vz - 1))) : TV(0);
+    }
+    // sum of the local solutions at the node, then the node's weight (constant over its boxes);
+    // the next box row is loaded while the current one is summed
     TG acc[N];
 #pragma unroll
     for (int i = 0; i < N; i++) acc[i] = TG(0);
     if (cyz) {
-        for (int iz = 0; iz < nz_; iz++)
-            for (int iy = 0; iy < ny_; iy++) {
-                const int64_t eyz = (int64_t)e + (int64_t)m.nelx * (dy[iy] + (int64_t)m.nely * dz[iz]);
-                const TV *row = zx + eyz * PV + (int64_t)P3 * (ty[iy] + P3 * tz[iz]);
-                TV v[P3];
+        const int nrow = ny_ * nz_;
+        TV v[P3], l0, l1, r0, r1;
+        auto load_row = [&](int k, TV (&vv)[P3], TV &a0, TV &a1, TV &b0, TV &b1) {
+            const int iz = k / ny_, iy = k - iz * ny_;
+            const int64_t eyz = (int64_t)e + (int64_t)m.nelx * (dy[iy] + (int64_t)m.nely * dz[iz]);
+            const TV *row = zx + eyz * PV + (int64_t)P3 * (ty[iy] + P3 * tz[iz]);
 #pragma unroll
-                for (int c = 0; c < P3 / VR; c++) {
-                    if constexpr (VR == 4) {
-                        const float4 t = __ldcg(reinterpret_cast<const float4 *>(row) + c);
-                        v[4 * c] = t.x; v[4 * c + 1] = t.y; v[4 * c + 2] = t.z; v[4 * c + 3] = t.w;
-                    } else if constexpr (VR == 2) {
-                        const double2 t = __ldcg(reinterpret_cast<const double2 *>(row) + c);
-                        v[2 * c] = t.x; v[2 * c + 1] = t.y;
-                    } else {
-                        v[c] = __ldcg(row + c);
-                    }
-                }
-                // x-neighbours' boxes: values at their indices N, N + 1 (nodes 0, 1) and 0, 1 (nodes N - 2, N - 1)
-                const TV l0 = xl ? __ldcg(row - PV + N) : TV(0), l1 = xl ? __ldcg(row - PV + N + 1) : TV(0);
-                const TV r0 = xr ? __ldcg(row + PV) : TV(0), r1 = xr ? __ldcg(row + PV + 1) : TV(0);
-#pragma unroll
-                for (int i = 0; i < N; i++) {
-                    if (i <= 1 && xl) acc[i] += (TG)(i == 0 ? l0 : l1);
-                    acc[i] += (TG)v[i + 1];
-                    if (i >= N - 2 && xr) acc[i] += (TG)(i == N - 2 ? r0 : r1);
+            for (int c = 0; c < P3 / VR; c++) {
+                if constexpr (VR == 4) {
+                    const float4 t = __ldcg(reinterpret_cast<const float4 *>(row) + c);
+                    vv[4 * c] = t.x; vv[4 * c + 1] = t.y; vv[4 * c + 2] = t.z; vv[4 * c + 3] = t.w;
+                } else if constexpr (VR == 2) {
+                    const double2 t = __ldcg(reinterpret_cast<const double2 *>(row) + c);
+                    vv[2 * c] = t.x; vv[2 * c + 1] = t.y;
+                } else {
+                    vv[c] = __ldcg(row + c);
                 }
             }
+            // x-neighbours' boxes: values at their indices N, N + 1 (nodes 0, 1) and 0, 1 (nodes N - 2, N - 1)
+            a0 = xl ? __ldcg(row - PV + N) : TV(0); a1 = xl ? __ldcg(row - PV + N + 1) : TV(0);
+            b0 = xr ? __ldcg(row + PV) : TV(0); b1 = xr ? __ldcg(row + PV + 1) : TV(0);
+        };
+        load_row(0, v, l0, l1, r0, r1);
+        for (int k = 0; k < nrow; k++) {
+            TV vn[P3], nl0 = TV(0), nl1 = TV(0), nr0 = TV(0), nr1 = TV(0);
+            if (k + 1 < nrow) load_row(k + 1, vn, nl0, nl1, nr0, nr1);
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                if (i <= 1 && xl) acc[i] += (TG)(i == 0 ? l0 : l1);
+                acc[i] += (TG)v[i + 1];
+                if (i >= N - 2 && xr) acc[i] += (TG)(i == N - 2 ? r0 : r1);
+            }
+            if (k + 1 < nrow) {
+#pragma unroll
+                for (int t = 0; t < P3; t++) v[t] = vn[t];
+                l0 = nl0; l1 = nl1; r0 = nr0; r1 = nr1;
+            }
+        }
 #pragma unroll
         for (int i = 0; i < N; i++) acc[i] *= wlut[S.cnt[0][(size_t)P.ex * P3 + i + 1] * cyz];
     }
     if (coarse) {   // trilinear interpolation of x0 from the element's interior corner vertices:
         // g[cx] = sum_{cz, cy} hz hy x0(corner) once per pencil, then per node hx0 g[0] + hx1 g[1]
         // (corner values of boundary vertices are 0; the same arithmetic at every copy of a node)
-        const TV *x0 = (const TV *)S.c0;
         const TV hy[2] = {(TV)S.phL[a], (TV)S.phR[a]}, hz[2] = {(TV)S.phL[b], (TV)S.phR[b]};
         TV g[2] = {TV(0), TV(0)};
 #pragma unroll
-        for (int c = 0; c < 8; c++) {
-            const int vx = P.ex + (c & 1), vy = P.ey + ((c >> 1) & 1), vz = P.ez + (c >> 2);
-            const bool in = vx >= 1 && vx <= S.nv[0] && vy >= 1 && vy <= S.nv[1] && vz >= 1 && vz <= S.nv[2];
-            const TV xcv = in ? __ldcg(x0 + (vx - 1) + (int64_t)S.nv[0] * ((vy - 1) + (int64_t)S.nv[1] * (vz - 1))) : TV(0);
-            g[c & 1] = fma(hz[c >> 2] * hy[(c >> 1) & 1], xcv, g[c & 1]);
-        }
+        for (int c = 0; c < 8; c++) g[c & 1] = fma(hz[c >> 2] * hy[(c >> 1) & 1], xc[c], g[c & 1]);
 #pragma unroll
         for (int i = 0; i < N; i++) {
             if (!(cyz && S.cnt[0][(size_t)P.ex * P3 + i + 1])) continue;   // Dirichlet node
             acc[i] += (TG)fma((TV)S.phL[i], g[0], (TV)S.phR[i] * g[1]);
         }
     }
-    TV rr[N], zz[N];
-    const size_t base = (size_t)pid * N;
-    ld_pencil<TV, N>(r + base, rr);
+    TV zz[N];
     const int mjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz);
 #pragma unroll
     for (int i = 0; i < N; i++) {
