@@ -84,6 +84,9 @@ template <int N, typename TVX> struct DsRow {
     static constexpr int SMEM = 2 * EL * N3 * (int)sizeof(TVX);
 };
 
+#ifndef NB_DS_PF
+#define NB_DS_PF 0
+#endif
 template <typename TVX, typename TGX, int N>
 __global__ void __launch_bounds__(DsRow<N, TVX>::NT) k_dssum_rows(const MeshDev m, TVX *__restrict__ u)
 {
@@ -111,6 +114,17 @@ __global__ void __launch_bounds__(DsRow<N, TVX>::NT) k_dssum_rows(const MeshDev 
         const int ey = (int)(row % m.nely), ez = (int)(row / m.nely);
         const int exa = c * CH, exb = min(m.nelx, exa + CH);
         const int64_t erow = (int64_t)m.nelx * (ey + (int64_t)m.nely * ez);
+#if NB_DS_PF
+        // the block's next unit (a contiguous run of elements) into L2 while this one is summed
+        // (measured slower at 32^3: mixed p9 84 -> 93 us, fp64 p11 192 -> 227 us; off)
+        if (threadIdx.x == 0 && unit + gridDim.x < units) {
+            const int64_t un = unit + gridDim.x;
+            const int cn = (int)(un % cpr);
+            const int64_t rn = un / cpr;
+            const int xa = cn * CH, xb = min(m.nelx, xa + CH);
+            l2_prefetch(u + (rn * m.nelx + xa) * (int64_t)N3, (size_t)(xb - xa) * N3 * sizeof(TVX));
+        }
+#endif
         const bool sy = j == 0 && ey > 0, sz = k == 0 && ez > 0;
         const bool upyz = (j == N - 1 && ey < m.nely - 1) || (k == N - 1 && ez < m.nelzl - 1);
         TVX pre[PV];
