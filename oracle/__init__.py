@@ -91,8 +91,8 @@ def lib():
         L.or_glsc3_f_dot2.argtypes = [P, P, P, C.c_int64]
         L.or_two_sum_f.argtypes = [C.c_float, C.c_float, P, P]
         L.or_two_prod_f.argtypes = [C.c_float, C.c_float, P, P]
-        L.or_schwarz_apply_d.argtypes = [P, P, P]
-        L.or_schwarz_apply_f.argtypes = [P, C.c_int, P, P]
+        L.or_schwarz_apply_d.argtypes = [P, C.c_int, P, P]
+        L.or_schwarz_apply_f.argtypes = [P, C.c_int, C.c_int, P, P]
         L.or_schwarz_tables.argtypes = [P, C.c_int, C.c_int, P, P, P, P, P, P]
         L.or_cg.argtypes = [P, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                             C.c_int, P, P, P, P, C.POINTER(_Report)]
@@ -225,16 +225,18 @@ class Mesh:
             lib().or_ax_f(self._h, policy, order, _p(u), _p(w))
         return w
 
-    def schwarz(self, r: np.ndarray, policy: int = FP64) -> np.ndarray:
-        """NEXT-4: z = M^-1 r of the two-level Schwarz preconditioner under a policy."""
+    def schwarz(self, r: np.ndarray, policy: int = FP64, order: int = GS_CONSISTENT) -> np.ndarray:
+        """NEXT-4: z = M^-1 r of the two-level Schwarz preconditioner under a policy (and the
+        gather-scatter order of its overlap sum)."""
         if policy == FP64:
             r = np.ascontiguousarray(r, dtype=np.float64)
             z = np.zeros_like(r)
-            lib().or_schwarz_apply_d(self._h, _p(r), _p(z))
+            if lib().or_schwarz_apply_d(self._h, order, _p(r), _p(z)):
+                raise ValueError("or_schwarz_apply_d: bad arguments")
         else:
             r = np.ascontiguousarray(r, dtype=np.float32)
             z = np.zeros_like(r)
-            if lib().or_schwarz_apply_f(self._h, policy, _p(r), _p(z)):
+            if lib().or_schwarz_apply_f(self._h, policy, order, _p(r), _p(z)):
                 raise ValueError("or_schwarz_apply_f: bad arguments")
         return z
 

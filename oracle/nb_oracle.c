@@ -1066,7 +1066,57 @@ OR_FDM_APPLY(fdm_apply_f, float)
 
 /* z = M^-1 r on the local copies (r consistent: every copy of a global node holds its value).
    rd / zd: double vectors (SW_D); rf / zf: float vectors (SW_MIX, SW_F). */
-static void schwarz_apply(or_mesh *m, int var, const double *rd, double *zd, const float *rf, float *zf)
+/* the overlap sum of the local solutions at one copy under the gather-scatter orders of the
+   per-copy / rank-partitioned modes (NEXT-2 crossed with NEXT-4, reading 28): the
+   contributions c_k (k ascending in element order, element e_k of rank r_k, TG values) of the
+   boxes holding the node are combined like the copies of a node in the ranked dssum
+   (OR_DSSUM_RANKED): OR_GS_PER_COPY: the copy's own element's box first, then the others
+   ascending; OR_GS_PAIRWISE: rank partials (ascending within a rank), the copy's own rank's first,
+   then the other ranks ascending; OR_GS_ALLREDUCE: all rank partials in ascending rank order. */
+#define OR_SW_COMBINE(NAME, TGX)                                                                  \
+    static TGX NAME(int order, int cnt, const TGX *c, const int64_t *ek, const int *rk, int64_t eown, int rown) \
+    {                                                                                             \
+        TGX t = 0;                                                                                \
+        if (order == OR_GS_PER_COPY) {                                                            \
+            for (int k = 0; k < cnt; k++)                                                         \
+                if (ek[k] == eown) t += c[k];                                                     \
+            for (int k = 0; k < cnt; k++)                                                         \
+                if (ek[k] != eown) t += c[k];                                                     \
+            return t;                                                                             \
+        }                                                                                         \
+        TGX part[27];                                                                             \
+        for (int k = 0; k < cnt; k++) {                                                           \
+            TGX u = 0;                                                                            \
+            for (int k2 = 0; k2 < cnt; k2++)                                                      \
+                if (rk[k2] == rk[k]) u += c[k2];                                                  \
+            part[k] = u;                                                                          \
+        }                                                                                         \
+        int own = -1;                                                                             \
+        for (int k = 0; k < cnt; k++)                                                             \
+            if (rk[k] == rown) { own = k; break; }                                                \
+        if (order == OR_GS_PAIRWISE && own >= 0) t = part[own];                                   \
+        int prev = -1;                                                                            \
+        for (;;) {                                                                                \
+            int best = -1;                                                                        \
+            for (int k = 0; k < cnt; k++)                                                         \
+                if (rk[k] > prev && (best < 0 || rk[k] < rk[best])) best = k;                     \
+            if (best < 0) break;                                                                  \
+            prev = rk[best];                                                                      \
+            if (order == OR_GS_PAIRWISE && own >= 0 && rk[best] == rown) continue;                \
+            t += part[best];                                                                      \
+        }                                                                                         \
+        return t;                                                                                 \
+    }
+OR_SW_COMBINE(sw_combine_d, double)
+OR_SW_COMBINE(sw_combine_f, float)
+
+static void schwarz_apply_ord(or_mesh *m, int var, int order, const double *rd, double *zd, const float *rf, float *zf);
+static inline void schwarz_apply(or_mesh *m, int var, const double *rd, double *zd, const float *rf, float *zf)
+{
+    schwarz_apply_ord(m, var, OR_GS_CONSISTENT, rd, zd, rf, zf);
+}
+
+static void schwarz_apply_ord(or_mesh *m, int var, int order, const double *rd, double *zd, const float *rf, float *zf)
 {
     struct or_schwarz *sw = schwarz_setup(m);
     const int p = m->p, P3 = p + 3, n = m->n;
@@ -1088,6 +1138,11 @@ static void schwarz_apply(or_mesh *m, int var, const double *rd, double *zd, con
     float *dlf = (float *)malloc(mx * sizeof(float));
     float *Sxf = (float *)malloc(P3 * P3 * sizeof(float)), *Syf = (float *)malloc(P3 * P3 * sizeof(float));
     float *Szf = (float *)malloc(P3 * P3 * sizeof(float));
+    /* per element (other orders): the unweighted local solution on its box (TG values) */
+    const int ordered = order != OR_GS_CONSISTENT;
+    double *ue_d = ordered && var != SW_F ? (double *)calloc((size_t)m->E * P3 * P3 * P3, sizeof(double)) : NULL;
+    float *ue_f = ordered && var == SW_F ? (float *)calloc((size_t)m->E * P3 * P3 * P3, sizeof(float)) : NULL;
+    double *cgd = (double *)calloc(NG, sizeof(double));   /* coarse term per node (TV value widened) */
     /* 2. local solves on the extended boxes, elements in ascending order */
     for (int64_t e = 0; e < m->E; e++) {
         int ex, ey, ez;
@@ -1130,6 +1185,8 @@ static void schwarz_apply(or_mesh *m, int var, const double *rd, double *zd, con
                     if (var == SW_D) zg[G] = zg[G] + ud[q] * (1.0 / sqrt((double)cnt));
                     else if (var == SW_MIX) zg[G] = zg[G] + (double)uf[q] * (1.0 / sqrt((double)cnt));
                     else zgf[G] = zgf[G] + uf[q] * (1.0f / sqrtf((float)cnt));
+                    if (ue_d) ue_d[(size_t)e * P3 * P3 * P3 + q] = var == SW_D ? ud[q] : (double)uf[q];
+                    if (ue_f) ue_f[(size_t)e * P3 * P3 * P3 + q] = uf[q];
                 }
     }
     /* 3. coarse correction: b0 = Phi^T r (sums in fp64 unless SW_F), x0 = A0^-1 b0, z += Phi x0 */
@@ -1194,6 +1251,7 @@ static void schwarz_apply(or_mesh *m, int var, const double *rd, double *zd, con
                     if (var == SW_D) zg[G] = zg[G] + sd;
                     else if (var == SW_MIX) zg[G] = zg[G] + (double)sf;
                     else zgf[G] = zgf[G] + sf;
+                    cgd[G] = var == SW_D ? sd : (double)sf;
                 }
         free(b0); free(x0); free(c1); free(c2); free(dl0); free(b0f); free(x0f); free(c1f); free(c2f); free(dl0f);
         free(S0x); free(S0y); free(S0z);
@@ -1205,21 +1263,57 @@ static void schwarz_apply(or_mesh *m, int var, const double *rd, double *zd, con
         else if (var == SW_MIX) zf[l] = m->mask[l] ? (float)zg[G] : 0.0f;
         else zf[l] = m->mask[l] ? zgf[G] : 0.0f;
     }
-    (void)n;
+    /* 4'. other gather-scatter orders: every copy combines the box contributions of its node in
+       its own order (OR_SW_COMBINE), then adds the coarse term */
+    if (ordered) {
+        const int64_t n3 = (int64_t)n * n * n;
+        for (int64_t l = 0; l < NL; l++) {
+            if (!m->mask[l]) continue;
+            const int64_t G = m->gid[l];
+            const int I = (int)(G % NX), J = (int)((G / NX) % NY), K = (int)(G / (NX * NY));
+            const int cnt = ov_count(m->nelx, p, I) * ov_count(m->nely, p, J) * ov_count(m->nelz, p, K);
+            double cd[27];
+            float cf[27];
+            int64_t ek[27];
+            int rk[27];
+            int nc = 0;
+            for (int ez = K / p - 1; ez <= K / p + 1; ez++)
+                for (int ey = J / p - 1; ey <= J / p + 1; ey++)
+                    for (int ex = I / p - 1; ex <= I / p + 1; ex++) {
+                        if (ex < 0 || ex >= m->nelx || ey < 0 || ey >= m->nely || ez < 0 || ez >= m->nelz) continue;
+                        const int I0 = X->t0[ex], J0 = Y->t0[ey], K0 = Z->t0[ez];
+                        const int nx = X->nt[ex], ny = Y->nt[ey], nz = Z->nt[ez];
+                        if (I < I0 || I >= I0 + nx || J < J0 || J >= J0 + ny || K < K0 || K >= K0 + nz) continue;
+                        const int64_t e = ex + (int64_t)m->nelx * (ey + (int64_t)m->nely * ez);
+                        const size_t q = (size_t)e * P3 * P3 * P3 + (size_t)((I - I0) + nx * ((J - J0) + ny * (K - K0)));
+                        if (var == SW_F) cf[nc] = ue_f[q] * (1.0f / sqrtf((float)cnt));
+                        else cd[nc] = ue_d[q] * (1.0 / sqrt((double)cnt));
+                        ek[nc] = e;
+                        rk[nc] = elem_rank(m, e);
+                        nc++;
+                    }
+            const int64_t eown = l / n3;
+            const int rown = elem_rank(m, eown);
+            if (var == SW_D) zd[l] = sw_combine_d(order, nc, cd, ek, rk, eown, rown) + cgd[G];
+            else if (var == SW_MIX) zf[l] = (float)(sw_combine_d(order, nc, cd, ek, rk, eown, rown) + cgd[G]);
+            else zf[l] = sw_combine_f(order, nc, cf, ek, rk, eown, rown) + (float)cgd[G];
+        }
+    }
+    free(ue_d); free(ue_f); free(cgd);
     free(rg); free(zg); free(rgf); free(zgf); free(fd); free(ud); free(w1d); free(w2d); free(dld);
     free(ff); free(uf); free(w1f); free(w2f); free(dlf); free(Sxf); free(Syf); free(Szf);
 }
 
-int or_schwarz_apply_d(or_mesh *m, const double *r, double *z)
+int or_schwarz_apply_d(or_mesh *m, int order, const double *r, double *z)
 {
-    if (!m || !r || !z) return 1;
-    schwarz_apply(m, SW_D, r, z, NULL, NULL);
+    if (!m || !r || !z || order < OR_GS_CONSISTENT || order > OR_GS_ALLREDUCE) return 1;
+    schwarz_apply_ord(m, SW_D, order, r, z, NULL, NULL);
     return 0;
 }
-int or_schwarz_apply_f(or_mesh *m, int policy, const float *r, float *z)
+int or_schwarz_apply_f(or_mesh *m, int policy, int order, const float *r, float *z)
 {
-    if (!m || !r || !z || policy == OR_FP64) return 1;
-    schwarz_apply(m, policy == OR_MIXED ? SW_MIX : SW_F, NULL, NULL, r, z);
+    if (!m || !r || !z || policy == OR_FP64 || order < OR_GS_CONSISTENT || order > OR_GS_ALLREDUCE) return 1;
+    schwarz_apply_ord(m, policy == OR_MIXED ? SW_MIX : SW_F, order, NULL, NULL, r, z);
     return 0;
 }
 /* the fast-diagonalisation tables: per axis a and element position ex, t0/nt and S, lambda
@@ -1308,7 +1402,7 @@ static int cg_fp64(const or_mesh *m, int max_iter, double rtol, int order, int W
     else {
         for (k = 1; k <= max_iter; k++) {
             if (pc == OR_PC_IDENTITY) for (int64_t l = 0; l < NL; l++) z[l] = r[l];  /* solveM: none */
-            else if (pc == OR_PC_SCHWARZ) schwarz_apply((or_mesh *)m, SW_D, r, z, NULL, NULL);   /* NEXT-4 */
+            else if (pc == OR_PC_SCHWARZ) schwarz_apply_ord((or_mesh *)m, SW_D, order, r, z, NULL, NULL);   /* NEXT-4 */
             else for (int64_t l = 0; l < NL; l++) z[l] = r[l] * m->dinv[l];          /* solveM */
             rho = or_glsc3_d(r, m->c, z, NL);                                        /* glsc3 */
             double beta = (k == 1) ? 0.0 : rho / rho_old;
@@ -1362,7 +1456,7 @@ static int cg_f32(const or_mesh *m, int policy, int max_iter, double rtol, int o
             /* solveM: mixed z = (float)((double)r * dinv64); fp32 (and the Neko-style fp32 copy
                under mixed) z = r * dinv32; identity z = r */
             if (pc == OR_PC_IDENTITY) for (int64_t l = 0; l < NL; l++) z[l] = r[l];
-            else if (pc == OR_PC_SCHWARZ) schwarz_apply((or_mesh *)m, mixed ? SW_MIX : SW_F, NULL, NULL, r, z);
+            else if (pc == OR_PC_SCHWARZ) schwarz_apply_ord((or_mesh *)m, mixed ? SW_MIX : SW_F, order, NULL, NULL, r, z);
             else if (mixed && pc == OR_PC_JACOBI) for (int64_t l = 0; l < NL; l++) z[l] = (float)((double)r[l] * m->dinv[l]);
             else for (int64_t l = 0; l < NL; l++) z[l] = r[l] * m->dinvf[l];
             float beta_f;

@@ -105,12 +105,15 @@ enum { OR_PC_JACOBI = 0, OR_PC_IDENTITY = 1, OR_PC_JACOBI_F32 = 2, OR_PC_SCHWARZ
  * Galerkin coarse operator on the interior element vertices; both by fast diagonalisation.
  * _d: fp64.  _f: policy OR_MIXED (fp32 arithmetic, sqrt / weights and the sums over subdomains
  * in fp64) or OR_FP32 / OR_FP32_DOT2 (all fp32).  Also or_cg(precond = OR_PC_SCHWARZ).
+ * order: the gather-scatter order of the overlap sum (OR_GS_*; the ranked orders use the
+ * or_set_ranks partition): the box contributions at a copy are combined like the copies of a
+ * node in or_dssum (own element's box / own rank's partial first, ...); or_cg passes its gs_order.
  * or_schwarz_tables: the 1-D tables of axis a (0 x, 1 y, 2 z) at element position ex: first
  * lattice index and size of the extended index set, S ((p+3) x (p+3), row-major) and lambda
  * (p+3); the coarse S0 (nv x nv, nv = nel_a - 1) and lambda0 (nullable outputs).
  */
-int or_schwarz_apply_d(or_mesh *m, const double *r, double *z);
-int or_schwarz_apply_f(or_mesh *m, int policy, const float *r, float *z);
+int or_schwarz_apply_d(or_mesh *m, int order, const double *r, double *z);
+int or_schwarz_apply_f(or_mesh *m, int policy, int order, const float *r, float *z);
 int or_schwarz_tables(or_mesh *m, int axis, int ex, int *t0, int *nt, double *S, double *lam, double *S0, double *lam0);
 int or_cg(const or_mesh *m, int policy, int max_iter, double rtol, int gs_order, int stag_window,
           int seqdot, int x64, int precond, const double *b64, double *x_out, double *hist, double *scal,

@@ -239,3 +239,56 @@ def test_schwarz_policy_precision_rules():
     assert em < 1e-5 and ef < 1e-5
     assert em < ef
     assert not np.array_equal(zm, zf)
+
+
+def test_schwarz_orders_reduce_to_textbook_cases():
+    """The overlap sum under the per-copy / ranked gather-scatter orders (NEXT-2 x NEXT-4): one
+    rank -> pairwise = allreduce = consistent bit for bit; in fp64 every order agrees to rounding;
+    allreduce keeps the fp32 copies consistent, pairwise over four ranks does not."""
+    m = oracle.Mesh(4, 3, 2, 5, 0.1, 0)
+    gid, mask, _, _ = m.maps()
+    r = m.rhs(seed=2)
+    zc = m.schwarz(r, oracle.FP64)
+    zcf = m.schwarz(r.astype(np.float32), oracle.FP32)
+    m.set_ranks(1, 1, 1)
+    for order in (oracle.GS_PAIRWISE, oracle.GS_ALLREDUCE):
+        assert np.array_equal(m.schwarz(r, oracle.FP64, order), zc)
+        assert np.array_equal(m.schwarz(r.astype(np.float32), oracle.FP32, order), zcf)
+    m.set_ranks(2, 2, 1)
+    for order in (oracle.GS_PER_COPY, oracle.GS_PAIRWISE, oracle.GS_ALLREDUCE):
+        z = m.schwarz(r, oracle.FP64, order)
+        assert np.max(np.abs(z - zc)) <= 1e-14 * np.max(np.abs(zc))
+
+    def inconsistent(z):
+        zg = np.full(m.n_global, np.nan)
+        zg[gid] = z
+        return int(np.count_nonzero(z != zg[gid]))
+
+    assert inconsistent(m.schwarz(r.astype(np.float32), oracle.FP32, oracle.GS_ALLREDUCE)) == 0
+    assert inconsistent(m.schwarz(r.astype(np.float32), oracle.FP32, oracle.GS_PAIRWISE)) > 0
+    assert inconsistent(m.schwarz(r.astype(np.float32), oracle.MIXED, oracle.GS_PAIRWISE)) == 0
+    m.set_ranks(1, 1, 1)
+
+
+def test_table3_schwarz_pcg():
+    """PAPER.md:324-341, :704-709 for the multigrid (Schwarz) PCG: with the preconditioner's square
+    roots in fp64 (here: any IEEE sqrt), fp32 with the pairwise gather-scatter still stagnates on
+    >= 4 ranks while two ranks, allreduce, or fp64 gather-scatter (the mixed policy) converge in the
+    fp64 iteration count -- "the biggest need for more accuracy lies in global communication"."""
+    m = oracle.Mesh(6, 6, 6, 5)
+    b = m.rhs()
+    _, _, r64 = m.cg(b, oracle.FP64, 300, 1e-10, precond=oracle.PC_SCHWARZ)
+    assert r64.status == oracle.CONVERGED
+    kw = dict(max_iter=120, rtol=1e-10, stag_window=40, precond=oracle.PC_SCHWARZ)
+    for ranks in ((2, 2, 2), (2, 2, 1)):
+        m.set_ranks(*ranks)
+        _, _, rp = m.cg(b, oracle.FP32, gs_order=oracle.GS_PAIRWISE, **kw)
+        assert rp.status in (oracle.STAGNATED, oracle.BREAKDOWN) and rp.rel_res_min > 1e-10, ranks
+        _, _, ra = m.cg(b, oracle.FP32, gs_order=oracle.GS_ALLREDUCE, **kw)
+        assert ra.status == oracle.CONVERGED and abs(ra.iterations - r64.iterations) <= 1
+        _, _, rm = m.cg(b, oracle.MIXED, gs_order=oracle.GS_PAIRWISE, **kw)
+        assert rm.status == oracle.CONVERGED and abs(rm.iterations - r64.iterations) <= 1
+    m.set_ranks(1, 1, 2)
+    _, _, r2 = m.cg(b, oracle.FP32, gs_order=oracle.GS_PAIRWISE, **kw)
+    assert r2.status == oracle.CONVERGED and abs(r2.iterations - r64.iterations) <= 1
+    m.set_ranks(1, 1, 1)
