@@ -118,8 +118,10 @@ typedef struct {
  *                     Galerkin coarse level on the interior element vertices.  Precision: the
  *                     policy's vector type for the fast-diagonalisation arithmetic; square roots,
  *                     weights and the sums over subdomains in the gather-scatter precision (fp64
- *                     under NB_MIXED, the paper's "sqrt and GS in fp64").  Whole-box handles,
- *                     consistent GS order only (NB_EINVAL otherwise). */
+ *                     under NB_MIXED, the paper's "sqrt and GS in fp64").  Whole-box handles
+ *                     (NB_EINVAL otherwise); every gs_order: the per-copy / pairwise / allreduce
+ *                     orders also combine the overlapping local solutions at each copy in that
+ *                     order (own element's / own rank's contribution first, ...). */
 typedef enum { NB_PC_JACOBI = 0, NB_PC_IDENTITY = 1, NB_PC_JACOBI_F32 = 2, NB_PC_SCHWARZ = 3 } nb_precond;
 
 typedef struct {

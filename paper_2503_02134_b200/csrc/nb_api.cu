@@ -591,6 +591,8 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
                (int)o->x_fp64, ws0.tim, A);
         A.wlo = A.whi = nullptr;
         nb::sw_fill(h0, prec, A.sw);
+        A.rp = nb::RankPart{o->ranks[0] > 0 ? o->ranks[0] : 1, o->ranks[1] > 0 ? o->ranks[1] : 1,
+                            o->ranks[2] > 0 ? o->ranks[2] : 1};
         NB_CU(cudaMemsetAsync(ws0.bar, 0, 2 * sizeof(unsigned int), st), "memset bar");
         NB_CU(NB_POL(prec, nb::launch_cg_sw, h0, A, ws0.mega_G, false, st), "cg Schwarz megakernel");
         launches = 1;
@@ -691,7 +693,6 @@ static int cg_args(nb_handle *h, const nb_cg_opts *o)
     if (o->policy < NB_FP64 || o->policy > NB_FP32_DOT2) return fail(NB_EINVAL, "bad policy");
     if (o->precond < NB_PC_JACOBI || o->precond > NB_PC_SCHWARZ) return fail(NB_EINVAL, "bad precond");
     if (o->precond == NB_PC_SCHWARZ) {
-        if (o->gs_order != NB_GS_CONSISTENT) return fail(NB_EINVAL, "NB_PC_SCHWARZ runs with the consistent GS order");
         if (h->nelzl != h->nelz || h->ws[o->policy].peer.nrank > 0)
             return fail(NB_EINVAL, "NB_PC_SCHWARZ needs a whole-box handle (no slabs, no peers)");
     }

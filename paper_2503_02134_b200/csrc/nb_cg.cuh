@@ -1191,11 +1191,12 @@ k_cg_mega_mr(const __grid_constant__ MultiArgs M, const __grid_constant__ DMat<t
 
 // Schwarz-preconditioned solve (NB_PC_SCHWARZ): the same body with the
 // preconditioner phases of nb_schwarz.cuh between phase B and the next phase A (VAR = 3).
-template <int PREC, int N>
+// FUSED = 0: the per-copy / ranked gather-scatter orders (CSR phase for Ax, ordered overlap sum).
+template <int PREC, int N, int FUSED>
 __global__ void NB_KERNEL_BOUNDS(AxCfg<typename Pol<PREC>::TV, N>)
 k_cg_sw(const __grid_constant__ MegaArgs A, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D)
 {
-    constexpr int FUSED = 1, VAR = 3;
+    constexpr int VAR = 3;
     const MrArgs *const mr = nullptr;
     const int vr = 0, bid = 0, G = 0;
     (void)vr; (void)bid; (void)G; (void)mr;

@@ -156,13 +156,13 @@ cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int
 
 // ---- Schwarz-preconditioned solve (k_cg_sw) and solveM alone (k_sw_apply), NEXT-4 ----
 // Full occupancy grid (every block resident), at most `gmax` blocks (the workspace's partials).
-template <int PREC, int N, bool APPLY>
+template <int PREC, int N, bool APPLY, int FUSED>
 static cudaError_t sw_launch_t(const nb_handle *h, const MegaArgs &A, int gmax, cudaStream_t st)
 {
     using TV = typename Pol<PREC>::TV;
     using C = AxCfg<TV, N>;
     constexpr int SMEM = C::SMEM > SwCfg<TV, N>::SMEM ? C::SMEM : SwCfg<TV, N>::SMEM;
-    const void *fn = APPLY ? (const void *)k_sw_apply<PREC, N> : (const void *)k_cg_sw<PREC, N>;
+    const void *fn = APPLY ? (const void *)k_sw_apply<PREC, N> : (const void *)k_cg_sw<PREC, N, FUSED>;
     static DevCache cache;
     int &occ = cache.here();
     if (occ < 0) {
@@ -185,8 +185,9 @@ static cudaError_t sw_launch_t(const nb_handle *h, const MegaArgs &A, int gmax, 
 template <int PREC>
 cudaError_t launch_cg_sw(const nb_handle *h, const MegaArgs &A, int gmax, bool apply_only, cudaStream_t st)
 {
-    if (apply_only) { NB_DISPATCH_N(h->n, return (sw_launch_t<PREC, NN, true>(h, A, gmax, st))) }
-    NB_DISPATCH_N(h->n, return (sw_launch_t<PREC, NN, false>(h, A, gmax, st)))
+    if (apply_only) { NB_DISPATCH_N(h->n, return (sw_launch_t<PREC, NN, true, 1>(h, A, gmax, st))) }
+    if (A.order == NB_GS_CONSISTENT && !h->cg_csr) { NB_DISPATCH_N(h->n, return (sw_launch_t<PREC, NN, false, 1>(h, A, gmax, st))) }
+    NB_DISPATCH_N(h->n, return (sw_launch_t<PREC, NN, false, 0>(h, A, gmax, st)))
 }
 
 // ---- multi-rank (z-slab) megakernel: consistent order, runtime options ----

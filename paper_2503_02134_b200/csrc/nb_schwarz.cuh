@@ -19,6 +19,7 @@
 // Grid barriers separate the phases (the caller passes the barrier counter and target).
 #pragma once
 #include "nb_common.cuh"
+#include "nb_gs.cuh"   // elem_rank
 
 namespace nb {
 
@@ -414,6 +415,105 @@ __device__ __forceinline__ void sw_gather_pencil(const MeshDev &m, const SwArgs 
 #pragma unroll
     for (int i = 0; i < N; i++) {
         zz[i] = (TV)acc[i];
+        const TS c = (TS)1 / (TS)(mjk * axis_mult(i, N, P.ex, m.nelx));
+        const TS rs = (TS)rr[i];
+        rho.add(rs * c, (TS)zz[i]);
+    }
+    st_pencil<TV, N>(z + base, zz);
+}
+
+// S2 under the per-copy / rank-partitioned gather-scatter orders (NEXT-2 x NEXT-4; the oracle's
+// OR_SW_COMBINE): per node, the weighted contributions of the boxes holding it (ascending element
+// order, with each box's element and rank) are combined -- per-copy: the pencil's own element's box
+// first, then the others; pairwise: rank partials (ascending within a rank), the own rank's first,
+// then the other ranks ascending; allreduce: all rank partials ascending.  Then the coarse term.
+template <int PREC, int N>
+__device__ __forceinline__ void sw_gather_pencil_ordered(const MeshDev &m, const SwArgs &S, int order, const RankPart &rp,
+                                                         const typename Pol<PREC>::TV *__restrict__ r,
+                                                         typename Pol<PREC>::TV *__restrict__ z, int64_t pid,
+                                                         Acc<PREC> &rho, const typename Pol<PREC>::TG *__restrict__ wlut)
+{
+    using TV = typename Pol<PREC>::TV;
+    using TG = typename Pol<PREC>::TG;
+    using TS = typename Pol<PREC>::TS;
+    constexpr int N2 = N * N, P3 = N + 2, P2 = P3 * P3, PV = P2 * P3;
+    const int e = (int)(pid / N2);
+    const int q = (int)(pid - (int64_t)e * N2);
+    const int a = q % N, b = q / N;
+    const ElemPos P = elem_pos<false>(m, e);
+    const TV *zx = (const TV *)S.zext;
+    const bool coarse = S.nv[0] > 0 && S.nv[1] > 0 && S.nv[2] > 0;
+    const int rown = elem_rank(m, rp, e);
+    TV xc[8];
+#pragma unroll
+    for (int c = 0; c < 8; c++) {
+        const int vx = P.ex + (c & 1), vy = P.ey + ((c >> 1) & 1), vz = P.ez + (c >> 2);
+        const bool in = coarse && vx >= 1 && vx <= S.nv[0] && vy >= 1 && vy <= S.nv[1] && vz >= 1 && vz <= S.nv[2];
+        xc[c] = in ? __ldcg((const TV *)S.c0 + (vx - 1) + (int64_t)S.nv[0] * ((vy - 1) + (int64_t)S.nv[1] * (vz - 1))) : TV(0);
+    }
+    const TV hy[2] = {(TV)S.phL[a], (TV)S.phR[a]}, hz[2] = {(TV)S.phL[b], (TV)S.phR[b]};
+    TV g[2] = {TV(0), TV(0)};
+#pragma unroll
+    for (int c = 0; c < 8; c++) g[c & 1] = fma(hz[c >> 2] * hy[(c >> 1) & 1], xc[c], g[c & 1]);
+    const int cyz = S.cnt[1][(size_t)P.ey * P3 + a + 1] * S.cnt[2][(size_t)P.ez * P3 + b + 1];
+    TV rr[N], zz[N];
+    const size_t base = (size_t)pid * N;
+    ld_pencil<TV, N>(r + base, rr);
+    const int mjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz);
+    for (int i = 0; i < N; i++) {
+        const int cnt = S.cnt[0][(size_t)P.ex * P3 + i + 1] * cyz;
+        TG acc = TG(0);
+        if (cnt) {
+            const TG w = wlut[cnt];
+            TG cv[27];
+            int ce[27], cr[27], nc = 0;
+            for (int dz = -1; dz <= 1; dz++) {
+                const int tz = b + 1 - dz * (N - 1);   // the node's index in that element's box
+                if (P.ez + dz < 0 || P.ez + dz >= m.nelz || tz < 0 || tz >= P3) continue;
+                for (int dy = -1; dy <= 1; dy++) {
+                    const int ty = a + 1 - dy * (N - 1);
+                    if (P.ey + dy < 0 || P.ey + dy >= m.nely || ty < 0 || ty >= P3) continue;
+                    for (int dx = -1; dx <= 1; dx++) {
+                        const int tx = i + 1 - dx * (N - 1);
+                        if (P.ex + dx < 0 || P.ex + dx >= m.nelx || tx < 0 || tx >= P3) continue;
+                        const int e2 = e + dx + m.nelx * (dy + m.nely * dz);
+                        cv[nc] = (TG)__ldcg(zx + (int64_t)e2 * PV + tx + P3 * (ty + P3 * tz)) * w;
+                        ce[nc] = e2;
+                        cr[nc] = elem_rank(m, rp, e2);
+                        nc++;
+                    }
+                }
+            }
+            if (order == NB_GS_PER_COPY) {
+                for (int k = 0; k < nc; k++)
+                    if (ce[k] == e) acc += cv[k];
+                for (int k = 0; k < nc; k++)
+                    if (ce[k] != e) acc += cv[k];
+            } else {
+                int own = -1;
+                for (int k = 0; k < nc; k++)
+                    if (cr[k] == rown) { own = k; break; }
+                auto part = [&](int rk) {
+                    TG u = TG(0);
+                    for (int k2 = 0; k2 < nc; k2++)
+                        if (cr[k2] == rk) u += cv[k2];
+                    return u;
+                };
+                if (order == NB_GS_PAIRWISE && own >= 0) acc = part(rown);
+                int prev = -1;
+                for (;;) {
+                    int best = -1;
+                    for (int k = 0; k < nc; k++)
+                        if (cr[k] > prev && (best < 0 || cr[k] < cr[best])) best = k;
+                    if (best < 0) break;
+                    prev = cr[best];
+                    if (order == NB_GS_PAIRWISE && own >= 0 && cr[best] == rown) continue;
+                    acc += part(cr[best]);
+                }
+            }
+            if (coarse) acc += (TG)fma((TV)S.phL[i], g[0], (TV)S.phR[i] * g[1]);
+        }
+        zz[i] = (TV)acc;
         const TS c = (TS)1 / (TS)(mjk * axis_mult(i, N, P.ex, m.nelx));
         const TS rs = (TS)rr[i];
         rho.add(rs * c, (TS)zz[i]);
