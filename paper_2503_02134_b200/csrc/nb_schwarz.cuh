@@ -28,10 +28,12 @@ namespace nb {
 #endif
 template <typename TV, int N> struct SwCfg {
     static constexpr int P3 = N + 2, P2 = P3 * P3, PV = P2 * P3;
-    // one slot: F, T [PV] (TV); S_x, S_y, S_z and their transposes [P2] (TV); lambda_x,y,z [P3] (double)
+    // one slot: F, T [PV] (TV); S_x, S_y, S_z and their transposes [P2] (TV); lambda_x,y,z [P3] (double);
     static constexpr int OFF_S = 2 * PV * (int)sizeof(TV);
     static constexpr int OFF_L = ((OFF_S + 6 * P2 * (int)sizeof(TV)) + 15) / 16 * 16;
-    static constexpr int SLOT = ((OFF_L + 3 * P3 * 8) + 15) / 16 * 16;
+    // D [PV] (TV): 1/(lambda_x + lambda_y + lambda_z) per box point, rebuilt with the tables
+    static constexpr int OFF_D = ((OFF_L + 3 * P3 * 8) + 15) / 16 * 16;
+    static constexpr int SLOT = ((OFF_D + PV * (int)sizeof(TV)) + 15) / 16 * 16;
     // elements per S1 step (slots): NB_SW_EB while the slots fit in 110 KB, else 1
     static constexpr int EB = (NB_SW_EB * SLOT <= 110 * 1024) ? NB_SW_EB : 1;
     static constexpr int SMEM = EB * SLOT;
@@ -60,8 +62,9 @@ __device__ __forceinline__ void sw_weights_init(TG *wlut)
 // outputs in packed FMAs (FFMA2) fed by 8-byte shared loads.  l outermost (unrolled by 2): one row
 // of M live at a time (all P3^2 coefficients hoisted into registers would spill at the
 // megakernel's register cap).  SCALE: multiply output (ti,tj,tk) by 1/(lx[ti] + ly[tj] + lz[tk])
-// (computed in double, rounded once to TV).  Byte offsets within a slot: IN, OUT (OUT < 0: the
-// global zext of the slot's element), M; the slot's lambdas at SwCfg::OFF_L.
+// (the slot's table at SwCfg::OFF_D, computed in double and rounded once to TV when the slot's
+// 1-D tables change).  Byte offsets within a slot: IN, OUT (OUT < 0: the global zext of the
+// slot's element), M.
 template <typename TV, int N, int AXIS, bool SCALE>
 __device__ __forceinline__ void sw_pass(unsigned char *smraw, int ne, int in_off, int out_off, int m_off,
                                         TV *__restrict__ zext, int e0)
@@ -74,7 +77,7 @@ __device__ __forceinline__ void sw_pass(unsigned char *smraw, int ne, int in_off
         unsigned char *slot = smraw + sl * C::SLOT;
         const TV *in = reinterpret_cast<const TV *>(slot + in_off);
         const TV *M = reinterpret_cast<const TV *>(slot + m_off);
-        const double *lm = reinterpret_cast<const double *>(slot + C::OFF_L);
+        const TV *dl = reinterpret_cast<const TV *>(slot + C::OFF_D);
         TV *out = out_off >= 0 ? reinterpret_cast<TV *>(slot + out_off) : zext + (size_t)(e0 + sl) * C::PV;
         const int u = line % P3, w = line / P3;
         // base index and stride of the line along AXIS
@@ -127,10 +130,7 @@ __device__ __forceinline__ void sw_pass(unsigned char *smraw, int ne, int in_off
 #pragma unroll
         for (int l = 0; l < P3; l++) {
             TV val = o[l];
-            if (SCALE) {   // AXIS == 2: (ti, tj) = (u, w), tk = l
-                const double d = 1.0 / (lm[u] + lm[P3 + w] + lm[2 * P3 + l]);
-                val = val * (TV)d;
-            }
+            if (SCALE) val = val * dl[base + st * l];   // AXIS == 2: point (u, w, l)
             out[base + st * l] = val;
         }
     }
@@ -169,6 +169,12 @@ __device__ __forceinline__ void sw_local(const MeshDev &m, const SwArgs &S, cons
             for (int q = tid; q < 3 * P3; q += blockDim.x) {
                 const int a = q / P3, k = q - a * P3;
                 lm[q] = S.lam[a][(size_t)S.cs[a][pos[a]] * P3 + k];
+            }
+            __syncthreads();
+            TV *dl = reinterpret_cast<TV *>(smraw + sl * C::SLOT + C::OFF_D);
+            for (int q = tid; q < C::PV; q += blockDim.x) {   // in double, rounded once to TV
+                const int ti = q % P3, tj = (q / P3) % P3, tk = q / P2;
+                dl[q] = (TV)(1.0 / (lm[ti] + lm[P3 + tj] + lm[2 * P3 + tk]));
             }
             cur[sl][0] = cs0; cur[sl][1] = cs1; cur[sl][2] = cs2;
         }
