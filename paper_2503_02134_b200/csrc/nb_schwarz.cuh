@@ -24,7 +24,7 @@
 namespace nb {
 
 #ifndef NB_SW_EB
-#define NB_SW_EB 2
+#define NB_SW_EB 0   // 0: the measured choice per data size and order (SwCfg::EBW)
 #endif
 template <typename TV, int N> struct SwCfg {
     static constexpr int P3 = N + 2, P2 = P3 * P3, PV = P2 * P3;
@@ -34,8 +34,12 @@ template <typename TV, int N> struct SwCfg {
     // D [PV] (TV): 1/(lambda_x + lambda_y + lambda_z) per box point, rebuilt with the tables
     static constexpr int OFF_D = ((OFF_L + 3 * P3 * 8) + 15) / 16 * 16;
     static constexpr int SLOT = ((OFF_D + PV * (int)sizeof(TV)) + 15) / 16 * 16;
-    // elements per S1 step (slots): NB_SW_EB while the slots fit in 110 KB, else 1
-    static constexpr int EB = (NB_SW_EB * SLOT <= 110 * 1024) ? NB_SW_EB : 1;
+    // elements per S1 step (slots), while the slots fit in 110 KB, else 1.  Measured (solveM alone,
+    // 32^3, profiles/r2_ab_schwarz_eb.txt): 2 for p = 7 and fp64; single precision p = 9: 3
+    // (1077 -> 1035 us), p = 11: 1 (1950 -> 1761 us)
+    static constexpr int EBW = NB_SW_EB ? NB_SW_EB
+                             : (sizeof(TV) == 4 && N == 10) ? 3 : (sizeof(TV) == 4 && N == 12) ? 1 : 2;
+    static constexpr int EB = (EBW * SLOT <= 110 * 1024) ? EBW : 1;
     static constexpr int SMEM = EB * SLOT;
 };
 

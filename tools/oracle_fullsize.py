@@ -19,6 +19,7 @@ Usage (one run per process; they are independent and can run side by side):
   python tools/oracle_fullsize.py --config 2 --policy mixed
   python tools/oracle_fullsize.py --config 2 --policy mixed_x64
   python tools/oracle_fullsize.py --gaps --config 2
+  python tools/oracle_fullsize.py --config 2 --policy sw_mixed      # Schwarz PCG (NEXT-4)
 """
 from __future__ import annotations
 
@@ -39,7 +40,8 @@ CONFIGS = {
     3: dict(nel=(64, 32, 32), p=11, deform=0.0, rhs=oracle.RHS_MANUFACTURED, rtol=1e-10, stride=12007,
             desc="BASELINE.json configs[3]: 64x32x32, p=11, manufactured RHS + 1e-3 noise seed 0, rtol 1e-10"),
 }
-POLICIES = {"fp64": (oracle.FP64, False), "mixed": (oracle.MIXED, False), "mixed_x64": (oracle.MIXED, True)}
+POLICIES = {"fp64": (oracle.FP64, False), "mixed": (oracle.MIXED, False), "mixed_x64": (oracle.MIXED, True),
+            "sw_fp64": (oracle.FP64, False), "sw_mixed": (oracle.MIXED, False)}   # sw_*: NEXT-4 Schwarz PCG
 HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(HERE, "tests", "golden")
 
@@ -55,7 +57,8 @@ def run(cfg: int, pol: str, scratch: str, max_iter: int) -> None:
     m = oracle.Mesh(*c["nel"], c["p"], c["deform"], 0)
     b = m.rhs(c["rhs"], 1e-3, 0)
     t1 = time.time()
-    x, hist, rep, sc = m.cg(b, policy, max_iter=max_iter, rtol=c["rtol"], x64=x64, scalars=True)
+    pc = oracle.PC_SCHWARZ if pol.startswith("sw_") else oracle.PC_JACOBI
+    x, hist, rep, sc = m.cg(b, policy, max_iter=max_iter, rtol=c["rtol"], x64=x64, scalars=True, precond=pc)
     t2 = time.time()
     cw = m.geom()["c"]
     xnorm = float(np.sqrt(np.sum(cw * x * x)))
@@ -65,7 +68,8 @@ def run(cfg: int, pol: str, scratch: str, max_iter: int) -> None:
     out = dict(
         source="tools/oracle_fullsize.py (oracle/ only; plain C, one thread, -O2 -ffp-contract=off)",
         config=c["desc"], nel=list(c["nel"]), p=c["p"], deform=c["deform"], rhs=c["rhs"], seed=0,
-        rtol=c["rtol"], policy=pol, x_fp64=x64, n_local=m.n_local,
+        rtol=c["rtol"], policy=pol, x_fp64=x64, precond="schwarz" if pc == oracle.PC_SCHWARZ else "jacobi",
+        n_local=m.n_local,
         iterations=rep.iterations, status=rep.status, rtr0=rep.rtr0, rel_res_final=rep.rel_res_final,
         rel_res_min=rep.rel_res_min, true_res=rep.true_res,
         history=[float(v) for v in hist],
@@ -87,6 +91,8 @@ def gaps(cfg: int, scratch: str) -> None:
     cw = m.geom()["c"]
     xs = {}
     for pol in POLICIES:
+        if pol.startswith("sw_"):
+            continue
         f = os.path.join(scratch, f"x_configs{cfg}_{pol}.npy")
         if os.path.exists(f):
             xs[pol] = np.load(f)
