@@ -1217,13 +1217,11 @@ k_sw_apply(const __grid_constant__ MegaArgs A)
     sw_weights_init(sw_w);
     const int tid = threadIdx.x;
     unsigned int tgt = 0;
-    int cur[EB][3];
-#pragma unroll
-    for (int s = 0; s < EB; s++) cur[s][0] = cur[s][1] = cur[s][2] = -1;
+
     const int64_t ng = ((int64_t)A.m.E + C::EPB - 1) / C::EPB;
     const int64_t g0 = split(ng, gridDim.x, blockIdx.x), g1 = split(ng, gridDim.x, blockIdx.x + 1);
     const int e0 = (int)min((int64_t)A.m.E, g0 * C::EPB), e1 = (int)min((int64_t)A.m.E, g1 * C::EPB);
-    for (int e = e0; e < e1; e += EB) sw_local<PREC, N>(A.m, A.sw, (const TV *)A.r, e, min(EB, e1 - e), smraw, sw_red, cur, sw_w);
+    sw_local_range<PREC, N>(A.m, A.sw, (const TV *)A.r, e0, e1, smraw, sw_red, sw_w);
     __syncthreads();
     if (tid == 0) { tgt += gridDim.x; grid_arrive_wait(A.bar, tgt); }
     __syncthreads();

@@ -39,7 +39,7 @@ template <typename TV, int N> struct SwCfg {
     // (1077 -> 1035 us), p = 11: 1 (1950 -> 1761 us)
     static constexpr int EBW = NB_SW_EB ? NB_SW_EB
                              : (sizeof(TV) == 4 && N == 10) ? 3 : (sizeof(TV) == 4 && N == 12) ? 1 : 2;
-    static constexpr int EB = (EBW * SLOT <= 110 * 1024) ? EBW : 1;
+    static constexpr int EB = (EBW * SLOT <= 110 * 1024) ? (EBW > 3 ? 3 : EBW) : 1;   // <= 3 named barriers
     static constexpr int SMEM = EB * SLOT;
 };
 
@@ -60,7 +60,8 @@ __device__ __forceinline__ void sw_weights_init(TG *wlut)
     __syncthreads();
 }
 
-// one 1-D pass over the P3^3 boxes of the ne slots: axis 0 (x), 1 (y), 2 (z), one line per thread:
+// one 1-D pass over the P3^3 box of one slot (its tps threads, lt = thread in the slot): axis 0
+// (x), 1 (y), 2 (z), one line per thread:
 // o[i] = sum_l M[l*P3 + i] in_l with M = S (S^T applied) or M = S^T (S applied), both stored
 // row-major in the slot's shared memory so a row of M is contiguous: single precision pairs the
 // outputs in packed FMAs (FFMA2) fed by 8-byte shared loads.  l outermost (unrolled by 2): one row
@@ -70,19 +71,17 @@ __device__ __forceinline__ void sw_weights_init(TG *wlut)
 // 1-D tables change).  Byte offsets within a slot: IN, OUT (OUT < 0: the global zext of the
 // slot's element), M.
 template <typename TV, int N, int AXIS, bool SCALE>
-__device__ __forceinline__ void sw_pass(unsigned char *smraw, int ne, int in_off, int out_off, int m_off,
-                                        TV *__restrict__ zext, int e0)
+__device__ __forceinline__ void sw_pass(unsigned char *slot, int lt, int tps, int in_off, int out_off, int m_off,
+                                        TV *__restrict__ zext, int e)
 {
     using C = SwCfg<TV, N>;
     constexpr int P3 = C::P3, P2 = C::P2;
     constexpr bool PAIR = sizeof(TV) == 4 && P3 % 2 == 0 && NB_FFMA2;
-    for (int L = threadIdx.x; L < ne * P2; L += blockDim.x) {
-        const int sl = L / P2, line = L - sl * P2;
-        unsigned char *slot = smraw + sl * C::SLOT;
-        const TV *in = reinterpret_cast<const TV *>(slot + in_off);
-        const TV *M = reinterpret_cast<const TV *>(slot + m_off);
-        const TV *dl = reinterpret_cast<const TV *>(slot + C::OFF_D);
-        TV *out = out_off >= 0 ? reinterpret_cast<TV *>(slot + out_off) : zext + (size_t)(e0 + sl) * C::PV;
+    const TV *in = reinterpret_cast<const TV *>(slot + in_off);
+    const TV *M = reinterpret_cast<const TV *>(slot + m_off);
+    const TV *dl = reinterpret_cast<const TV *>(slot + C::OFF_D);
+    TV *out = out_off >= 0 ? reinterpret_cast<TV *>(slot + out_off) : zext + (size_t)e * C::PV;
+    for (int line = lt; line < P2; line += tps) {
         const int u = line % P3, w = line / P3;
         // base index and stride of the line along AXIS
         const int base = AXIS == 0 ? P3 * line : AXIS == 1 ? u + P2 * w : line;
@@ -140,65 +139,67 @@ __device__ __forceinline__ void sw_pass(unsigned char *smraw, int ne, int in_off
     }
 }
 
-// S1: the local solves of elements e0 .. e0 + ne - 1 (ne <= SwCfg::EB, one shared-memory slot
-// each; all threads of the block); writes S.zext and S.cpart of those elements.  cur[sl]: the
-// cases of the tables the slot holds (kept across steps when they match: block-uniform test).
+// barrier of the tps threads of slot sl (named barrier 1 + sl, immediate ids so that ptxas
+// reserves only barriers 0..3 -- a register id reserves all 16 and can cost residency)
+__device__ __forceinline__ void slot_sync(int sl, int tps)
+{
+    if (sl == 0) asm volatile("bar.sync 1, %0;" ::"r"(tps) : "memory");
+    else if (sl == 1) asm volatile("bar.sync 2, %0;" ::"r"(tps) : "memory");
+    else asm volatile("bar.sync 3, %0;" ::"r"(tps) : "memory");
+}
+
+// S1 for one element e on slot sl (the slot's tps = SwCfg::TPS threads, warp-aligned, lt = thread
+// in the slot; the slots of a block proceed independently, synchronised by named barriers):
+// writes S.zext[e] and S.cpart[e].  cur: the cases of the tables the slot holds (kept across
+// elements when they match).  red: the slot's 8 x (tps/32) partials.
 template <int PREC, int N>
 __device__ __forceinline__ void sw_local(const MeshDev &m, const SwArgs &S, const typename Pol<PREC>::TV *__restrict__ r,
-                                         int e0, int ne, unsigned char *smraw, typename Pol<PREC>::TG *red,
-                                         int (&cur)[SwCfg<typename Pol<PREC>::TV, N>::EB][3],
+                                         int e, int sl, int lt, int tps, unsigned char *slot,
+                                         typename Pol<PREC>::TG *red, int (&cur)[3],
                                          const typename Pol<PREC>::TG *__restrict__ wlut)
 {
     using TV = typename Pol<PREC>::TV;
     using TG = typename Pol<PREC>::TG;
     using C = SwCfg<TV, N>;
-    constexpr int P3 = C::P3, P2 = C::P2, N3 = N * N * N, EB = C::EB;
-    const int tid = threadIdx.x;
-    // the slots' 1-D tables: S_a at [a], S_a^T at [3 + a]
-#pragma unroll
-    for (int sl = 0; sl < EB; sl++) {
-        if (sl >= ne) break;
-        const ElemPos P = elem_pos<false>(m, e0 + sl);
+    constexpr int P3 = C::P3, P2 = C::P2, N3 = N * N * N;
+    const ElemPos P = elem_pos<false>(m, e);
+    // the element's 1-D tables: S_a at [a], S_a^T at [3 + a]; 1/(lx + ly + lz) per point
+    {
         const int pos[3] = {P.ex, P.ey, P.ez};
         const int cs0 = S.cs[0][P.ex], cs1 = S.cs[1][P.ey], cs2 = S.cs[2][P.ez];
-        if (cs0 != cur[sl][0] || cs1 != cur[sl][1] || cs2 != cur[sl][2]) {
-            TV *Sm = reinterpret_cast<TV *>(smraw + sl * C::SLOT + C::OFF_S);
-            double *lm = reinterpret_cast<double *>(smraw + sl * C::SLOT + C::OFF_L);
-            for (int q = tid; q < 3 * P2; q += blockDim.x) {
+        if (cs0 != cur[0] || cs1 != cur[1] || cs2 != cur[2]) {
+            TV *Sm = reinterpret_cast<TV *>(slot + C::OFF_S);
+            double *lm = reinterpret_cast<double *>(slot + C::OFF_L);
+            for (int q = lt; q < 3 * P2; q += tps) {
                 const int a = q / P2, k = q - a * P2;
                 const TV v = ((const TV *)S.S[a])[(size_t)S.cs[a][pos[a]] * P2 + k];
                 Sm[q] = v;
                 Sm[(3 + a) * P2 + (k % P3) * P3 + k / P3] = v;
             }
-            for (int q = tid; q < 3 * P3; q += blockDim.x) {
+            for (int q = lt; q < 3 * P3; q += tps) {
                 const int a = q / P3, k = q - a * P3;
                 lm[q] = S.lam[a][(size_t)S.cs[a][pos[a]] * P3 + k];
             }
-            __syncthreads();
-            TV *dl = reinterpret_cast<TV *>(smraw + sl * C::SLOT + C::OFF_D);
-            for (int q = tid; q < C::PV; q += blockDim.x) {   // in double, rounded once to TV
+            slot_sync(sl, tps);
+            TV *dl = reinterpret_cast<TV *>(slot + C::OFF_D);
+            for (int q = lt; q < C::PV; q += tps) {   // in double, rounded once to TV
                 const int ti = q % P3, tj = (q / P3) % P3, tk = q / P2;
                 dl[q] = (TV)(1.0 / (lm[ti] + lm[P3 + tj] + lm[2 * P3 + tk]));
             }
-            cur[sl][0] = cs0; cur[sl][1] = cs1; cur[sl][2] = cs2;
+            cur[0] = cs0; cur[1] = cs1; cur[2] = cs2;
         }
     }
-    // R_e r, its coarse restriction partials and W R_e r, one x-line (tj, tk) of an extended box
+    // R_e r, its coarse restriction partials and W R_e r, one x-line (tj, tk) of the extended box
     // per thread: the line is a row of the (y, z)-neighbour element's copy (N contiguous values)
-    // plus one value from each x-neighbour of that element.  Slot sl is served by the warps
-    // [sl TPS/32, (sl+1) TPS/32) so that every warp's partials belong to one element.
-    const int TPS = ((int)(blockDim.x >> 5) / EB) * 32;
-    const int sl = tid / TPS, lt = tid - sl * TPS;
+    // plus one value from each x-neighbour of that element
     TG cp[8];
 #pragma unroll
     for (int c = 0; c < 8; c++) cp[c] = TG(0);
     const bool coarse = S.nv[0] > 0 && S.nv[1] > 0 && S.nv[2] > 0;
-    if (sl < ne) {
-        const int e = e0 + sl;
-        const ElemPos P = elem_pos<false>(m, e);
+    {
         const uint8_t *cx = S.cnt[0] + (size_t)P.ex * P3, *cy = S.cnt[1] + (size_t)P.ey * P3, *cz = S.cnt[2] + (size_t)P.ez * P3;
-        TV *F = reinterpret_cast<TV *>(smraw + sl * C::SLOT);
-        for (int line = lt; line < P2; line += TPS) {
+        TV *F = reinterpret_cast<TV *>(slot);
+        for (int line = lt; line < P2; line += tps) {
             const int tj = line % P3, tk = line / P3;
             const int cyz = cy[tj] * cz[tk];
             TV v[P3];
@@ -239,40 +240,56 @@ __device__ __forceinline__ void sw_local(const MeshDev &m, const SwArgs &S, cons
             for (int t = 0; t < P3; t++) F[P3 * line + t] = v[t];
         }
     }
-    if (coarse) {   // per slot: block sum of the 8 partials over its warps (fixed tree)
-        const int lane = tid & 31, wid = tid >> 5, wps = TPS >> 5;
+    if (coarse) {   // the slot's sum of the 8 partials over its warps (fixed tree)
+        const int lane = lt & 31, wl = lt >> 5, wps = tps >> 5;
 #pragma unroll
         for (int c = 0; c < 8; c++)
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) cp[c] += __shfl_down_sync(0xffffffffu, cp[c], o);
-        if (lane == 0 && wid < EB * wps)
+        if (lane == 0)
 #pragma unroll
-            for (int c = 0; c < 8; c++) red[wid * 8 + c] = cp[c];
-        __syncthreads();
-        if (tid < ne * 8) {
-            const int s2 = tid >> 3, c = tid & 7;
+            for (int c = 0; c < 8; c++) red[wl * 8 + c] = cp[c];
+        slot_sync(sl, tps);
+        if (lt < 8) {
             TG sacc = TG(0);
-            for (int w = s2 * wps; w < (s2 + 1) * wps; w++) sacc += red[w * 8 + c];
-            ((TG *)S.cpart)[(size_t)(e0 + s2) * 8 + c] = sacc;
+            for (int w = 0; w < wps; w++) sacc += red[w * 8 + lt];
+            ((TG *)S.cpart)[(size_t)e * 8 + lt] = sacc;
         }
     } else {
-        __syncthreads();
+        slot_sync(sl, tps);
     }
     // K_e^-1 by fast diagonalisation: S_x^T, S_y^T, S_z^T + Lambda^-1, S_z, S_y, S_x
     constexpr int oF = 0, oT = C::PV * (int)sizeof(TV), oS = C::OFF_S, P2B = P2 * (int)sizeof(TV);
     TV *zx = (TV *)S.zext;
-    sw_pass<TV, N, 0, false>(smraw, ne, oF, oT, oS, zx, e0);
-    __syncthreads();
-    sw_pass<TV, N, 1, false>(smraw, ne, oT, oF, oS + P2B, zx, e0);
-    __syncthreads();
-    sw_pass<TV, N, 2, true>(smraw, ne, oF, oT, oS + 2 * P2B, zx, e0);
-    __syncthreads();
-    sw_pass<TV, N, 2, false>(smraw, ne, oT, oF, oS + 5 * P2B, zx, e0);
-    __syncthreads();
-    sw_pass<TV, N, 1, false>(smraw, ne, oF, oT, oS + 4 * P2B, zx, e0);
-    __syncthreads();
-    sw_pass<TV, N, 0, false>(smraw, ne, oT, -1, oS + 3 * P2B, zx, e0);
-    __syncthreads();   // smem reused by the next step
+    sw_pass<TV, N, 0, false>(slot, lt, tps, oF, oT, oS, zx, e);
+    slot_sync(sl, tps);
+    sw_pass<TV, N, 1, false>(slot, lt, tps, oT, oF, oS + P2B, zx, e);
+    slot_sync(sl, tps);
+    sw_pass<TV, N, 2, true>(slot, lt, tps, oF, oT, oS + 2 * P2B, zx, e);
+    slot_sync(sl, tps);
+    sw_pass<TV, N, 2, false>(slot, lt, tps, oT, oF, oS + 5 * P2B, zx, e);
+    slot_sync(sl, tps);
+    sw_pass<TV, N, 1, false>(slot, lt, tps, oF, oT, oS + 4 * P2B, zx, e);
+    slot_sync(sl, tps);
+    sw_pass<TV, N, 0, false>(slot, lt, tps, oT, -1, oS + 3 * P2B, zx, e);
+    slot_sync(sl, tps);   // the slot's smem is reused by its next element
+}
+
+// S1 over elements [e0, e1) of the block: slot sl takes e0 + sl, e0 + sl + EB, ... (its threads
+// only; threads beyond the slots idle until the caller's block barrier)
+template <int PREC, int N>
+__device__ __forceinline__ void sw_local_range(const MeshDev &m, const SwArgs &S, const typename Pol<PREC>::TV *__restrict__ r,
+                                               int e0, int e1, unsigned char *smraw, typename Pol<PREC>::TG *red,
+                                               const typename Pol<PREC>::TG *__restrict__ wlut)
+{
+    using C = SwCfg<typename Pol<PREC>::TV, N>;
+    constexpr int EB = C::EB;
+    const int tps = ((int)(blockDim.x >> 5) / EB) * 32;
+    const int sl = (int)threadIdx.x / tps, lt = (int)threadIdx.x - sl * tps;
+    if (sl >= EB) return;
+    int cur[3] = {-1, -1, -1};
+    for (int e = e0 + sl; e < e1; e += EB)
+        sw_local<PREC, N>(m, S, r, e, sl, lt, tps, smraw + sl * C::SLOT, red + sl * 8 * (tps >> 5), cur, wlut);
 }
 
 // coarse pass `pass` (0: assemble b0; 1..6: the fast-diagonalisation passes), thread gt of gn
