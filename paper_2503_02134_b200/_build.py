@@ -38,6 +38,11 @@ def stale() -> bool:
 
 
 def _compile(src: str, verbose: bool) -> str:
+    # experiment variants: NB_UNITS_ONLY=a.cu,b.cu recompiles (with NB_OBJ_TAG / NB_NVCC_EXTRA) only those
+    # units and links the default build's objects for the rest
+    only = [u for u in os.environ.get("NB_UNITS_ONLY", "").split(",") if u]
+    if only and os.path.basename(src) not in only:
+        return os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
     obj = os.path.join(OBJ, os.path.basename(src)[:-3] + os.environ.get("NB_OBJ_TAG", "") + ".o")
     cmd = [NVCC, *FLAGS, "-c", "-o", obj, src]
     if os.environ.get("NB_PTXAS_V"):

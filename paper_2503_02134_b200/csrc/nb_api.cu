@@ -169,8 +169,8 @@ static int alloc_ws(nb_handle *h, int prec, int32_t max_iter)
         // each for the Dot2 expansions (nb_mega_launch.cuh: launch_cg_mega)
         const int mslots = (prec == NB_FP32_DOT2 ? 8 : 4) * ws.mega_G;
         NB_CU(cudaMalloc(&ws.part, sizeof(double) * mslots), "cudaMalloc part");
-        NB_CU(cudaMalloc(&ws.bar, sizeof(unsigned int) * 2), "cudaMalloc bar");
-        NB_CU(cudaMemset(ws.bar, 0, sizeof(unsigned int) * 2), "memset bar");
+        NB_CU(cudaMalloc(&ws.bar, sizeof(unsigned int) * nb::BAR_WORDS), "cudaMalloc bar");
+        NB_CU(cudaMemset(ws.bar, 0, sizeof(unsigned int) * nb::BAR_WORDS), "memset bar");
         NB_CU(cudaMalloc(&ws.scal, sizeof(nb::Scal)), "cudaMalloc scal");
         NB_CU(cudaMallocHost(&ws.scal_host, sizeof(nb::Scal)), "cudaMallocHost scal");
         NB_CU(cudaMemset(ws.scal, 0, sizeof(nb::Scal)), "memset scal");
@@ -539,7 +539,7 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
             nb::Workspace &ws = h->ws[prec];
             NB_POL(prec, nb::fill_mega_args, h, ws, bdev[r], order, o->max_iter, o->rtol, (int)o->precond,
                    (int)o->x_fp64, ws.tim, M.a[r]);
-            NB_CU(cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned int), st), "memset bar");
+            NB_CU(cudaMemsetAsync(ws.bar, 0, nb::BAR_WORDS * sizeof(unsigned int), st), "memset bar");
         }
         if (nh > 1) {
             // slabs sharing this launch: neighbours' w and control blocks are plain device pointers
@@ -593,7 +593,7 @@ static int cg_run(nb_handle *const *hs, int nh, const nb_cg_opts *o, const void 
         nb::sw_fill(h0, prec, A.sw);
         A.rp = nb::RankPart{o->ranks[0] > 0 ? o->ranks[0] : 1, o->ranks[1] > 0 ? o->ranks[1] : 1,
                             o->ranks[2] > 0 ? o->ranks[2] : 1};
-        NB_CU(cudaMemsetAsync(ws0.bar, 0, 2 * sizeof(unsigned int), st), "memset bar");
+        NB_CU(cudaMemsetAsync(ws0.bar, 0, nb::BAR_WORDS * sizeof(unsigned int), st), "memset bar");
         NB_CU(NB_POL(prec, nb::launch_cg_sw, h0, A, ws0.mega_G, false, st), "cg Schwarz megakernel");
         launches = 1;
     } else {
@@ -759,7 +759,7 @@ int nb_precond_apply(nb_handle *h, nb_policy prec, nb_precond pc, const void *r,
     A.bar = ws.bar;
     nb::sw_fill(h, prec, A.sw);
     cudaStream_t st = (cudaStream_t)stream;
-    NB_CU(cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned int), st), "memset bar");
+    NB_CU(cudaMemsetAsync(ws.bar, 0, nb::BAR_WORDS * sizeof(unsigned int), st), "memset bar");
     NB_CU(NB_POL(prec, nb::launch_cg_sw, h, A, ws.mega_G, true, st), "Schwarz apply");
     return NB_OK;
 }

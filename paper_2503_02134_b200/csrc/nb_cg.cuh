@@ -88,9 +88,40 @@ template <typename T, int N> struct AxCfg {
     static constexpr bool HALF = NB_HALF64 && sizeof(T) == 8 && N == 8;
     static constexpr int N2P = HALF ? 2 * N2 : (NB_PAD_ELEM && N == 10) ? 128 : N2;
     static constexpr int NARR = HALF ? 4 : 3;
-    static constexpr int EPB = (N2P >= 256) ? 1 : (256 / N2P);  // elements per group
+    // fp64, N = 10: one element per 128-thread block and NB_E1_D10 resident blocks (0: two elements per
+    // 224-thread block, NB_MINB_D blocks): independent blocks desynchronise, so one block's loads
+    // overlap the other's contractions
+#ifndef NB_E1_D10
+#define NB_E1_D10 2
+#endif
+    static constexpr bool E1D = NB_E1_D10 && sizeof(T) == 8 && N == 10 && !HALF;
+    static constexpr int EPB = E1D ? 1 : (N2P >= 256) ? 1 : (256 / N2P);  // elements per group
     static constexpr int NT = ((EPB * N2P + 31) / 32) * 32;     // threads per block
     static constexpr int SMEM = NARR * EPB * ESZ * (int)sizeof(T);
+    // Geometric factors of the solve's phase A staged through shared memory (NB_GSTAGE bit 0: fp64
+    // N = 10, bit 1: single precision N = 10, bit 2: single precision N = 12): one 1-D TMA bulk copy
+    // per element (its 6 N^3 factors are contiguous) issued by one thread right after the element's
+    // threads consumed the previous group's, completing on the slot's mbarrier: the fetch (half of
+    // phase A's bytes) overlaps the rest of this group and the start of the next without registers,
+    // load instructions or L1 tag lookups (a pencil's 40 / 80-byte stride costs 10 / 20 tag lookups
+    // per warp load at N = 10).  The stage keeps the global layout: pencil reads at a 10- or 12-word
+    // stride are bank-conflict-free.
+#ifndef NB_GSTAGE
+#define NB_GSTAGE 3
+#endif
+    static constexpr bool GSTAGE = !HALF && N2P == N2 &&
+                                   ((N == 10 && sizeof(T) == 8 && (NB_GSTAGE & 1)) || (N == 10 && sizeof(T) == 4 && (NB_GSTAGE & 2)) ||
+                                    (N == 12 && sizeof(T) == 4 && (NB_GSTAGE & 4)) || (N == 8 && sizeof(T) == 8 && (NB_GSTAGE & 8)));
+    static constexpr int GSB = GSTAGE ? 6 * N3 * (int)sizeof(T) : 0;   // staged bytes per element
+    static constexpr int SMEM_CG = SMEM + EPB * GSB;                   // k_cg_mega / k_cg_sw
+    // Phase B of the default solve (Jacobi): the inverse diagonal of each trip of NT pencils (one
+    // contiguous range; under the mixed policy the heaviest stream of the phase, 8 of its 24 bytes per
+    // DOF) by one TMA bulk copy per trip into the (idle) stage, double-buffered -- it no longer passes
+    // through L1 (tag lookups, and capacity the neighbour gathers need).  TJB = bytes of a diagonal entry.
+#ifndef NB_BSTAGE
+#define NB_BSTAGE 1
+#endif
+    template <int TJB> static constexpr bool BSTAGE = NB_BSTAGE && GSTAGE && 2 * NT * N * TJB <= EPB * GSB && EPB <= 2;
     // resident blocks per SM the register allocation must allow (launch bound); fp64 pencils
     // need twice the registers
 // Phase-B loads of w (own pencil, neighbour copies): w was written by other blocks in phase A,
@@ -126,7 +157,7 @@ template <typename T, int N> struct AxCfg {
 #ifndef NB_MINB_D
 #define NB_MINB_D 1
 #endif
-    static constexpr int MINB = (NB_MINB_D && sizeof(T) == 8 && N == 10) ? NB_MINB_D
+    static constexpr int MINB = E1D ? NB_E1_D10 : (NB_MINB_D && sizeof(T) == 8 && N == 10) ? NB_MINB_D
                               : (NB_MINB_N12 && N == 12 && sizeof(T) == 4) ? NB_MINB_N12
                               : NB_MINB_MODE == 0 ? 1
                               : NB_MINB_MODE == 3 ? ((sizeof(T) == 4) ? (NT <= 128 ? 4 : 2) : (N <= 8 && !HALF ? 1 : 2))
@@ -196,13 +227,27 @@ __device__ __forceinline__ void elem_sync()
     __syncthreads();
 }
 
-template <int PREC, int N, int MODE, bool SLAB = false>
+// mbarriers and wait parities of the element slots' staged geometric factors (AxCfg::GSTAGE)
+struct GStage {
+    unsigned long long bar[4];
+    unsigned par[4];
+};
+// element e's 6 N^3 factors into the slot's stage (one thread)
+template <typename TV, int N>
+__device__ __forceinline__ void gstage_issue(const TV *__restrict__ g, int e, TV *__restrict__ gst, unsigned long long *bar)
+{
+    constexpr int N3 = N * N * N;
+    tma_load_1d(gst, g + (size_t)e * 6 * N3, 6 * N3 * (unsigned)sizeof(TV), bar);
+}
+
+template <int PREC, int N, int MODE, bool SLAB = false, bool GS = false>
 __device__ NB_PHASE_ATTR Acc<PREC>
 ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typename Pol<PREC>::TV *__restrict__ in,
          typename Pol<PREC>::TV *__restrict__ pv, typename Pol<PREC>::TV *__restrict__ xv,
          const typename Pol<PREC>::TV *__restrict__ g, typename Pol<PREC>::TV *__restrict__ w, bool apply_mask,
          typename Pol<PREC>::TV beta, typename Pol<PREC>::TV alpha, int e, bool active, int a, int b,
-         typename Pol<PREC>::TV *__restrict__ S0, double *__restrict__ xd = nullptr, double alpha_d = 0.0)
+         typename Pol<PREC>::TV *__restrict__ S0, double *__restrict__ xd = nullptr, double alpha_d = 0.0,
+         typename Pol<PREC>::TV *__restrict__ gst = nullptr, int e_next = -1, GStage *gsh = nullptr, int el = 0)
 {
     using TV = typename Pol<PREC>::TV;
     using TS = typename Pol<PREC>::TS;
@@ -226,28 +271,28 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
             // x_fp64 variant (C-15): x += alpha p in double with the double alpha
             TV zz[N], po[N];
             double xx[N];
-            ld_pencil<TV, N, LD_CS>(in + gbase, zz);
-            ld_pencil<TV, N>(pv + gbase, po);
-            ld_pencil<double, N, LD_CS>(xd + gbase, xx);
+            ldg_pencil<TV, N, LD_CS>(in + gbase, zz);
+            ldg_pencil<TV, N>(pv + gbase, po);
+            ldg_pencil<double, N, LD_CS>(xd + gbase, xx);
 #pragma unroll
             for (int i = 0; i < N; i++) {
                 u[i] = fma(beta, po[i], zz[i]);                 // add2s1
                 xx[i] = fma(alpha_d, (double)po[i], xx[i]);     // add2s2(x, p_old, alpha_prev)
             }
-            st_pencil<TV, N>(pv + gbase, u);
-            st_pencil<double, N, LD_CS>(xd + gbase, xx);
+            stg_pencil<TV, N>(pv + gbase, u);
+            stg_pencil<double, N, LD_CS>(xd + gbase, xx);
         } else {
             TV zz[N], po[N], xx[N];
-            ld_pencil<TV, N, LD_CS>(in + gbase, zz);
-            ld_pencil<TV, N>(pv + gbase, po);
-            ld_pencil<TV, N, LD_CS>(xv + gbase, xx);
+            ldg_pencil<TV, N, LD_CS>(in + gbase, zz);
+            ldg_pencil<TV, N>(pv + gbase, po);
+            ldg_pencil<TV, N, LD_CS>(xv + gbase, xx);
 #pragma unroll
             for (int i = 0; i < N; i++) {
                 u[i] = fma(beta, po[i], zz[i]);      // add2s1
                 xx[i] = fma(alpha, po[i], xx[i]);    // add2s2(x, p_old, alpha_prev)
             }
-            st_pencil<TV, N>(pv + gbase, u);
-            st_pencil<TV, N, LD_CS>(xv + gbase, xx);
+            stg_pencil<TV, N>(pv + gbase, u);
+            stg_pencil<TV, N, LD_CS>(xv + gbase, xx);
         }
         st_pencil<TV, N>(S0 + rp, u);
     }
@@ -279,15 +324,25 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
             contract<TV, N>(D, v, ur);
         }
         const TV *ge = g + (size_t)e * 6 * C::N3 + (size_t)N * q;
+        if constexpr (GS) mbar_wait(&gsh->bar[el], gsh->par[el]);
 #pragma unroll
         for (int c = 0; c < N / V; c++) {
             TV g1[V], g2[V], g3[V], g4[V], g5[V], g6[V], us[V], ut[V], ws[V], wt[V];
+            if constexpr (GS) {
+                ld_chunk<TV, V>(gst + 0 * C::N3 + N * q + c * V, g1);
+                ld_chunk<TV, V>(gst + 1 * C::N3 + N * q + c * V, g2);
+                ld_chunk<TV, V>(gst + 2 * C::N3 + N * q + c * V, g3);
+                ld_chunk<TV, V>(gst + 3 * C::N3 + N * q + c * V, g4);
+                ld_chunk<TV, V>(gst + 4 * C::N3 + N * q + c * V, g5);
+                ld_chunk<TV, V>(gst + 5 * C::N3 + N * q + c * V, g6);
+            } else {
             ld_chunk_h<TV, V, LD_CS>(ge + 0 * C::N3 + c * V, g1);
             ld_chunk_h<TV, V, LD_CS>(ge + 1 * C::N3 + c * V, g2);
             ld_chunk_h<TV, V, LD_CS>(ge + 2 * C::N3 + c * V, g3);
             ld_chunk_h<TV, V, LD_CS>(ge + 3 * C::N3 + c * V, g4);
             ld_chunk_h<TV, V, LD_CS>(ge + 4 * C::N3 + c * V, g5);
             ld_chunk_h<TV, V, LD_CS>(ge + 5 * C::N3 + c * V, g6);
+            }
             ld_chunk<TV, V>(A1 + rp + c * V, us);
             ld_chunk<TV, V>(A2 + rp + c * V, ut);
 #pragma unroll
@@ -303,6 +358,12 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
         contract_t<TV, N>(D, wr, wrt);
     }
     elem_sync<C::N2P, C::EPB>();
+    if constexpr (GS) {   // the element's threads are done with the stage: flip its parity, fetch the next group's
+        if (active && q == 0) {
+            gsh->par[el] ^= 1u;
+            if (e_next >= 0) gstage_issue<TV, N>(g, e_next, gst, &gsh->bar[el]);
+        }
+    }
     // ---- 4. s- and t-parts of local_grad3_t, in place on the owner's pencils
     if (active) {
         TV v[N], o[N];
@@ -349,7 +410,7 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
 #pragma unroll
             for (int i = 0; i < N; i++) acc.add((TS)out[i], (TS)pp[i]);
         }
-        st_pencil<TV, N>(w + gbase, out);
+        stg_pencil<TV, N>(w + gbase, out);
     }
     } else {
     // ---- 3. (register-lean) ur to the owner's S0 slots; the geometric factors streamed in
@@ -366,15 +427,25 @@ ax_group(const MeshDev &m, const DMat<typename Pol<PREC>::TV, N> &D, const typen
 // two chunks of geometric factors in flight for p >= 7 (fp64 phase A -3% / -14% / -7% at p = 7 / 9 / 11;
 // +2% at p = 5, so not below)
 constexpr int LEAN_U = N >= 8 ? NB_LEAN_UNROLL : 1;
+        if constexpr (GS) mbar_wait(&gsh->bar[el], gsh->par[el]);
 #pragma unroll LEAN_U
         for (int c = 0; c < N / V; c++) {
             TV g1[V], g2[V], g3[V], g4[V], g5[V], g6[V], ur[V], us[V], ut[V], wr[V], ws[V], wt[V];
+            if constexpr (GS) {
+                ld_chunk<TV, V>(gst + 0 * C::N3 + N * q + c * V, g1);
+                ld_chunk<TV, V>(gst + 1 * C::N3 + N * q + c * V, g2);
+                ld_chunk<TV, V>(gst + 2 * C::N3 + N * q + c * V, g3);
+                ld_chunk<TV, V>(gst + 3 * C::N3 + N * q + c * V, g4);
+                ld_chunk<TV, V>(gst + 4 * C::N3 + N * q + c * V, g5);
+                ld_chunk<TV, V>(gst + 5 * C::N3 + N * q + c * V, g6);
+            } else {
             ld_chunk<TV, V>(ge + 0 * C::N3 + c * V, g1);
             ld_chunk<TV, V>(ge + 1 * C::N3 + c * V, g2);
             ld_chunk<TV, V>(ge + 2 * C::N3 + c * V, g3);
             ld_chunk<TV, V>(ge + 3 * C::N3 + c * V, g4);
             ld_chunk<TV, V>(ge + 4 * C::N3 + c * V, g5);
             ld_chunk<TV, V>(ge + 5 * C::N3 + c * V, g6);
+            }
             ld_chunk<TV, V>(S0 + rp + c * V, ur);
             ld_chunk<TV, V>(A1 + rp + c * V, us);
             ld_chunk<TV, V>(A2 + rp + c * V, ut);
@@ -397,6 +468,12 @@ constexpr int LEAN_U = N >= 8 ? NB_LEAN_UNROLL : 1;
         }
     }
     elem_sync<C::N2P, C::EPB>();
+    if constexpr (GS) {   // the element's threads are done with the stage: flip its parity, fetch the next group's
+        if (active && q == 0) {
+            gsh->par[el] ^= 1u;
+            if (e_next >= 0) gstage_issue<TV, N>(g, e_next, gst, &gsh->bar[el]);
+        }
+    }
     // ---- 4. s- and t-parts of local_grad3_t, in place on the owner's pencils
     if (active) {
         TV v[N], o[N];
@@ -432,13 +509,13 @@ constexpr int LEAN_U = N >= 8 ? NB_LEAN_UNROLL : 1;
             if (MODE == 2) {   // unshared nodes only (c = 1); the CSR phase adds the shared ones
                 const bool sjk = axis_mult(a, N, P.ey, m.nely) * axis_mult(b, N, P.ez, m.nelz) > 1;
                 TV pp[N];
-                ld_pencil<TV, N>(pv + gbase, pp);   // written by this thread in step 1
+                ldg_pencil<TV, N>(pv + gbase, pp);   // written by this thread in step 1
 #pragma unroll
                 for (int i = 0; i < N; i++)
                     if (!sjk && axis_mult(i, N, P.ex, m.nelx) == 1) acc.add((TS)out[i], (TS)pp[i]);
             }
         }
-        st_pencil<TV, N>(w + gbase, out);
+        stg_pencil<TV, N>(w + gbase, out);
     }
     }
     return acc;
@@ -731,7 +808,8 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
                                            const void *__restrict__ dinv,
                                            typename Pol<PREC>::TV alpha, int64_t pid, Acc<PREC> &rtr, Acc<PREC> &rho,
                                            int pc = NB_PC_JACOBI, const typename Pol<PREC>::TV *wlo = nullptr,
-                                           const typename Pol<PREC>::TV *whi = nullptr)
+                                           const typename Pol<PREC>::TV *whi = nullptr,
+                                           const typename Pol<PREC>::TJ *dsm = nullptr)
 {
     using TV = typename Pol<PREC>::TV;
     using TJ = typename Pol<PREC>::TJ;
@@ -746,7 +824,10 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
     const ElemPos P = elem_pos<SLAB>(m, e);
     ld_pencil<TV, N, NB_WLD>(w + base, ww);
     ld_pencil<TV, N>(r + base, rr);
-    if (!SW) ld_dinv<TJ, N>(dinv, base, pc, dd);
+    if (!SW) {
+        if (dsm) ld_pencil<TJ, N>(dsm, dd);   // the trip's diagonal staged in shared memory (AxCfg::BSTAGE)
+        else ld_dinv<TJ, N>(dinv, base, pc, dd);
+    }
     if (GATHER) {
         constexpr int N3 = N * N * N;
         const TV ol = P.ex > 0 ? ldv<NB_WLD>(w + base - N3 + (N - 1)) : TV(0);
@@ -817,6 +898,24 @@ __device__ __forceinline__ void init_pencil(const MeshDev &m, const typename Pol
 
 // contiguous even split of [0, n) over `parts`
 __device__ __forceinline__ int64_t split(int64_t n, int parts, int i) { return n * i / parts; }
+
+// Element groups [lo, hi) of (virtual) block i of G.  S = 0: the contiguous even split over the
+// blocks.  S > 0 (a full persistent grid of G = occ * S blocks, block i = the k-th resident block of
+// the s-th SM, i = s occ + k): the groups are split evenly over the S SMs first and each SM's
+// contiguous share over its occ blocks, so the busiest SM holds ceil(ng / S) groups instead of
+// occ * ceil(ng / G) (configs[1]: 1024 groups, 148 SMs, occ 2: 7 instead of 8).
+__device__ __forceinline__ void grp_range(int64_t ng, int G, int S, int i, int64_t &lo, int64_t &hi)
+{
+    if (S > 0 && G > S && G % S == 0) {
+        const int occ = G / S, s = i / occ, k = i % occ;
+        const int64_t a = split(ng, S, s), b = split(ng, S, s + 1);
+        lo = a + split(b - a, occ, k);
+        hi = a + split(b - a, occ, k + 1);
+    } else {
+        lo = split(ng, G, i);
+        hi = split(ng, G, i + 1);
+    }
+}
 
 // ---------------------------------------------------------------------------
 // L2 prefetch distances (l2_prefetch, nb_common.cuh): phase A prefetches the operands of the

@@ -256,6 +256,96 @@ __device__ __forceinline__ void st_pencil(T *__restrict__ dst, const T (&v)[N])
 }
 
 // ---------------------------------------------------------------------------
+// Global pencil accesses at N = 10 (p = 9): a pencil is 40 / 80 bytes at a 40 / 80-byte stride, so
+// it is 8 / 16-byte aligned only and ld_pencil needs five 8 / 16-byte accesses, each a warp
+// instruction that touches ten / twenty 128-byte lines (L1 tag lookups, the measured limiter of
+// both phases at p = 9).  Pencils of even index are 16 / 32-byte aligned, odd ones become so 8 / 16
+// bytes in: every lane issues one narrow and two wide (16 / 32-byte) accesses at lane-dependent
+// offsets -- three instructions instead of five -- and picks its values by the pencil's parity.
+// (32-byte accesses: ld/st.global.v4.f64, sm_100.)  Used by phase A only: measured at 32^3 p9
+// (mixed / fp32 / fp64) phase A -2 / -4 / -4 %, but phase B +20 / +9 / +10 % with the same accesses
+// there, so phase B keeps ld_pencil.  NB_WIDE10=0: the plain form everywhere.
+// ---------------------------------------------------------------------------
+#ifndef NB_WIDE10
+#define NB_WIDE10 1
+#endif
+struct alignas(32) double4w { double x, y, z, w; };
+template <int H> __device__ __forceinline__ double4w ld256(const double *p)
+{
+    double4w r;
+    if (H == LD_CS)
+        asm volatile("ld.global.cs.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p) : "memory");
+    else if (H == LD_NC)
+        asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    else if (H == LD_CG)
+        asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p) : "memory");
+    else
+        asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p) : "memory");
+    return r;
+}
+template <int H> __device__ __forceinline__ void st256(double *p, const double4w &v)
+{
+    if (H == LD_CS)
+        asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+    else
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+}
+template <typename T, int N, int H = LD_DEF>
+__device__ __forceinline__ void ldg_pencil(const T *__restrict__ src, T (&v)[N])
+{
+    if constexpr (NB_WIDE10 && N == 10) {
+        // odd pencil: narrow piece first (values 0-1), then two wide ones; even: two wide, then narrow (8-9)
+        const bool odd = ((reinterpret_cast<unsigned long long>(src) / (2 * sizeof(T))) & 1ull) != 0;
+        const T *pa = src + (odd ? 0 : 8), *pb = src + (odd ? 2 : 0), *pc = src + (odd ? 6 : 4);
+        T a[2], b[4], c[4];
+        if constexpr (sizeof(T) == 4) {
+            const float2 ta = ldv<H>(reinterpret_cast<const float2 *>(pa));
+            const float4 tb = ldv<H>(reinterpret_cast<const float4 *>(pb));
+            const float4 tc = ldv<H>(reinterpret_cast<const float4 *>(pc));
+            a[0] = ta.x; a[1] = ta.y;
+            b[0] = tb.x; b[1] = tb.y; b[2] = tb.z; b[3] = tb.w;
+            c[0] = tc.x; c[1] = tc.y; c[2] = tc.z; c[3] = tc.w;
+        } else {
+            const double2 ta = ldv<H>(reinterpret_cast<const double2 *>(pa));
+            const double4w tb = ld256<H>(pb);
+            const double4w tc = ld256<H>(pc);
+            a[0] = ta.x; a[1] = ta.y;
+            b[0] = tb.x; b[1] = tb.y; b[2] = tb.z; b[3] = tb.w;
+            c[0] = tc.x; c[1] = tc.y; c[2] = tc.z; c[3] = tc.w;
+        }
+        v[0] = odd ? a[0] : b[0]; v[1] = odd ? a[1] : b[1];
+        v[2] = odd ? b[0] : b[2]; v[3] = odd ? b[1] : b[3];
+        v[4] = odd ? b[2] : c[0]; v[5] = odd ? b[3] : c[1];
+        v[6] = odd ? c[0] : c[2]; v[7] = odd ? c[1] : c[3];
+        v[8] = odd ? c[2] : a[0]; v[9] = odd ? c[3] : a[1];
+    } else {
+        ld_pencil<T, N, H>(src, v);
+    }
+}
+template <typename T, int N, int H = LD_DEF>
+__device__ __forceinline__ void stg_pencil(T *__restrict__ dst, const T (&v)[N])
+{
+    if constexpr (NB_WIDE10 && N == 10) {
+        const bool odd = ((reinterpret_cast<unsigned long long>(dst) / (2 * sizeof(T))) & 1ull) != 0;
+        T *pa = dst + (odd ? 0 : 8), *pb = dst + (odd ? 2 : 0), *pc = dst + (odd ? 6 : 4);
+        const T a0 = odd ? v[0] : v[8], a1 = odd ? v[1] : v[9];
+        const T b0 = odd ? v[2] : v[0], b1 = odd ? v[3] : v[1], b2 = odd ? v[4] : v[2], b3 = odd ? v[5] : v[3];
+        const T c0 = odd ? v[6] : v[4], c1 = odd ? v[7] : v[5], c2 = odd ? v[8] : v[6], c3 = odd ? v[9] : v[7];
+        if constexpr (sizeof(T) == 4) {
+            stv<H>(reinterpret_cast<float2 *>(pa), make_float2(a0, a1));
+            stv<H>(reinterpret_cast<float4 *>(pb), make_float4(b0, b1, b2, b3));
+            stv<H>(reinterpret_cast<float4 *>(pc), make_float4(c0, c1, c2, c3));
+        } else {
+            stv<H>(reinterpret_cast<double2 *>(pa), make_double2(a0, a1));
+            st256<H>(pb, double4w{b0, b1, b2, b3});
+            st256<H>(pc, double4w{c0, c1, c2, c3});
+        }
+    } else {
+        st_pencil<T, N, H>(dst, v);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // asynchronous global -> shared copies (cp.async, LDGSTS): stage a pencil in shared memory
 // without holding it in registers.  .cg (L2 only) for 16-byte chunks, .ca otherwise.
 // ---------------------------------------------------------------------------
@@ -279,6 +369,33 @@ __device__ __forceinline__ void cp_pencil_async(T *sdst, const T *gsrc)
 }
 
 // ---------------------------------------------------------------------------
+// 1-D TMA bulk copy global -> shared completing on an mbarrier (cp.async.bulk, sm_90+): one
+// instruction of one thread moves a contiguous range (16-byte aligned, a multiple of 16 bytes)
+// without registers, LSU instructions or L1 tag lookups.
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *sdst, const void *gsrc, unsigned bytes, unsigned long long *bar)
+{
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar), d = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d), "l"(gsrc),
+                 "r"(bytes), "r"(b)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity)
+{
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned ok;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok)
+                     : "r"(b), "r"(parity)
+                     : "memory");
+    } while (!ok);
+}
+
 // bulk L2 prefetch (cp.async.bulk.prefetch.L2, sm_90+): the TMA unit pulls a contiguous byte
 // range from HBM into L2 with no registers, shared memory or completion tracking.  The later
 // register loads of the range then wait an L2 round trip (~250 cycles) instead of a DRAM one

@@ -83,6 +83,9 @@ struct SwArgs {
 };
 
 // Arguments of the persistent CG megakernel (nb_cg.cuh), one slab's (or the whole box's) solve
+constexpr int SMID_MAX = 1024;            // SM ids tracked by the per-SM split
+constexpr int BAR_WORDS = 2 + SMID_MAX;   // Workspace::bar
+
 struct MegaArgs {
     MeshDev m;
     const void *b;
@@ -102,7 +105,11 @@ struct MegaArgs {
     int32_t x64;            // NB_MIXED: x is double (x_fp64 option)
     int32_t phase_only;     // measurement only (NB_PHASE_ONLY=A|B at setup): 1 = phase A alone,
                             // 2 = phase B alone, max_iter iterations, no stop test (ncu traffic per phase)
-    unsigned int *bar;      // [2] grid barrier: arrival count, generation
+    unsigned int *bar;      // [BAR_WORDS] grid barrier: arrival count, generation; then the resident-block
+                            // count of every SM id (sm_split), all zeroed before the launch
+    int32_t sm_split;       // S > 0 (a full grid of occ * S blocks): the element groups are split per SM first
+                            // and each SM's contiguous share over the blocks resident on it (the blocks find
+                            // their SM and slot at the start of the solve; grp_range()); 0: per block
     Scal *scal;             // result scalars (written by block 0)
     // multi-rank (z-slab) solves only: the neighbour slabs' w, rebased so that the element
     // index of this slab addresses them (wlo + e*N3 for e < 0, whi + e*N3 for e >= E); else null

@@ -21,9 +21,13 @@ static void set_carveout(const void *fn, int occ, int smem)   // called once per
         mode = (s && s[0] == '0') ? 0 : 1;
     }
     if (!mode) return;
-    const int need = occ * (smem + 1024) + 1024;                   // + per-block reservation
+    cudaFuncAttributes fa{};
+    const int stat = cudaFuncGetAttributes(&fa, fn) == cudaSuccess ? (int)fa.sharedSizeBytes : 0;
+    const int need = occ * (smem + stat + 1024) + 1024;            // + static + per-block reservation
     int pct = (int)((100LL * need + 228 * 1024 - 1) / (228 * 1024));
-    if (pct > 100) pct = 100;
+    // close to the maximum: ask for all of it (a preference that maps to a smaller supported size than
+    // the resident blocks need lowers the cooperative-launch limit: "too many blocks")
+    if (pct > 80) pct = 100;
     cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
@@ -31,7 +35,7 @@ template <int PREC, int N, int FUSED, int VAR>
 static int mega_grid_t(const nb_handle *h)
 {
     using C = AxCfg<typename Pol<PREC>::TV, N>;
-    constexpr int SMEM_MEGA = C::SMEM;
+    constexpr int SMEM_MEGA = C::SMEM_CG;
     const void *fn = (const void *)k_cg_mega<PREC, N, FUSED, VAR>;
     static DevCache cache;   // the attributes and the residency are per device
     int &occ = cache.here();
@@ -80,10 +84,12 @@ static cudaError_t mega_launch_t(const nb_handle *h, const MegaArgs &args, cudaS
 {
     using TV = typename Pol<PREC>::TV;
     using C = AxCfg<TV, N>;
-    constexpr int SMEM_MEGA = C::SMEM;
+    constexpr int SMEM_MEGA = C::SMEM_CG;
     DMat<TV, N> D = make_dmat<TV, N>(h->D);
-    void *params[2] = {(void *)&args, (void *)&D};
+    MegaArgs a2 = args;
+    void *params[2] = {(void *)&a2, (void *)&D};
     int grid = mega_grid_t<PREC, N, FUSED, VAR>(h);
+    const int full = grid;
     // Balanced grid: the fewest blocks that keep the same number of element groups on the
     // busiest block (configs[1]: 1024 groups on 256 blocks x 4 instead of 296 blocks x 3-4), so
     // no wave is partly idle and the barriers have fewer arrivals -- unless that raises the
@@ -100,6 +106,25 @@ static cudaError_t mega_launch_t(const nb_handle *h, const MegaArgs &args, cudaS
         const long long g = waves > 0 ? (ng + waves - 1) / waves : grid;
         if (g >= 1 && g < grid && balanced_sm_max(ng, g, h->sm_count) <= balanced_sm_max(ng, grid, h->sm_count))
             grid = (int)g;
+    }
+    // Per-SM split (grp_range, nb_cg.cuh; the blocks find their SM at the start of the solve): the full
+    // grid with every SM's share of the groups split over its resident blocks, where that lowers the
+    // busiest SM's group count against occ blocks of the (balanced) grid's busiest kind (configs[1] in
+    // single precision: 7 instead of 2 x 4 groups).  NB_SM_SPLIT=0: off.
+    static int smsplit = -1;
+    if (smsplit < 0) {
+        const char *s = std::getenv("NB_SM_SPLIT");
+        smsplit = (s && s[0] == '0') ? 0 : 1;
+    }
+    a2.sm_split = 0;
+    if (smsplit && h->sm_count > 0 && h->sm_count < SMID_MAX && full > h->sm_count && full % h->sm_count == 0) {
+        const long long ng = ((long long)h->E + C::EPB - 1) / C::EPB;
+        const long long per_sm = (ng + h->sm_count - 1) / h->sm_count;
+        const long long occ = full / h->sm_count;
+        if (ng >= full && per_sm < occ * ((ng + grid - 1) / grid)) {
+            grid = full;
+            a2.sm_split = h->sm_count;
+        }
     }
     return cudaLaunchCooperativeKernel((const void *)k_cg_mega<PREC, N, FUSED, VAR>, dim3(grid), dim3(C::NT), params,
                                        (size_t)SMEM_MEGA, st);
@@ -134,6 +159,7 @@ void fill_mega_args(const nb_handle *h, Workspace &ws, const void *b, int order,
     const size_t W = (size_t)Acc<PREC>::W;
     A.partA = ws.part; A.partS = ws.part + W * ws.mega_G; A.partB = ws.part + 2 * W * ws.mega_G;
     A.bar = ws.bar;
+    A.sm_split = 0;
     A.scal = ws.scal;
     A.wlo = ws.peer.wlo;
     A.whi = ws.peer.whi;
@@ -148,7 +174,7 @@ cudaError_t launch_cg_mega(const nb_handle *h, Workspace &ws, const void *b, int
     A.wlo = A.whi = nullptr;
     A.rp = rp;
     const bool fused = order == NB_GS_CONSISTENT && !h->cg_csr;
-    cudaError_t e = cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned int), st);   // barrier epoch 0
+    cudaError_t e = cudaMemsetAsync(ws.bar, 0, BAR_WORDS * sizeof(unsigned int), st);   // barrier epoch 0
     if (e != cudaSuccess) return e;
     const bool var = precond != NB_PC_JACOBI || A.x64;
     return var ? launch_cg_mega_var<PREC, 1>(h, A, fused, st) : launch_cg_mega_var<PREC, 0>(h, A, fused, st);
@@ -161,7 +187,7 @@ static cudaError_t sw_launch_t(const nb_handle *h, const MegaArgs &A, int gmax, 
 {
     using TV = typename Pol<PREC>::TV;
     using C = AxCfg<TV, N>;
-    constexpr int SMEM = C::SMEM > SwCfg<TV, N>::SMEM ? C::SMEM : SwCfg<TV, N>::SMEM;
+    constexpr int SMEM = C::SMEM_CG > SwCfg<TV, N>::SMEM ? C::SMEM_CG : SwCfg<TV, N>::SMEM;
     const void *fn = APPLY ? (const void *)k_sw_apply<PREC, N> : (const void *)k_cg_sw<PREC, N, FUSED>;
     static DevCache cache;
     int &occ = cache.here();
