@@ -114,14 +114,15 @@ template <typename T, int N> struct AxCfg {
                                     (N == 12 && sizeof(T) == 4 && (NB_GSTAGE & 4)) || (N == 8 && sizeof(T) == 8 && (NB_GSTAGE & 8)));
     static constexpr int GSB = GSTAGE ? 6 * N3 * (int)sizeof(T) : 0;   // staged bytes per element
     static constexpr int SMEM_CG = SMEM + EPB * GSB;                   // k_cg_mega / k_cg_sw
-    // Phase B of the default solve (Jacobi): the inverse diagonal of each trip of NT pencils (one
-    // contiguous range; under the mixed policy the heaviest stream of the phase, 8 of its 24 bytes per
-    // DOF) by one TMA bulk copy per trip into the (idle) stage, double-buffered -- it no longer passes
-    // through L1 (tag lookups, and capacity the neighbour gathers need).  TJB = bytes of a diagonal entry.
-#ifndef NB_BSTAGE
-#define NB_BSTAGE 1
+    // the standalone operator k_ax (no phase B that wants the L1): also single precision N = 12 (bit 0)
+    // and N = 8 (bit 1; 32^3 p7 mixed 127 -> 100 us, 50^3 p7 504 -> 330 us = 0.95 of the copy peak)
+#ifndef NB_GSTAGE_AX
+#define NB_GSTAGE_AX 3
 #endif
-    template <int TJB> static constexpr bool BSTAGE = NB_BSTAGE && GSTAGE && 2 * NT * N * TJB <= EPB * GSB && EPB <= 2;
+    static constexpr bool GSTAGE_AX = !HALF && N2P == N2 && (((NB_GSTAGE_AX & 1) && (N == 10 || (N == 12 && sizeof(T) == 4))) ||
+                                                             ((NB_GSTAGE_AX & 2) && N == 8 && sizeof(T) == 4));
+    static constexpr int GSB_AX = GSTAGE_AX ? 6 * N3 * (int)sizeof(T) : 0;
+    static constexpr int SMEM_AX = SMEM + EPB * GSB_AX;                // k_ax
     // resident blocks per SM the register allocation must allow (launch bound); fp64 pencils
     // need twice the registers
 // Phase-B loads of w (own pencil, neighbour copies): w was written by other blocks in phase A,
@@ -808,8 +809,7 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
                                            const void *__restrict__ dinv,
                                            typename Pol<PREC>::TV alpha, int64_t pid, Acc<PREC> &rtr, Acc<PREC> &rho,
                                            int pc = NB_PC_JACOBI, const typename Pol<PREC>::TV *wlo = nullptr,
-                                           const typename Pol<PREC>::TV *whi = nullptr,
-                                           const typename Pol<PREC>::TJ *dsm = nullptr)
+                                           const typename Pol<PREC>::TV *whi = nullptr)
 {
     using TV = typename Pol<PREC>::TV;
     using TJ = typename Pol<PREC>::TJ;
@@ -824,10 +824,7 @@ __device__ __forceinline__ void upd_pencil(const MeshDev &m, const typename Pol<
     const ElemPos P = elem_pos<SLAB>(m, e);
     ld_pencil<TV, N, NB_WLD>(w + base, ww);
     ld_pencil<TV, N>(r + base, rr);
-    if (!SW) {
-        if (dsm) ld_pencil<TJ, N>(dsm, dd);   // the trip's diagonal staged in shared memory (AxCfg::BSTAGE)
-        else ld_dinv<TJ, N>(dinv, base, pc, dd);
-    }
+    if (!SW) ld_dinv<TJ, N>(dinv, base, pc, dd);
     if (GATHER) {
         constexpr int N3 = N * N * N;
         const TV ol = P.ex > 0 ? ldv<NB_WLD>(w + base - N3 + (N - 1)) : TV(0);
@@ -1359,21 +1356,37 @@ k_ax(const MeshDev m, const __grid_constant__ DMat<typename Pol<PREC>::TV, N> D,
     const int64_t ngroups = ((int64_t)m.E + C::EPB - 1) / C::EPB;
     const int64_t g0 = split(ngroups, gridDim.x, blockIdx.x), g1 = split(ngroups, gridDim.x, blockIdx.x + 1);
     // u and g of the next group into L2 (measured at 32^3: mixed p9 323 -> 270 us, p11 587 -> 406 us,
-    // fp64 p9 721 -> 634 us; fp64 p7 slower, 226 -> 240 us, so not there)
+    // fp64 p9 721 -> 634 us; fp64 p7 slower, 226 -> 240 us, so not there); with the staged geometric
+    // factors (AxCfg::GSTAGE_AX: one TMA bulk copy per element, as in the solve's phase A) only u
+    constexpr bool GS = C::GSTAGE_AX;
     constexpr bool PF = NB_L2PF_AX && !(sizeof(TV) == 8 && N == 8);
-    if (PF) pf_group<TV, N, C::EPB, 3>(g0, g1, m.E, g, in, nullptr, nullptr, 0);
+    constexpr int PFM = GS ? 2 : 3;
+    __shared__ GStage gsh;
+    TV *const gst = GS ? reinterpret_cast<TV *>(smraw + C::SMEM + (el < C::EPB ? el : 0) * C::GSB_AX) : nullptr;
+    if constexpr (GS) {
+        if (tid < 4) {
+            mbar_init(&gsh.bar[tid], 1);
+            gsh.par[tid] = 0;
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        const int e0 = (int)(g0 * C::EPB) + el;
+        if (g0 < g1 && el < C::EPB && q == 0 && e0 < m.E) gstage_issue<TV, N>(g, e0, gst, &gsh.bar[el]);
+    }
+    if (PF) pf_group<TV, N, C::EPB, PFM>(g0, g1, m.E, g, in, nullptr, nullptr, 0);
 #pragma unroll 1
     for (int64_t gr = g0; gr < g1; gr++) {
-        if (PF) pf_group<TV, N, C::EPB, 3>(gr + 1, g1, m.E, g, in, nullptr, nullptr, 0);
+        if (PF) pf_group<TV, N, C::EPB, PFM>(gr + 1, g1, m.E, g, in, nullptr, nullptr, 0);
         const int e = (int)(gr * C::EPB) + el;
         const bool active = el < C::EPB && (C::N2P == C::N2 || C::HALF || q < C::N2) && e < m.E;
+        const int en = (GS && gr + 1 < g1 && e + C::EPB < m.E) ? e + C::EPB : -1;
         // the handle may be a z-slab (global mask layers): SLAB = true
         if constexpr (C::HALF)
             ax_group_half<PREC, N, 0, true>(m, D, in, nullptr, nullptr, g, w, apply_mask != 0, TV(0), TV(0), e, active,
                                             a, b, h, S0);
         else
-            ax_group<PREC, N, 0, true>(m, D, in, nullptr, nullptr, g, w, apply_mask != 0, TV(0), TV(0), e, active, a, b,
-                                       S0);
+            ax_group<PREC, N, 0, true, GS>(m, D, in, nullptr, nullptr, g, w, apply_mask != 0, TV(0), TV(0), e, active, a, b,
+                                           S0, nullptr, 0.0, gst, en, &gsh, el < C::EPB ? el : 0);
     }
 }
 
@@ -1401,9 +1414,9 @@ static int ax_grid_t(const nb_handle *h)
     static DevCache cache;
     int &occ = cache.here();
     if (occ < 0) {
-        cudaFuncSetAttribute(k_ax<PREC, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(k_ax<PREC, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_AX);
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_ax<PREC, N>, C::NT, C::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_ax<PREC, N>, C::NT, C::SMEM_AX);
         occ = o > 0 ? o : 1;
     }
     const int64_t ngroups = (h->E + C::EPB - 1) / C::EPB;
@@ -1419,7 +1432,7 @@ static cudaError_t ax_launch_t(const nb_handle *h, const void *in, void *w, int 
     using C = AxCfg<TV, N>;
     const int grid = ax_grid_t<PREC, N>(h);
     const TV *g = (const TV *)(sizeof(TV) == 8 ? (const void *)h->g64 : (const void *)h->g32);
-    k_ax<PREC, N><<<grid, C::NT, C::SMEM, st>>>(h->md(), make_dmat<TV, N>(h->D), (const TV *)in, g, (TV *)w,
+    k_ax<PREC, N><<<grid, C::NT, C::SMEM_AX, st>>>(h->md(), make_dmat<TV, N>(h->D), (const TV *)in, g, (TV *)w,
                                                 apply_mask);
     return cudaGetLastError();
 }
