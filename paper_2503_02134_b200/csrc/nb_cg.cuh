@@ -94,7 +94,19 @@ template <typename T, int N> struct AxCfg {
 #ifndef NB_E1_D10
 #define NB_E1_D10 2
 #endif
-    static constexpr bool E1D = NB_E1_D10 && sizeof(T) == 8 && N == 10 && !HALF;
+    // Single precision N = 10 the same way with NB_E1_S10 resident blocks -- set to 3 by the MIXED
+    // policy's translation units only (nb_cg_mixed.cu, nb_cg_mixed_var.cu): 12 warps at 168 registers
+    // and 122 KB of shared memory per SM instead of 14 warps at 128 registers and 163 KB leave phase B
+    // more L1 and registers (32^3 p9 mixed: phase B 208 -> 187 us, iteration 496 -> 476 us; 20^3 -7%,
+    // 50^3 -6%).  The fp32 policy measured 3% slower with it (its phase B has no fp64 diagonal and
+    // sums), so AxCfg<float, 10> deliberately differs between the mixed and the fp32 / Dot2 / Schwarz
+    // translation units: every use is a compile-time constant inside one unit (the library exports
+    // no AxCfg symbol, device code is per unit), and the workspace is sized by the policy's largest grid.
+#ifndef NB_E1_S10
+#define NB_E1_S10 0
+#endif
+    static constexpr bool E1S = NB_E1_S10 && sizeof(T) == 4 && N == 10 && !HALF && !(NB_PAD_ELEM);
+    static constexpr bool E1D = (NB_E1_D10 && sizeof(T) == 8 && N == 10 && !HALF) || E1S;
     static constexpr int EPB = E1D ? 1 : (N2P >= 256) ? 1 : (256 / N2P);  // elements per group
     static constexpr int NT = ((EPB * N2P + 31) / 32) * 32;     // threads per block
     static constexpr int SMEM = NARR * EPB * ESZ * (int)sizeof(T);
@@ -158,7 +170,7 @@ template <typename T, int N> struct AxCfg {
 #ifndef NB_MINB_D
 #define NB_MINB_D 1
 #endif
-    static constexpr int MINB = E1D ? NB_E1_D10 : (NB_MINB_D && sizeof(T) == 8 && N == 10) ? NB_MINB_D
+    static constexpr int MINB = E1S ? NB_E1_S10 : E1D ? NB_E1_D10 : (NB_MINB_D && sizeof(T) == 8 && N == 10) ? NB_MINB_D
                               : (NB_MINB_N12 && N == 12 && sizeof(T) == 4) ? NB_MINB_N12
                               : NB_MINB_MODE == 0 ? 1
                               : NB_MINB_MODE == 3 ? ((sizeof(T) == 4) ? (NT <= 128 ? 4 : 2) : (N <= 8 && !HALF ? 1 : 2))

@@ -1,5 +1,7 @@
 // nb_cg_mixed_var.cu -- the mixed policy's megakernels for the preconditioner / x_fp64 variants
 // (VAR = 1), in their own translation unit so the build runs in parallel.
+// mixed policy, N = 10: one element per 128-thread block, three resident blocks (AxCfg::E1S, nb_cg.cuh)
+#define NB_E1_S10 3
 #include "nb_mega_launch.cuh"
 
 namespace nb {
